@@ -1,0 +1,486 @@
+#!/usr/bin/env python3
+"""HCNN encrypted-batch benchmark on B200 (BASELINE.json metric).
+
+Workload (default): the MNIST HCNN (conv-square-conv-square-fc, nn_oracle.py:
+108-126) at the paper's >80-bit parameter set 1 (N = 2^13, 11 x 30-bit primes,
+log q = 330, t = 5522259017729, presets.py:62-69), ONE full slot-batch of 8192
+synthetic 28x28 images (scale-4 pixels), dense random 4-bit weights (every tap
+executes).  One step = one homomorphic evaluation of the whole network over
+the batch (engine.eval_network), 1520 HSquares + 46,000 plaintext MACs.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Multi-GPU (torchrun, one process per GPU): every rank evaluates its own
+independent slot-batch (weak scaling); the logit ciphertexts are gathered to
+rank 0 with NCCL at the end of each step (the final-gather step of the
+pipeline).  `value` = images of all ranks / max-over-ranks step time.
+
+`--impl reference` times the reference algorithm on the host CPU (the pinned
+oracle port in oracle/, all host cores) on a bounded sample and extrapolates
+to the same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "HCNN encrypted-batch latency (s) and images/s, MNIST/CIFAR-10, at 1/2/4/8 B200"
+SET1_PRIMES = (1073643521, 1073479681, 1073184769, 1073053697, 1072857089, 1072496641,
+               1071513601, 1071415297, 1071087617, 1070727169, 1070432257)
+MNIST_T = 5522259017729
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--seed", type=int, default=2024)
+    ap.add_argument("--profile-only", action="store_true", help="one step, no timing (for ncu)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- workload
+
+
+def build_workload(rank: int, seed: int):
+    from paper_1811_00778_b200 import bfv as B
+    from paper_1811_00778_b200 import engine as E
+    from paper_1811_00778_b200 import nn
+
+    n = 8192
+    params = B.BfvParams(B.RnsContext(n, SET1_PRIMES), MNIST_T)
+    sk, pk, rlk = B.keygen(params, np.random.default_rng(seed))
+    model = nn.random_model(nn.mnist_hcnn(), np.random.default_rng(seed + 1))
+    irng = np.random.default_rng(seed + 100 + rank)
+    images = list(irng.integers(0, 5, (n, 28, 28, 1)))
+    enc = B.SlotEncoder(MNIST_T, n)
+    t0 = time.time()
+    gin = E.pack_images_device(images, E.PackingLayout(n, n), enc, pk, params,
+                               np.random.default_rng(seed + 200 + rank), delta=4)
+    setup_s = time.time() - t0
+    return dict(params=params, sk=sk, pk=pk, rlk=rlk, model=model, images=images, enc=enc,
+                gin=gin, setup_s=setup_s)
+
+
+# ---------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi style sampling through NVML during the timed region."""
+
+    def __init__(self, index: int):
+        self.samples = []
+        self.reasons = set()
+        self._stop = threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except Exception:
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.th = threading.Thread(target=self._run, daemon=True)
+            self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.th.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- work model
+
+
+def kernel_work(name: str, K: int, KP: int, D: int, N: int, per_launch_cts: float):
+    """Algorithmic (bytes, IMAD-equivalents) of one launch of a hot kernel.
+
+    IMAD-equivalents count 3 per Shoup/Barrett modular multiply (NTT
+    butterfly, pointwise product) and 1 per lazy 64-bit multiply-accumulate;
+    bytes are the compulsory HBM reads + writes of the kernel's operands
+    (u32 residues, each touched once).  DESIGN.md section 4 derives them.
+    """
+    logn = N.bit_length() - 1
+    bfly = (N // 2) * logn
+    L = K + KP
+    if name == "k_tensor":  # per ct: 2 fwd + 3 inv NTT per prime, 3 products + N^-1
+        imad = L * (5 * bfly * 3 + 3 * N * 3 + 3 * N * 3)
+        byts = L * N * 4 * (2 + 3)
+    elif name == "k_relin":  # per ct: D fwd + 2 inv NTT per prime, 2D MACs per coeff
+        imad = K * ((D + 2) * bfly * 3 + 2 * D * N + 2 * N * 3)
+        byts = 4 * N * (D + 2 * D * K + 2 * K + 2 * K)
+    elif name == "k_scale":  # per ct: 3 parts x (K + KP(K+2) + KP K) MACs + digits
+        imad = 3 * N * (K * 3 + KP * (K + 2 * 3 + 3) + K * KP) + N * (K * 3 + K * (K + 1) + 2 * K)
+        byts = 4 * N * (3 * L + 3 * K + D)
+    elif name == "k_extend":  # per ct: 2 parts x (K Shoup + K*KP MACs + fixed point)
+        imad = 2 * N * (K * 3 + K * KP + KP * 3 + 2 * K)
+        byts = 4 * N * 2 * (K + KP)
+    elif name in ("k_conv", "k_fc"):
+        return None
+    else:
+        return None
+    return byts * per_launch_cts, imad * per_launch_cts
+
+
+# ---------------------------------------------------------------- our arm
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1811_00778_b200 import _lib
+    from paper_1811_00778_b200 import engine as E
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    W = build_workload(rank, args.seed)
+    params, rlk, model, gin = W["params"], W["rlk"], W["model"], W["gin"]
+    g = E.context_for(params)
+
+    def step(x):
+        counter = E.OpCounter()
+        out = E.eval_network(x, model, rlk, params, counter)
+        if world > 1:
+            buf = [torch.empty_like(out.data) for _ in range(world)] if rank == 0 else None
+            dist.gather(out.data, buf, dst=0)
+        return out, counter
+
+    if args.profile_only:
+        step(gin)
+        torch.cuda.synchronize()
+        return
+
+    for _ in range(max(args.warmup, 0)):
+        out, counter = step(gin)
+    torch.cuda.synchronize()
+
+    # ---- timed region (device resident inputs; 565 MB > L2 per step)
+    stream = torch.cuda.current_stream()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    L = _lib.lib()
+    _lib.check(L.hcnn_profile(g.handle, 1))
+    launches0 = g.launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            out, counter = step(gin)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = g.launches() - launches0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    buf = __import__("ctypes").create_string_buffer(1 << 16)
+    L.hcnn_profile_dump(g.handle, buf, len(buf))
+    _lib.check(L.hcnn_profile(g.handle, 0))
+    prof = {}
+    for line in buf.value.decode().splitlines():
+        name, cnt, tot = line.split()
+        prof[name] = (int(cnt), float(tot))
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- end to end through the public API: pinned host u32 ciphertexts in,
+    # logits out, copies inside the timed region
+    host_in = torch.empty(gin.data.shape, dtype=torch.int32, pin_memory=True)
+    host_in.copy_(gin.data)
+    host_out = torch.empty((10, 2, g.K, g.N), dtype=torch.int32, pin_memory=True)
+    e2e_steps = max(2, min(args.steps, 5))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        x = E.GpuCipherTensor(gin.shape, host_in.to("cuda", non_blocking=True), gin.delta,
+                              gin.channel_modulus, params)
+        o, _ = step(x)
+        host_out.copy_(o.data, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    wall_e2e = (time.perf_counter() - w0) / e2e_steps
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_src = "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback"
+    imad = __import__("ctypes").c_double()
+    _lib.check(L.hcnn_int_peak(local, 0, __import__("ctypes").byref(imad)))
+    imad_peak = imad.value / 1e12
+    total_ms = sum(v[1] for v in prof.values())
+    dom = max(prof, key=lambda k: prof[k][1]) if prof else None
+    roof = None
+    kernels = {}
+    for name, (cnt, tot) in prof.items():
+        kernels[name] = {"launches": cnt, "ms_total": round(tot, 4), "share": round(tot / total_ms, 4)}
+    if dom:
+        cnt, tot = prof[dom]
+        # cts processed by this kernel over the timed region
+        n_sq = counter.hsquare * args.steps
+        work = kernel_work(dom, g.K, g.KP, g.D, g.N, n_sq / cnt)
+        avg_s = tot / cnt / 1e3
+        if work:
+            byts, ops = work
+            gbs = byts / avg_s / 1e9
+            tops = ops / avg_s / 1e12
+            hbm_frac = gbs / hbm_peak
+            int_frac = tops / imad_peak
+            traffic = None
+            try:
+                with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+                    traffic = json.load(fh).get(dom)
+                    traffic = traffic * (n_sq / cnt) if traffic else None
+            except Exception:
+                pass
+            int_bound = int_frac >= hbm_frac
+            roof = {
+                "kernel": dom,
+                "bound": "int" if int_bound else "hbm",
+                "achieved": round(tops if int_bound else gbs, 3),
+                "peak": round(imad_peak if int_bound else hbm_peak, 3),
+                "unit": "TIMAD/s" if int_bound else "GB/s",
+                "frac": round(int_frac if int_bound else hbm_frac, 4),
+                "traffic": traffic,
+                "hbm": {"achieved_gbs": round(gbs, 1), "peak_gbs": hbm_peak, "frac": round(hbm_frac, 4),
+                        "peak_source": hbm_src, "algorithmic_bytes_per_launch": byts},
+                "int": {"achieved_timad_s": round(tops, 3), "peak_timad_s": round(imad_peak, 3),
+                        "frac": round(int_frac, 4), "peak_source": "measured in bench.py (hcnn_int_peak IMAD probe)",
+                        "imad_equiv_per_launch": ops},
+                "avg_launch_ms": round(avg_s * 1e3, 4),
+                "share_of_step": round(tot / total_ms, 4),
+            }
+
+    images = 8192 * world
+    value = images / (ms / 1e3)
+    in_bytes = int(host_in.numel() * 4)
+    out_bytes = int(host_out.numel() * 4)
+    line = {
+        "metric": METRIC,
+        "value": round(value, 2),
+        "unit": "images/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 4),
+        "latency_s": round(ms / 1e3, 6),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u32",
+        "data": "synthetic",
+        "config": {
+            "workload": "MNIST HCNN, preset 1 (N=8192, 11x30-bit primes, log q 330, t=5522259017729), one 8192-image slot-batch per GPU",
+            "model": "mnist_hcnn conv5x5s2(5)-square-conv5x5s2(50,g5)-square-fc10, dense random 4-bit weights",
+            "global_batch": images,
+            "parallelism": f"replicas{world}" if world > 1 else "single",
+            "hsquare_per_step": counter.hsquare,
+            "mult_plain_per_step": counter.mult_plain_scheduled,
+            "l2_policy": "inputs 565 MB per GPU > 126 MB L2 (no flush needed)",
+            "setup_s": round(W["setup_s"], 2),
+        },
+        "e2e": {"value": round(images / (e2e_ms / 1e3), 2), "unit": "images/s",
+                "ms_per_step": round(e2e_ms, 3), "wall_ms_per_step": round(wall_e2e * 1e3, 3),
+                "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": out_bytes,
+                "path": "pinned host u32 ciphertexts -> engine.eval_network -> pinned host logits"},
+        "gpu_launches": int(launches),
+        "kernels": kernels,
+        "roofline": roof,
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_sample(W, threads=1)
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- CPU arms
+
+
+def _oracle_inputs(W):
+    """one ciphertext + rlk of the workload as numpy, for the oracle port"""
+    import hcnn_oracle as O
+
+    params = W["params"]
+    op = O.Params(O.Context(params.ring_degree, SET1_PRIMES), params.t)
+    rlk = [(k0.residues, k1.residues) for k0, k1 in W["rlk"].components]
+    x = W["gin"].data[:1].cpu().numpy().view(np.uint32).astype(np.int64)[0]
+    return op, rlk, (x[0], x[1])
+
+
+def _hsq_time(op, rlk, ct):
+    import hcnn_oracle as O
+
+    t0 = time.perf_counter()
+    O.hsquare(op, ct, rlk)
+    return time.perf_counter() - t0
+
+
+def _ws_time(op, ct, taps):
+    import hcnn_oracle as O
+
+    t0 = time.perf_counter()
+    O.weighted_sum(op, [(ct, 3)] * taps, O.Counter())
+    return time.perf_counter() - t0
+
+
+def _extrapolate(t_hsq, t_ws25, t_ws800):
+    # MNIST: conv1 720 outputs x 25 taps, 720 HSquare, conv2 800 x 25, 800 HSquare, fc 10 x 800
+    return 1520 * t_hsq + 1520 * t_ws25 + 10 * t_ws800
+
+
+def cpu_baseline_sample(W, threads: int = 1):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    op, rlk, ct = _oracle_inputs(W)
+    t_hsq = _hsq_time(op, rlk, ct)
+    t_ws25 = _ws_time(op, ct, 25)
+    t_ws800 = _ws_time(op, ct, 800)
+    T = _extrapolate(t_hsq, t_ws25, t_ws800)
+    return {"value": round(8192 / T, 4), "unit": "images/s", "cores": threads, "kind": "port",
+            "latency_s_extrapolated": round(T, 1),
+            "sample": f"oracle port (oracle/hcnn_oracle.py, same algorithm as hefir: exact CRT lift + "
+                      f"Kronecker big-int tensor) at N=8192/set 1: 1 HSquare ({t_hsq:.2f}s) + one 25-tap and "
+                      f"one 800-tap weighted sum, extrapolated x1520 HSquare / 1520 25-tap / 10 800-tap"}
+
+
+def _worker_hsq(args):
+    op, rlk, ct = args
+    return _hsq_time(op, rlk, ct)
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import hcnn_oracle as O
+    from paper_1811_00778_b200 import bfv as B
+
+    n = 8192
+    params = B.BfvParams(B.RnsContext(n, SET1_PRIMES), MNIST_T)
+    sk, pk, rlk = B.keygen(params, np.random.default_rng(args.seed))
+    erng = np.random.default_rng(args.seed + 5)
+    c = B.encrypt(pk, B.Plaintext(erng.integers(0, MNIST_T, n), MNIST_T), params, erng)
+    op = O.Params(O.Context(n, SET1_PRIMES), MNIST_T)
+    orlk = [(k0.residues, k1.residues) for k0, k1 in rlk.components]
+    ct = (c.parts[0].residues, c.parts[1].residues)
+    cores = os.cpu_count() or 1
+    t_ws25 = _ws_time(op, ct, 25)
+    t_ws800 = _ws_time(op, ct, 800)
+    ctxm = mp.get_context("fork")
+    vals = []
+    with ctxm.Pool(cores) as pool:
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            pool.map(_worker_hsq, [(op, orlk, ct)] * cores)
+            wall = time.perf_counter() - t0
+            if i >= args.warmup:
+                vals.append(wall)
+    wall = float(np.mean(vals))
+    # `cores` HSquares per `wall` seconds; MACs parallelise the same way
+    T = (1520 * wall / cores) + (1520 * t_ws25 + 10 * t_ws800) / cores
+    value = 8192 / T
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": "images/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(T * 1e3, 1),
+        "latency_s": round(T, 2), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int (Python big int / int64)", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": "MNIST HCNN, preset 1 (N=8192, 11 primes, t=5522259017729), one 8192-image slot-batch",
+                   "parallelism": f"{cores} host processes"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "images/s", "cores": cores, "kind": "port",
+                         "sample": f"per step: {cores} HSquares in parallel (one per core, oracle port of "
+                                   f"hefir's exact Kronecker path) at N=8192/set 1, mean wall {wall:.2f}s; plus "
+                                   f"25/800-tap weighted sums; extrapolated to 1520 HSquare + 46,000 MACs"},
+        "e2e": {"value": round(value, 4), "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,141 @@
+/* hcnn_b200.h — C ABI of the B200 backend for HCNN's homomorphic-evaluation
+ * hot path (RNS-BFV over Z_q[X]/(X^N+1), exact FV scaling, base-w relin).
+ *
+ * The reference (hefir, pure Python) has no FFI; its seam is the Python layer
+ * API of engine.py / bfv.py.  Each entry point below replaces one reference
+ * function; the Python mirror (paper_1811_00778_b200/engine.py) binds them
+ * with ctypes behind the reference's own signatures.
+ *
+ * Conventions
+ *   - Ciphertext tensors live in device memory as u32 residues, limb-major:
+ *     [ct][part][limb][N] (parts = 2, or 3 for a raw product).  Residues are
+ *     canonical [0, p_i), coefficient domain, exactly the reference's
+ *     RingElem.residues (ring.py:98-112) narrowed from int64.
+ *   - Device pointers are plain pointers (the caller may allocate them with
+ *     hcnn_alloc or with any CUDA allocator, e.g. torch's).  All work is
+ *     enqueued on the context's stream; call hcnn_sync to wait.
+ *   - Every function returns 0 on success or an HCNN_ERR_* code;
+ *     hcnn_last_error() gives the message (thread-local).  The codes map onto
+ *     the reference's exception hierarchy (errors.py:4-54).
+ */
+#ifndef HCNN_B200_H
+#define HCNN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  HCNN_OK = 0,
+  HCNN_ERR_PARAM = 1,       /* ParameterMismatchError (bfv.py:146-148, engine.py:248-251) */
+  HCNN_ERR_MISSING_KEY = 2, /* MissingKeyError (bfv.py:370-371, 437-438) */
+  HCNN_ERR_CAPACITY = 3,    /* CapacityError (engine.py:109-112) */
+  HCNN_ERR_UNSUPPORTED = 4, /* UnsupportedParametersError (presets.py:72-88) */
+  HCNN_ERR_CUDA = 5,        /* device / runtime failure */
+  HCNN_ERR_DOMAIN = 6       /* DomainError (ring.py:147-163) */
+};
+
+enum { HCNN_DOMAIN_COEFF = 0, HCNN_DOMAIN_REF_NTT = 1 };
+
+typedef struct hcnn_ctx hcnn_ctx;
+
+/* Context for one BFV parameter set (one plaintext-CRT channel t).
+ * Replaces RnsContext + NttPlan + BfvParams construction
+ * (ring.py:51-95, ntt.py:88-108, bfv.py:45-91, presets.py:145-162).
+ * primes: k RNS primes of q (< 2^30, = 1 mod 2n); log2w in {8, 16, 32}. */
+int hcnn_ctx_create(hcnn_ctx** out, uint32_t n, uint32_t k, const uint64_t* primes, uint64_t t,
+                    uint32_t log2w, int device);
+int hcnn_ctx_destroy(hcnn_ctx* ctx);
+/* stream: a cudaStream_t to enqueue on (NULL = the legacy default stream);
+ * until this is called the context uses a private non-blocking stream. */
+int hcnn_ctx_set_stream(hcnn_ctx* ctx, void* stream);
+/* HCNN_Q_*: query context properties */
+enum {
+  HCNN_Q_N = 0,
+  HCNN_Q_K = 1,
+  HCNN_Q_KP = 2,       /* primes of the auxiliary base P */
+  HCNN_Q_DIGITS = 3,   /* l + 1 relinearisation digits (bfv.py:70-76) */
+  HCNN_Q_LOG2W = 4,
+  HCNN_Q_WS_BYTES = 5, /* workspace currently held */
+  HCNN_Q_KERNELS = 6   /* kernels launched since creation */
+};
+int64_t hcnn_ctx_query(hcnn_ctx* ctx, int what);
+/* psi (primitive 2N-th root) of prime i, i < K + KP (ntt.py:50-60) */
+uint64_t hcnn_ctx_prime(hcnn_ctx* ctx, int i, uint64_t* psi);
+/* upper bound on the workspace the context may hold (default 2 GiB) */
+int hcnn_ctx_set_workspace_limit(hcnn_ctx* ctx, size_t bytes);
+
+/* Relinearisation key, host u64 [digits][2][K][N] (RelinKey.components,
+ * bfv.py:129-133, 177-187).  domain: HCNN_DOMAIN_REF_NTT for the in-memory
+ * reference keys (natural-order NTT), HCNN_DOMAIN_COEFF for serialised ones
+ * (serial.py:87-90, 171-187). */
+int hcnn_set_relin_key(hcnn_ctx* ctx, const uint64_t* rlk, int domain);
+
+/* Public key, host u64 [2][K][N] (PublicKey b_ntt, a_ntt; bfv.py:122-126). */
+int hcnn_set_public_key(hcnn_ctx* ctx, const uint64_t* pk, int domain);
+/* Client-side encryption of n plaintext polys with host-drawn randomness
+ * (bfv.py:201-216): u [n][N] in {0,1}, e1/e2 [n][N] in [-19,19], msg [n][N]
+ * in [0,t) (all host), out: device [n][2][K][N]. */
+int hcnn_encrypt(hcnn_ctx* ctx, const int8_t* u, const int8_t* e1, const int8_t* e2,
+                 const int64_t* msg, uint32_t* out, size_t n);
+
+/* Device memory helpers (stream-ordered). */
+int hcnn_alloc(hcnn_ctx* ctx, size_t bytes, void** out);
+int hcnn_free(hcnn_ctx* ctx, void* ptr);
+/* host int64/u64 residues -> device u32 (count residues), and back */
+int hcnn_upload_u64(hcnn_ctx* ctx, uint32_t* dst, const uint64_t* src, size_t count);
+int hcnn_download_u64(hcnn_ctx* ctx, uint64_t* dst, const uint32_t* src, size_t count);
+int hcnn_sync(hcnn_ctx* ctx);
+
+/* Weights (host int64, any sign) reduced per prime of q into device
+ * out[count][K] (the per-prime reduction of ring.accumulate_scaled,
+ * ring.py:199-207 / RnsContext.reduce_scalar, ring.py:91-95). */
+int hcnn_reduce_weights(hcnn_ctx* ctx, const int64_t* w, size_t count, uint32_t* out);
+
+/* Convolution layer: engine.eval_conv (engine.py:237-303).
+ * in: h*w*c cts, (y,x,c) row-major; weights wred [f][kh][kw][c/groups][K]. */
+int hcnn_conv(hcnn_ctx* ctx, const uint32_t* in, uint32_t* out, int h, int w, int c,
+              const uint32_t* wred, int f, int kh, int kw, int sh, int sw, int padded, int groups);
+/* Dense layer: engine.eval_fc (engine.py:306-334); wred [n_out][n_in][K]. */
+int hcnn_fc(hcnn_ctx* ctx, const uint32_t* in, uint32_t* out, int n_in, int n_out,
+            const uint32_t* wred);
+/* Sum-pool layer: engine.eval_pool (engine.py:367-397). */
+int hcnn_pool(hcnn_ctx* ctx, const uint32_t* in, uint32_t* out, int h, int w, int c, int extent,
+              int sh, int sw);
+/* Square activation over n cts: engine.eval_square / bfv.hsquare
+ * (engine.py:337-364, bfv.py:435-443). */
+int hcnn_square(hcnn_ctx* ctx, const uint32_t* in, uint32_t* out, size_t n);
+/* 3-part scaled tensor: bfv.hmult_raw (bfv.py:407-416); b may equal a. */
+int hcnn_hmult_raw(hcnn_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out3, size_t n);
+/* ct x ct multiply + relinearise: bfv.hmult (bfv.py:419-432). */
+int hcnn_hmult(hcnn_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, size_t n);
+/* 3-part -> 2-part key switch: bfv.relinearize (bfv.py:368-404). */
+int hcnn_relinearize(hcnn_ctx* ctx, const uint32_t* in3, uint32_t* out, size_t n);
+/* Elementwise add of two ct tensors: bfv.hadd (bfv.py:264-274). */
+int hcnn_hadd(hcnn_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, size_t n);
+/* In-place NTT of n_rows rows of N residues; row r uses prime
+ * prime_offset + r % limbs (indices over Q then P).  inverse = 0 forward.
+ * Device spectral order: dev[i] = ref[brv(i)] (ring.py:147-163). */
+int hcnn_ntt(hcnn_ctx* ctx, uint32_t* rows, size_t n_rows, uint32_t limbs, uint32_t prime_offset,
+             int inverse);
+
+/* Per-kernel CUDA-event timing on the context's stream.  hcnn_profile(ctx, 1)
+ * resets and starts recording; hcnn_profile_dump writes "name count total_ms"
+ * lines (returns the text length, or -status). */
+int hcnn_profile(hcnn_ctx* ctx, int enable);
+int64_t hcnn_profile_dump(hcnn_ctx* ctx, char* buf, size_t len);
+
+/* Integer-pipe probe (roofline denominator): kind 0 = 32-bit IMAD,
+ * 1 = IMAD.HI (umulhi), 2 = IMAD.WIDE (32x32->64); ops per second. */
+int hcnn_int_peak(int device, int kind, double* ops_per_s);
+
+const char* hcnn_last_error(void);
+const char* hcnn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HCNN_B200_H */

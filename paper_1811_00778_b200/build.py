@@ -1,0 +1,73 @@
+"""Build libhcnn_b200.so in-tree for sm_100a (nvcc; one object per ring degree).
+
+    python -m paper_1811_00778_b200.build [--force] [-j N]
+"""
+
+from __future__ import annotations
+
+import argparse
+import concurrent.futures
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(PKG, "csrc")
+BUILD = os.path.join(os.path.dirname(PKG), "build", "hcnn")
+LIB = os.path.join(PKG, "libhcnn_b200.so")
+LOGNS = list(range(2, 16))
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
+]
+
+
+def _sources():
+    return [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [
+        os.path.join(os.path.dirname(PKG), "include", "hcnn_b200.h")
+    ]
+
+
+def _newest_source() -> float:
+    return max(os.path.getmtime(p) for p in _sources())
+
+
+def _compile(args):
+    src, obj, defs = args
+    cmd = [NVCC, *FLAGS, *defs, "-c", src, "-o", obj]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {os.path.basename(obj)}:\n{r.stderr[-4000:]}")
+    return obj
+
+
+def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> str:
+    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _newest_source():
+        return LIB
+    os.makedirs(BUILD, exist_ok=True)
+    units = [(os.path.join(CSRC, "hcnn.cu"), os.path.join(BUILD, "hcnn.o"), [])]
+    for L in LOGNS:
+        units.append((os.path.join(CSRC, "ntt_inst.cu"), os.path.join(BUILD, f"ntt_{L}.o"),
+                      [f"-DHCNN_LOGN={L}"]))
+    # biggest units first
+    units.sort(key=lambda u: -int(u[2][0].split("=")[1]) if u[2] else -99)
+    jobs = jobs or os.cpu_count() or 4
+    with concurrent.futures.ThreadPoolExecutor(jobs) as ex:
+        objs = list(ex.map(_compile, units))
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *objs]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
+    if verbose:
+        print(f"built {LIB}")
+    return LIB
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-j", type=int, default=None)
+    a = ap.parse_args()
+    build(force=a.force, jobs=a.j, verbose=True)
+    sys.exit(0)

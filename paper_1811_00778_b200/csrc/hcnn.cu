@@ -1,0 +1,935 @@
+// Context, dispatch and the exported C ABI (include/hcnn_b200.h).
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/hcnn_b200.h"
+#include "kernels.cuh"
+#include "ntt_kernels.cuh"
+#include "tables.hpp"
+
+using namespace hcnn;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Error{HCNN_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+#define CK(x) check_cuda((x), #x)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return HCNN_OK;
+  } catch (const Error& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HCNN_ERR_UNSUPPORTED;
+  }
+}
+
+void fail(int code, const std::string& m) { throw Error{code, m}; }
+
+}  // namespace
+
+struct hcnn_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  uint32_t N = 0, logN = 0, K = 0, KP = 0, D = 0, log2w = 0;
+  uint64_t t = 0;
+  std::vector<u64> primes;  // Q then P
+  std::vector<u64> psi;
+  ConvTabs tabs{};
+  NttTabs nt{};
+  uint32_t* d_prime = nullptr;
+  uint64_t* d_mu = nullptr;
+  uint2* d_tw = nullptr;
+  uint2* d_itw = nullptr;
+  uint2* d_ninv = nullptr;
+  uint32_t* d_rlk = nullptr;
+  uint32_t* d_pk = nullptr;
+  uint2* d_delta = nullptr;
+  bool rlk_reduce = false;
+  uint8_t* ws = nullptr;
+  size_t ws_bytes = 0;
+  size_t ws_limit = size_t(2) << 30;
+  int64_t launches = 0;
+
+  uint8_t* workspace(size_t bytes) {
+    if (bytes > ws_bytes) {
+      if (ws) CK(cudaFreeAsync(ws, stream));
+      ws = nullptr;
+      ws_bytes = 0;
+      CK(cudaMallocAsync((void**)&ws, bytes, stream));
+      ws_bytes = bytes;
+    }
+    return ws;
+  }
+  // per-launch CUDA events on the launching stream (hcnn_profile): kernel i
+  // spans [event after launch i-1 (or the call's mark), event after launch i]
+  struct ProfRec {
+    const char* name;
+    cudaEvent_t a, b;
+  };
+  bool prof = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> ev_pool, ev_used;
+  cudaEvent_t last_ev = nullptr;
+  cudaEvent_t new_event() {
+    cudaEvent_t e;
+    if (ev_pool.empty()) {
+      CK(cudaEventCreate(&e));
+    } else {
+      e = ev_pool.back();
+      ev_pool.pop_back();
+    }
+    ev_used.push_back(e);
+    return e;
+  }
+  void mark() {
+    if (!prof) return;
+    last_ev = new_event();
+    CK(cudaEventRecord(last_ev, stream));
+  }
+  void launched(const char* what) {
+    ++launches;
+    check_cuda(cudaGetLastError(), what);
+    if (prof) {
+      if (!last_ev) mark();
+      cudaEvent_t e = new_event();
+      CK(cudaEventRecord(e, stream));
+      recs.push_back({what, last_ev, e});
+      last_ev = e;
+    }
+  }
+  void prof_reset() {
+    for (auto e : ev_used) ev_pool.push_back(e);
+    ev_used.clear();
+    recs.clear();
+    last_ev = nullptr;
+  }
+};
+
+namespace {
+
+void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
+  const uint32_t N = c->N;
+  // q, h = (q-1)/2, relin digit count l+1 (bfv.py:68-76)
+  Big Q = product(q);
+  {
+    Big acc(1);
+    for (uint32_t i = 0; i < c->log2w; ++i) acc = mul_small(acc, 2);
+    Big wpow = acc;
+    uint32_t l = 0;
+    while (cmp(wpow, Q) <= 0) {
+      for (uint32_t i = 0; i < c->log2w; ++i) wpow = mul_small(wpow, 2);
+      ++l;
+    }
+    c->D = l + 1;
+  }
+  if (c->D > (uint32_t)DMAX) fail(HCNN_ERR_UNSUPPORTED, "too many relinearisation digits");
+  // auxiliary base: P > 8 t N q + 4 so that round(t d / q) is centred in P
+  // with |y| < P/4 (exact rounding, no ambiguity)
+  Big bound = mul_small(mul_small(mul_small(Q, t), N), 8);
+  bound = add(bound, Big(4));
+  std::vector<u64> P;
+  Big Pp(1);
+  {
+    std::vector<u64> cand = aux_primes(q, KPMAX + 1);
+    for (u64 p : cand) {
+      if (cmp(Pp, bound) > 0) break;
+      P.push_back(p);
+      Pp = mul_small(Pp, p);
+    }
+    if (cmp(Pp, bound) <= 0 || P.size() > (size_t)KPMAX)
+      fail(HCNN_ERR_UNSUPPORTED, "auxiliary base would need more than 16 primes");
+  }
+  c->KP = (uint32_t)P.size();
+  c->primes = q;
+  c->primes.insert(c->primes.end(), P.begin(), P.end());
+  const uint32_t L = c->K + c->KP;
+
+  // NTT tables
+  std::vector<uint32_t> hp(L);
+  std::vector<uint64_t> hmu(L);
+  std::vector<uint2> htw((size_t)L * N), hitw((size_t)L * N), hninv(L);
+  c->psi.resize(L);
+  for (uint32_t j = 0; j < L; ++j) {
+    const u64 p = c->primes[j];
+    const u64 psi = primitive_2n_root(p, N);
+    const u64 ipsi = invmod64(psi, p);
+    c->psi[j] = psi;
+    hp[j] = (uint32_t)p;
+    hmu[j] = (uint64_t)(((u128)1 << 64) / p);
+    std::vector<u64> pw(N), ipw(N);
+    pw[0] = ipw[0] = 1;
+    for (uint32_t i = 1; i < N; ++i) {
+      pw[i] = mulmod64(pw[i - 1], psi, p);
+      ipw[i] = mulmod64(ipw[i - 1], ipsi, p);
+    }
+    for (uint32_t i = 0; i < N; ++i) {
+      const uint32_t r = bitrev(i, c->logN);
+      htw[(size_t)j * N + i] = make_uint2((uint32_t)pw[r], shoup_of((uint32_t)pw[r], (uint32_t)p));
+      hitw[(size_t)j * N + i] = make_uint2((uint32_t)ipw[r], shoup_of((uint32_t)ipw[r], (uint32_t)p));
+    }
+    const uint32_t ninv = (uint32_t)invmod64(N % p, p);
+    hninv[j] = make_uint2(ninv, shoup_of(ninv, (uint32_t)p));
+  }
+
+  // exact base conversion and scaling constants
+  ConvTabs& tb = c->tabs;
+  std::memset(&tb, 0, sizeof(tb));
+  tb.K = (int)c->K;
+  tb.KP = (int)c->KP;
+  tb.D = (int)c->D;
+  tb.digit_bits = (int)c->log2w;
+  const Big Kq = mul_small(Q, c->K + 1);
+  tb.W = (Kq.bits() + 31) / 32 + 1;
+  if (tb.W > WMAX) fail(HCNN_ERR_UNSUPPORTED, "q too large");
+  for (int w2 = 0; w2 < WMAX; ++w2) tb.q_w[w2] = Q.word(w2);
+  const Big h = shr1(Q);  // (q-1)/2, q odd
+  for (uint32_t i = 0; i < c->K; ++i) {
+    const u64 qi = q[i];
+    tb.q[i] = (uint32_t)qi;
+    tb.qmu[i] = (uint64_t)(((u128)1 << 64) / qi);
+    const Big qhat = div_small(Q, qi);
+    const u64 qhi = invmod64(mod_small(qhat, qi), qi);
+    tb.qhi[i] = (uint32_t)qhi;
+    tb.qhis[i] = shoup_of((uint32_t)qhi, (uint32_t)qi);
+    int b = 0;
+    while ((1ull << b) <= qi) ++b;
+    tb.qb[i] = b;
+    tb.qG[i] = (uint64_t)(((u128)1 << (60 + b)) / qi);
+    for (int w2 = 0; w2 < WMAX; ++w2) tb.qhat_w[i][w2] = qhat.word(w2);
+    for (uint32_t j = 0; j < c->KP; ++j) tb.qhat_p[i][j] = (uint32_t)mod_small(qhat, P[j]);
+    // scale: r~_i = (t d + h) qhi = d (t qhi) + h qhi
+    const u64 A = mulmod64(t % qi, qhi, qi);
+    tb.A[i] = (uint32_t)A;
+    tb.As[i] = shoup_of((uint32_t)A, (uint32_t)qi);
+    tb.B[i] = (uint32_t)mulmod64(mod_small(h, qi), qhi, qi);
+  }
+  for (uint32_t j = 0; j < c->KP; ++j) {
+    const u64 pj = P[j];
+    tb.p[j] = (uint32_t)pj;
+    tb.pmu[j] = (uint64_t)(((u128)1 << 64) / pj);
+    tb.negq_p[j] = (uint32_t)((pj - mod_small(Q, pj)) % pj);
+    const Big phat = div_small(Pp, pj);
+    const u64 phi = invmod64(mod_small(phat, pj), pj);
+    int b = 0;
+    while ((1ull << b) <= pj) ++b;
+    tb.pb[j] = b;
+    tb.pG[j] = (uint64_t)(((u128)1 << (60 + b)) / pj);
+    for (uint32_t i = 0; i < c->K; ++i) tb.phat_q[j][i] = (uint32_t)mod_small(phat, q[i]);
+    // y~_j = (t d + h - r) q^-1 phi = d C + (p - r) E + F
+    const u64 E = mulmod64(invmod64(mod_small(Q, pj), pj), phi, pj);
+    const u64 C = mulmod64(t % pj, E, pj);
+    tb.C[j] = (uint32_t)C;
+    tb.Cs[j] = shoup_of((uint32_t)C, (uint32_t)pj);
+    tb.Ej[j] = (uint32_t)E;
+    tb.Ejs[j] = shoup_of((uint32_t)E, (uint32_t)pj);
+    tb.F[j] = (uint32_t)mulmod64(mod_small(h, pj), E, pj);
+  }
+  for (uint32_t i = 0; i < c->K; ++i) tb.negp_q[i] = (uint32_t)((q[i] - mod_small(Pp, q[i])) % q[i]);
+
+  // upload
+  CK(cudaMalloc(&c->d_prime, L * sizeof(uint32_t)));
+  CK(cudaMalloc(&c->d_mu, L * sizeof(uint64_t)));
+  CK(cudaMalloc(&c->d_tw, (size_t)L * N * sizeof(uint2)));
+  CK(cudaMalloc(&c->d_itw, (size_t)L * N * sizeof(uint2)));
+  CK(cudaMalloc(&c->d_ninv, L * sizeof(uint2)));
+  CK(cudaMemcpy(c->d_prime, hp.data(), L * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_mu, hmu.data(), L * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_tw, htw.data(), (size_t)L * N * sizeof(uint2), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_itw, hitw.data(), (size_t)L * N * sizeof(uint2), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_ninv, hninv.data(), L * sizeof(uint2), cudaMemcpyHostToDevice));
+  c->nt = NttTabs{c->d_prime, c->d_mu, c->d_tw, c->d_itw, c->d_ninv};
+}
+
+// ---------------------------------------------------------------- dispatch
+void ntt_dispatch(hcnn_ctx* c, int op, NttLaunch& a, const char* what) {
+  a.stream = c->stream;
+  a.nt = c->nt;
+  cudaError_t e;
+  switch (c->logN) {
+#define X(L)                              \
+  case L:                                 \
+    e = hcnn_ntt_launch_##L(op, a);       \
+    break;
+    HCNN_LOGN_LIST(X)
+#undef X
+    default:
+      fail(HCNN_ERR_UNSUPPORTED, "ring degree");
+  }
+  c->launched(what);
+  (void)e;
+}
+
+void launch_ntt_rows(hcnn_ctx* c, uint32_t* rows, size_t n_rows, int limbs, int off, int inverse) {
+  if (n_rows == 0) return;
+  NttLaunch a{};
+  a.grid = dim3((unsigned)n_rows);
+  a.rows = rows;
+  a.limbs = limbs;
+  a.prime_off = off;
+  a.inverse = inverse;
+  ntt_dispatch(c, 0, a, "k_ntt_rows");
+}
+
+void launch_tensor(hcnn_ctx* c, const uint32_t* a_, const uint32_t* ae, const uint32_t* b,
+                   const uint32_t* be, uint32_t* d, size_t nct, int square) {
+  NttLaunch a{};
+  a.grid = dim3(c->K + c->KP, (unsigned)nct);
+  a.a = a_;
+  a.ae = ae;
+  a.b = b;
+  a.be = be;
+  a.d = d;
+  a.K = (int)c->K;
+  a.KP = (int)c->KP;
+  a.square = square;
+  ntt_dispatch(c, 1, a, "k_tensor");
+}
+
+void launch_relin(hcnn_ctx* c, const uint32_t* dig, const uint32_t* y3, uint32_t* out, size_t nct) {
+  NttLaunch a{};
+  a.grid = dim3(c->K, (unsigned)nct);
+  a.dig = dig;
+  a.y3 = y3;
+  a.rlk = c->d_rlk;
+  a.out = out;
+  a.K = (int)c->K;
+  a.D = (int)c->D;
+  a.reduce_digits = c->rlk_reduce ? 1 : 0;
+  ntt_dispatch(c, 2, a, "k_relin");
+}
+
+unsigned cdiv(size_t a, size_t b) { return (unsigned)((a + b - 1) / b); }
+
+// bytes of workspace per ciphertext of a multiply chunk
+size_t mul_ws_per_ct(hcnn_ctx* c, bool general) {
+  const size_t N = c->N, K = c->K, KP = c->KP;
+  size_t b = (general ? 2 : 1) * 2 * KP * N;  // extensions
+  b += 3 * (K + KP) * N;                      // tensor
+  b += 3 * K * N;                             // scaled 3-part
+  b += (size_t)c->D * N;                      // digits
+  return b * sizeof(uint32_t);
+}
+
+size_t chunk_cts(hcnn_ctx* c, size_t n, bool general) {
+  size_t per = mul_ws_per_ct(c, general);
+  size_t ch = c->ws_limit / per;
+  if (ch < 1) ch = 1;
+  if (ch > 16384) ch = 16384;
+  return ch < n ? ch : n;
+}
+
+// a (and b) -> out3 (3-part scaled) and, if dig, the digits of part 2
+void mul_chunk(hcnn_ctx* c, const uint32_t* a, const uint32_t* b, size_t nct, uint32_t* y3,
+               uint32_t* dig, uint8_t* ws) {
+  const size_t N = c->N, K = c->K, KP = c->KP;
+  const bool square = (a == b);
+  uint32_t* ae = (uint32_t*)ws;
+  uint32_t* be = square ? ae : ae + nct * 2 * KP * N;
+  uint32_t* d = be + nct * 2 * KP * N;
+  const unsigned tpb = 128;
+  k_extend<<<dim3(cdiv(N, tpb), (unsigned)(nct * 2)), tpb, 0, c->stream>>>(a, ae, (int)N, c->tabs);
+  c->launched("k_extend");
+  if (!square) {
+    k_extend<<<dim3(cdiv(N, tpb), (unsigned)(nct * 2)), tpb, 0, c->stream>>>(b, be, (int)N, c->tabs);
+    c->launched("k_extend");
+  }
+  launch_tensor(c, a, ae, b, be, d, nct, square ? 1 : 0);
+  k_scale<<<dim3(cdiv(N, tpb), (unsigned)(nct * 3)), tpb, 0, c->stream>>>(d, y3, dig, (int)N, c->tabs);
+  c->launched("k_scale");
+  (void)K;
+}
+
+void require_rlk(hcnn_ctx* c) {
+  if (!c->d_rlk) fail(HCNN_ERR_MISSING_KEY, "relinearization key required");
+}
+
+// y3 = hmult_raw(a, b); optionally relinearised into out
+void multiply(hcnn_ctx* c, const uint32_t* a, const uint32_t* b, size_t n, uint32_t* out3,
+              uint32_t* out2) {
+  if (n == 0) return;
+  const size_t N = c->N, K = c->K;
+  const bool general = a != b;
+  const size_t ch = chunk_cts(c, n, general);
+  const size_t per = mul_ws_per_ct(c, general);
+  uint8_t* ws = c->workspace(per * ch);
+  const size_t ext_bytes = ((general ? 2 : 1) * 2 * c->KP + 3 * (K + c->KP)) * N * sizeof(uint32_t);
+  for (size_t s = 0; s < n; s += ch) {
+    const size_t m = (n - s < ch) ? n - s : ch;
+    const uint32_t* ac = a + s * 2 * K * N;
+    const uint32_t* bc = b + s * 2 * K * N;
+    uint32_t* y3 = out3 ? out3 + s * 3 * K * N : (uint32_t*)(ws + ext_bytes * ch);
+    uint32_t* dig = out2 ? (uint32_t*)(ws + ext_bytes * ch + 3 * K * N * sizeof(uint32_t) * ch) : nullptr;
+    mul_chunk(c, ac, general ? bc : ac, m, y3, dig, ws);
+    if (out2) launch_relin(c, dig, y3, out2 + s * 2 * K * N, m);
+  }
+}
+
+// digits of part 2 of a 3-part tensor (for hcnn_relinearize)
+__global__ void k_digits(const uint32_t* __restrict__ in3, uint32_t* __restrict__ dig, int N,
+                         const __grid_constant__ ConvTabs tb) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  const size_t ct = blockIdx.y;
+  const uint32_t* src = in3 + (ct * 3 + 2) * tb.K * N + n;
+  uint32_t xt[KMAX];
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i)
+    if (i < tb.K) xt[i] = mul_shoup(src[(size_t)i * N], tb.qhi[i], tb.qhis[i], tb.q[i]);
+  const uint32_t v = exact_v(xt, tb);
+  uint32_t S[WMAX];
+  mw_lift(xt, tb, S);
+  mw_sub_mq(S, v, tb);
+  uint32_t* dd = dig + ct * tb.D * N + n;
+  const int db = tb.digit_bits;
+  const uint32_t mask = db == 32 ? 0xffffffffu : ((1u << db) - 1);
+  for (int k = 0; k < tb.D; ++k) {
+    const int bit = k * db;
+    const int wi = bit >> 5, sh = bit & 31;
+    uint32_t word = 0;
+#pragma unroll
+    for (int w = 0; w < WMAX; ++w)
+      if (w == wi) word = S[w];
+    dd[(size_t)k * N] = (word >> sh) & mask;
+  }
+}
+
+__global__ void k_hadd(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                       uint32_t* __restrict__ out, int K, int N, size_t total,
+                       const uint32_t* __restrict__ primes) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int limb = (int)((i / N) % K);
+  out[i] = add_mod(a[i], b[i], primes[limb]);
+}
+
+// integer-pipe throughput probe: 8 independent chains per thread
+template <int KIND>
+__global__ void k_int_peak(uint32_t* out, uint32_t a, uint32_t b, int iters) {
+  uint32_t x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 7 + i + blockIdx.x;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (KIND == 0) {
+        x[i] = x[i] * a + b;
+      } else if (KIND == 1) {
+        x[i] = __umulhi(x[i], a) + b;
+      } else {
+        const uint64_t w = (uint64_t)x[i] * a + b;
+        x[i] = (uint32_t)(w >> 32) + (uint32_t)w;
+      }
+    }
+  }
+  uint32_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc ^= x[i];
+  if (acc == 0x9e3779b9u) out[0] = acc;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+const char* hcnn_last_error(void) { return g_err.c_str(); }
+int hcnn_int_peak(int device, int kind, double* ops_per_s) {
+  return guarded([&] {
+    CK(cudaSetDevice(device));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    uint32_t* out = nullptr;
+    CK(cudaMalloc(&out, 4));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    const int iters = 4096, tpb = 256, blocks = sms * 8;
+    auto run = [&] {
+      switch (kind) {
+        case 0: k_int_peak<0><<<blocks, tpb>>>(out, 0x9e3779b1u, 12345u, iters); break;
+        case 1: k_int_peak<1><<<blocks, tpb>>>(out, 0x9e3779b1u, 12345u, iters); break;
+        default: k_int_peak<2><<<blocks, tpb>>>(out, 0x9e3779b1u, 12345u, iters); break;
+      }
+    };
+    run();
+    CK(cudaDeviceSynchronize());
+    CK(cudaEventRecord(e0));
+    for (int r = 0; r < 5; ++r) run();
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    *ops_per_s = 5.0 * blocks * tpb * (double)iters * 8 / (ms * 1e-3);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+  });
+}
+
+const char* hcnn_version(void) { return "hcnn_b200 0.1 (sm_100a)"; }
+
+int hcnn_ctx_create(hcnn_ctx** out, uint32_t n, uint32_t k, const uint64_t* primes, uint64_t t,
+                    uint32_t log2w, int device) {
+  return guarded([&] {
+    if (!out || !primes) fail(HCNN_ERR_PARAM, "null argument");
+    *out = nullptr;
+    if (n < 4 || (n & (n - 1)) || n > (1u << 15)) fail(HCNN_ERR_UNSUPPORTED, "ring degree must be a power of two in [4, 2^15]");
+    if (k < 1 || k > (uint32_t)KMAX) fail(HCNN_ERR_UNSUPPORTED, "1..16 primes supported");
+    if (log2w != 8 && log2w != 16 && log2w != 32) fail(HCNN_ERR_PARAM, "relin base must be 2^8, 2^16 or 2^32");
+    std::vector<u64> q(primes, primes + k);
+    for (uint32_t i = 0; i < k; ++i) {
+      if (q[i] >= (1ull << 30) || q[i] < 3) fail(HCNN_ERR_UNSUPPORTED, "RNS primes must be below 2^30 on the u32 path");
+      if (!is_prime64(q[i])) fail(HCNN_ERR_UNSUPPORTED, std::to_string(q[i]) + " is not prime");
+      if (q[i] % (2ull * n) != 1) fail(HCNN_ERR_UNSUPPORTED, std::to_string(q[i]) + " is not 1 mod 2N");
+      for (uint32_t j = 0; j < i; ++j)
+        if (q[j] == q[i]) fail(HCNN_ERR_PARAM, "primes must be pairwise distinct");
+    }
+    if (t < 2) fail(HCNN_ERR_PARAM, "plaintext modulus must be >= 2");
+    {
+      Big Q = product(q);
+      if (cmp(Big(t), Q) >= 0) fail(HCNN_ERR_PARAM, "plaintext modulus must be below q");
+    }
+    auto c = std::make_unique<hcnn_ctx>();
+    c->device = device;
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    c->stream = c->own_stream;
+    c->N = n;
+    c->logN = 0;
+    while ((1u << c->logN) < n) ++c->logN;
+    c->K = k;
+    c->t = t;
+    c->log2w = log2w;
+    build_tables(c.get(), q, t);
+    *out = c.release();
+  });
+}
+
+int hcnn_ctx_destroy(hcnn_ctx* c) {
+  return guarded([&] {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    if (c->ws) cudaFree(c->ws);
+    cudaFree(c->d_prime);
+    cudaFree(c->d_mu);
+    cudaFree(c->d_tw);
+    cudaFree(c->d_itw);
+    cudaFree(c->d_ninv);
+    if (c->d_rlk) cudaFree(c->d_rlk);
+    if (c->d_pk) cudaFree(c->d_pk);
+    if (c->d_delta) cudaFree(c->d_delta);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    delete c;
+  });
+}
+
+int hcnn_profile(hcnn_ctx* c, int enable) {
+  return guarded([&] {
+    CK(cudaStreamSynchronize(c->stream));
+    c->prof_reset();
+    c->prof = enable != 0;
+  });
+}
+
+int64_t hcnn_profile_dump(hcnn_ctx* c, char* buf, size_t len) {
+  std::string out;
+  int rc = guarded([&] {
+    CK(cudaStreamSynchronize(c->stream));
+    std::vector<std::pair<std::string, std::pair<int64_t, double>>> agg;
+    for (auto& r : c->recs) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, r.a, r.b));
+      bool found = false;
+      for (auto& a : agg)
+        if (a.first == r.name) {
+          a.second.first += 1;
+          a.second.second += ms;
+          found = true;
+        }
+      if (!found) agg.push_back({r.name, {1, (double)ms}});
+    }
+    for (auto& a : agg) {
+      char line[256];
+      snprintf(line, sizeof line, "%s %lld %.6f\n", a.first.c_str(), (long long)a.second.first, a.second.second);
+      out += line;
+    }
+  });
+  if (rc != HCNN_OK) return -rc;
+  if (buf && len) {
+    size_t n = out.size() < len - 1 ? out.size() : len - 1;
+    memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return (int64_t)out.size();
+}
+
+int hcnn_ctx_set_stream(hcnn_ctx* c, void* stream) {
+  return guarded([&] { c->stream = (cudaStream_t)stream; });
+}
+
+int hcnn_ctx_set_workspace_limit(hcnn_ctx* c, size_t bytes) {
+  return guarded([&] { c->ws_limit = bytes; });
+}
+
+int64_t hcnn_ctx_query(hcnn_ctx* c, int what) {
+  switch (what) {
+    case HCNN_Q_N: return c->N;
+    case HCNN_Q_K: return c->K;
+    case HCNN_Q_KP: return c->KP;
+    case HCNN_Q_DIGITS: return c->D;
+    case HCNN_Q_LOG2W: return c->log2w;
+    case HCNN_Q_WS_BYTES: return (int64_t)c->ws_bytes;
+    case HCNN_Q_KERNELS: return c->launches;
+    default: return -1;
+  }
+}
+
+uint64_t hcnn_ctx_prime(hcnn_ctx* c, int i, uint64_t* psi) {
+  if (i < 0 || (size_t)i >= c->primes.size()) return 0;
+  if (psi) *psi = c->psi[i];
+  return c->primes[i];
+}
+
+int hcnn_set_relin_key(hcnn_ctx* c, const uint64_t* rlk, int domain) {
+  return guarded([&] {
+    if (!rlk) fail(HCNN_ERR_MISSING_KEY, "relinearization key required");
+    CK(cudaSetDevice(c->device));
+    const size_t rows = (size_t)c->D * 2 * c->K;
+    const size_t count = rows * c->N;
+    uint64_t* stage = nullptr;
+    uint32_t* tmp = nullptr;
+    CK(cudaMallocAsync((void**)&stage, count * sizeof(uint64_t), c->stream));
+    CK(cudaMallocAsync((void**)&tmp, count * sizeof(uint32_t), c->stream));
+    if (!c->d_rlk) CK(cudaMalloc((void**)&c->d_rlk, count * sizeof(uint32_t)));
+    CK(cudaMemcpyAsync(stage, rlk, count * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
+    k_narrow<<<cdiv(count, 256), 256, 0, c->stream>>>(stage, tmp, count);
+    c->launched("k_narrow");
+    if (domain == HCNN_DOMAIN_REF_NTT) {
+      k_bitrev_rows<<<dim3(cdiv(c->N, 256), (unsigned)rows), 256, 0, c->stream>>>(tmp, c->d_rlk, (int)c->N, (int)c->logN);
+      c->launched("k_bitrev_rows");
+    } else if (domain == HCNN_DOMAIN_COEFF) {
+      CK(cudaMemcpyAsync(c->d_rlk, tmp, count * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->stream));
+      launch_ntt_rows(c, c->d_rlk, rows, (int)c->K, 0, 0);
+    } else {
+      fail(HCNN_ERR_DOMAIN, "unknown key domain");
+    }
+    CK(cudaFreeAsync(stage, c->stream));
+    CK(cudaFreeAsync(tmp, c->stream));
+    // digits of w = 2^32 may exceed a prime; 2^8 / 2^16 digits never do here
+    c->rlk_reduce = false;
+    for (uint32_t i = 0; i < c->K; ++i)
+      if ((c->log2w >= 32) || ((1ull << c->log2w) > c->primes[i])) c->rlk_reduce = true;
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int hcnn_set_public_key(hcnn_ctx* c, const uint64_t* pk, int domain) {
+  return guarded([&] {
+    if (!pk) fail(HCNN_ERR_MISSING_KEY, "public key required");
+    CK(cudaSetDevice(c->device));
+    const size_t rows = 2 * (size_t)c->K;
+    const size_t count = rows * c->N;
+    uint64_t* stage = nullptr;
+    uint32_t* tmp = nullptr;
+    CK(cudaMallocAsync((void**)&stage, count * sizeof(uint64_t), c->stream));
+    CK(cudaMallocAsync((void**)&tmp, count * sizeof(uint32_t), c->stream));
+    if (!c->d_pk) CK(cudaMalloc((void**)&c->d_pk, count * sizeof(uint32_t)));
+    CK(cudaMemcpyAsync(stage, pk, count * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
+    k_narrow<<<cdiv(count, 256), 256, 0, c->stream>>>(stage, tmp, count);
+    c->launched("k_narrow");
+    if (domain == HCNN_DOMAIN_REF_NTT) {
+      k_bitrev_rows<<<dim3(cdiv(c->N, 256), (unsigned)rows), 256, 0, c->stream>>>(tmp, c->d_pk, (int)c->N, (int)c->logN);
+      c->launched("k_bitrev_rows");
+    } else if (domain == HCNN_DOMAIN_COEFF) {
+      CK(cudaMemcpyAsync(c->d_pk, tmp, count * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->stream));
+      launch_ntt_rows(c, c->d_pk, rows, (int)c->K, 0, 0);
+    } else {
+      fail(HCNN_ERR_DOMAIN, "unknown key domain");
+    }
+    // Delta = floor(q / t) mod q_i (bfv.py:77)
+    if (!c->d_delta) {
+      Big Q = product(std::vector<u64>(c->primes.begin(), c->primes.begin() + c->K));
+      // floor(Q / t) with t up to 64 bits: long division by a u64
+      Big D;
+      D.w.assign(Q.w.size(), 0);
+      u128 r = 0;
+      for (size_t i = Q.w.size(); i-- > 0;) {
+        r = (r << 32) | Q.w[i];
+        D.w[i] = (u32)(r / c->t);
+        r %= c->t;
+      }
+      D.trim();
+      std::vector<uint2> hd(c->K);
+      for (uint32_t i = 0; i < c->K; ++i) {
+        const uint32_t v = (uint32_t)mod_small(D, c->primes[i]);
+        hd[i] = make_uint2(v, shoup_of(v, (uint32_t)c->primes[i]));
+      }
+      CK(cudaMalloc((void**)&c->d_delta, c->K * sizeof(uint2)));
+      CK(cudaMemcpy(c->d_delta, hd.data(), c->K * sizeof(uint2), cudaMemcpyHostToDevice));
+    }
+    CK(cudaFreeAsync(stage, c->stream));
+    CK(cudaFreeAsync(tmp, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int hcnn_encrypt(hcnn_ctx* c, const int8_t* u, const int8_t* e1, const int8_t* e2, const int64_t* msg,
+                 uint32_t* out, size_t n) {
+  return guarded([&] {
+    if (!c->d_pk) fail(HCNN_ERR_MISSING_KEY, "public key required");
+    CK(cudaSetDevice(c->device));
+    if (n == 0) return;
+    c->mark();
+    const size_t N = c->N;
+    const size_t ch = n < 4096 ? n : 4096;
+    uint8_t* stage = nullptr;
+    const size_t bytes = ch * N * (3 + sizeof(int64_t));
+    CK(cudaMallocAsync((void**)&stage, bytes, c->stream));
+    for (size_t s0 = 0; s0 < n; s0 += ch) {
+      const size_t m = n - s0 < ch ? n - s0 : ch;
+      int8_t* du = (int8_t*)stage;
+      int8_t* d1 = du + ch * N;
+      int8_t* d2 = d1 + ch * N;
+      int64_t* dm = (int64_t*)(d2 + ch * N);
+      CK(cudaMemcpyAsync(du, u + s0 * N, m * N, cudaMemcpyHostToDevice, c->stream));
+      CK(cudaMemcpyAsync(d1, e1 + s0 * N, m * N, cudaMemcpyHostToDevice, c->stream));
+      CK(cudaMemcpyAsync(d2, e2 + s0 * N, m * N, cudaMemcpyHostToDevice, c->stream));
+      CK(cudaMemcpyAsync(dm, msg + s0 * N, m * N * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+      NttLaunch a{};
+      a.grid = dim3(c->K, (unsigned)m);
+      a.u = du;
+      a.e1 = d1;
+      a.e2 = d2;
+      a.msg = dm;
+      a.pk = c->d_pk;
+      a.delta = c->d_delta;
+      a.out = out + s0 * 2 * c->K * N;
+      a.K = (int)c->K;
+      ntt_dispatch(c, 3, a, "k_encrypt");
+    }
+    CK(cudaFreeAsync(stage, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int hcnn_alloc(hcnn_ctx* c, size_t bytes, void** out) {
+  return guarded([&] {
+    CK(cudaSetDevice(c->device));
+    CK(cudaMallocAsync(out, bytes, c->stream));
+  });
+}
+
+int hcnn_free(hcnn_ctx* c, void* ptr) {
+  return guarded([&] {
+    CK(cudaSetDevice(c->device));
+    CK(cudaFreeAsync(ptr, c->stream));
+  });
+}
+
+int hcnn_upload_u64(hcnn_ctx* c, uint32_t* dst, const uint64_t* src, size_t count) {
+  return guarded([&] {
+    CK(cudaSetDevice(c->device));
+    uint64_t* stage = nullptr;
+    CK(cudaMallocAsync((void**)&stage, count * sizeof(uint64_t), c->stream));
+    CK(cudaMemcpyAsync(stage, src, count * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
+    k_narrow<<<cdiv(count, 256), 256, 0, c->stream>>>(stage, dst, count);
+    c->launched("k_narrow");
+    CK(cudaFreeAsync(stage, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int hcnn_download_u64(hcnn_ctx* c, uint64_t* dst, const uint32_t* src, size_t count) {
+  return guarded([&] {
+    CK(cudaSetDevice(c->device));
+    uint64_t* stage = nullptr;
+    CK(cudaMallocAsync((void**)&stage, count * sizeof(uint64_t), c->stream));
+    k_widen<<<cdiv(count, 256), 256, 0, c->stream>>>(src, stage, count);
+    c->launched("k_widen");
+    CK(cudaMemcpyAsync(dst, stage, count * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaFreeAsync(stage, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int hcnn_sync(hcnn_ctx* c) {
+  return guarded([&] {
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int hcnn_reduce_weights(hcnn_ctx* c, const int64_t* w, size_t count, uint32_t* out) {
+  return guarded([&] {
+    if (count == 0) return;
+    CK(cudaSetDevice(c->device));
+    int64_t* stage = nullptr;
+    CK(cudaMallocAsync((void**)&stage, count * sizeof(int64_t), c->stream));
+    CK(cudaMemcpyAsync(stage, w, count * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    k_reduce_weights<<<cdiv(count, 256), 256, 0, c->stream>>>(stage, count, out, c->d_prime, (int)c->K);
+    c->launched("k_reduce_weights");
+    CK(cudaFreeAsync(stage, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int hcnn_conv(hcnn_ctx* c, const uint32_t* in, uint32_t* out, int h, int w, int ch,
+              const uint32_t* wred, int f, int kh, int kw, int sh, int sw, int padded, int groups) {
+  return guarded([&] {
+    c->mark();
+    if (groups < 1 || ch % groups || f % groups) fail(HCNN_ERR_PARAM, "conv: channel mismatch");
+    ConvGeom g;
+    g.h = h;
+    g.w = w;
+    g.c = ch;
+    g.f = f;
+    g.kh = kh;
+    g.kw = kw;
+    g.cg = ch / groups;
+    g.sh = sh;
+    g.sw = sw;
+    g.ph = padded ? (kh - 1) / 2 : 0;
+    g.pw = padded ? (kw - 1) / 2 : 0;
+    g.oh = (h + 2 * g.ph - kh) / sh + 1;
+    g.ow = (w + 2 * g.pw - kw) / sw + 1;
+    g.per_group = f / groups;
+    if (g.oh <= 0 || g.ow <= 0) fail(HCNN_ERR_PARAM, "conv: empty output");
+    CK(cudaSetDevice(c->device));
+    const unsigned tpb = c->N >= 512 ? 128 : (c->N / 4 >= 32 ? c->N / 4 : 32);
+    int fb = 1;
+    for (int cand : {8, 5, 4, 2, 1})
+      if (g.per_group % cand == 0) {
+        fb = cand;
+        break;
+      }
+    const size_t zdim = (size_t)g.oh * g.ow * (f / fb);
+    if (zdim > 65535) fail(HCNN_ERR_CAPACITY, "conv: too many output blocks for one launch");
+    dim3 grid(cdiv(c->N / 4, tpb), 2 * c->K, (unsigned)zdim);
+    switch (fb) {
+#define X(FB)                                                                                       \
+  case FB:                                                                                          \
+    k_conv<FB><<<grid, tpb, 0, c->stream>>>(in, out, wred, g, (int)c->K, (int)c->N, c->d_prime, c->d_mu); \
+    break;
+      X(1) X(2) X(4) X(5) X(8)
+#undef X
+    }
+    c->launched("k_conv");
+  });
+}
+
+int hcnn_fc(hcnn_ctx* c, const uint32_t* in, uint32_t* out, int n_in, int n_out, const uint32_t* wred) {
+  return guarded([&] {
+    c->mark();
+    CK(cudaSetDevice(c->device));
+    const unsigned tpb = c->N >= 512 ? 128 : (c->N / 4 >= 32 ? c->N / 4 : 32);
+    constexpr int OB = 8;
+    dim3 grid(cdiv(c->N / 4, tpb), 2 * c->K, cdiv(n_out, OB));
+    k_fc<OB><<<grid, tpb, 0, c->stream>>>(in, out, wred, n_in, n_out, (int)c->K, (int)c->N, c->d_prime, c->d_mu);
+    c->launched("k_fc");
+  });
+}
+
+int hcnn_pool(hcnn_ctx* c, const uint32_t* in, uint32_t* out, int h, int w, int ch, int e, int sh, int sw) {
+  return guarded([&] {
+    c->mark();
+    CK(cudaSetDevice(c->device));
+    const int oh = (h - e) / sh + 1, ow = (w - e) / sw + 1;
+    if (oh <= 0 || ow <= 0) fail(HCNN_ERR_PARAM, "pool: empty output");
+    const size_t nout = (size_t)oh * ow * ch;
+    if (nout > 65535) fail(HCNN_ERR_CAPACITY, "pool: too many outputs for one launch");
+    const unsigned tpb = c->N >= 512 ? 128 : (c->N / 4 >= 32 ? c->N / 4 : 32);
+    dim3 grid(cdiv(c->N / 4, tpb), 2 * c->K, (unsigned)nout);
+    k_pool<<<grid, tpb, 0, c->stream>>>(in, out, h, w, ch, e, sh, sw, ow, (int)c->K, (int)c->N, c->d_prime, c->d_mu);
+    c->launched("k_pool");
+  });
+}
+
+int hcnn_square(hcnn_ctx* c, const uint32_t* in, uint32_t* out, size_t n) {
+  return guarded([&] {
+    c->mark();
+    require_rlk(c);
+    CK(cudaSetDevice(c->device));
+    multiply(c, in, in, n, nullptr, out);
+  });
+}
+
+int hcnn_hmult_raw(hcnn_ctx* c, const uint32_t* a, const uint32_t* b, uint32_t* out3, size_t n) {
+  return guarded([&] {
+    c->mark();
+    CK(cudaSetDevice(c->device));
+    multiply(c, a, b, n, out3, nullptr);
+  });
+}
+
+int hcnn_hmult(hcnn_ctx* c, const uint32_t* a, const uint32_t* b, uint32_t* out, size_t n) {
+  return guarded([&] {
+    c->mark();
+    require_rlk(c);
+    CK(cudaSetDevice(c->device));
+    multiply(c, a, b, n, nullptr, out);
+  });
+}
+
+int hcnn_relinearize(hcnn_ctx* c, const uint32_t* in3, uint32_t* out, size_t n) {
+  return guarded([&] {
+    c->mark();
+    require_rlk(c);
+    CK(cudaSetDevice(c->device));
+    if (n == 0) return;
+    const size_t per = (size_t)c->D * c->N * sizeof(uint32_t);
+    size_t ch = c->ws_limit / per;
+    if (ch < 1) ch = 1;
+    if (ch > 65535) ch = 65535;
+    if (ch > n) ch = n;
+    uint32_t* dig = (uint32_t*)c->workspace(per * ch);
+    const size_t K = c->K, N = c->N;
+    for (size_t s = 0; s < n; s += ch) {
+      const size_t m = (n - s < ch) ? n - s : ch;
+      k_digits<<<dim3(cdiv(N, 128), (unsigned)m), 128, 0, c->stream>>>(in3 + s * 3 * K * N, dig, (int)N, c->tabs);
+      c->launched("k_digits");
+      launch_relin(c, dig, in3 + s * 3 * K * N, out + s * 2 * K * N, m);
+    }
+  });
+}
+
+int hcnn_hadd(hcnn_ctx* c, const uint32_t* a, const uint32_t* b, uint32_t* out, size_t n) {
+  return guarded([&] {
+    c->mark();
+    CK(cudaSetDevice(c->device));
+    const size_t total = n * 2 * c->K * c->N;
+    if (!total) return;
+    k_hadd<<<cdiv(total, 256), 256, 0, c->stream>>>(a, b, out, (int)c->K, (int)c->N, total, c->d_prime);
+    c->launched("k_hadd");
+  });
+}
+
+int hcnn_ntt(hcnn_ctx* c, uint32_t* rows, size_t n_rows, uint32_t limbs, uint32_t off, int inverse) {
+  return guarded([&] {
+    c->mark();
+    if (limbs == 0 || off + limbs > c->K + c->KP) fail(HCNN_ERR_PARAM, "ntt: prime range");
+    CK(cudaSetDevice(c->device));
+    launch_ntt_rows(c, rows, n_rows, (int)limbs, (int)off, inverse);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,290 @@
+// Non-NTT kernels of the hot path (included by hcnn.cu only).
+#pragma once
+#include "common.cuh"
+
+namespace hcnn {
+
+// --------------------------------------------------------- Q -> P extension
+// in: [B][2][K][N] canonical residues; ext: [B][2][KP][N]
+__global__ void k_extend(const uint32_t* __restrict__ in, uint32_t* __restrict__ ext, int N,
+                         const __grid_constant__ ConvTabs tb) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  const size_t poly = blockIdx.y;  // ct * 2 + part
+  const uint32_t* src = in + poly * tb.K * N + n;
+  uint32_t xt[KMAX];
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i)
+    if (i < tb.K) xt[i] = mul_shoup(src[(size_t)i * N], tb.qhi[i], tb.qhis[i], tb.q[i]);
+  const uint32_t v = exact_v(xt, tb);
+  uint32_t* dst = ext + poly * tb.KP * N + n;
+#pragma unroll
+  for (int j = 0; j < KPMAX; ++j)
+    if (j < tb.KP) dst[(size_t)j * N] = q_to_p(xt, v, j, tb);
+}
+
+// ------------------------------------------------------- scale and round
+// d: [B][3][K+KP][N] exact tensor residues (coefficient domain).
+// y3: [B][3][K][N] = round(t d / q) mod q for each part (bfv.py:325-328);
+// dig (if not null): [B][D][N] base-w digits of canonical y_2 (bfv.py:350-365).
+__global__ void k_scale(const uint32_t* __restrict__ d, uint32_t* __restrict__ y3,
+                        uint32_t* __restrict__ dig, int N, const __grid_constant__ ConvTabs tb) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  const int part = blockIdx.y % 3;
+  const size_t ct = blockIdx.y / 3;
+  const int K = tb.K, KP = tb.KP;
+  const uint32_t* src = d + (size_t)blockIdx.y * (K + KP) * N + n;
+
+  // r = (t d + h) mod q, h = (q-1)/2, as r~_i = r_i (q/q_i)^-1 mod q_i
+  uint32_t rt[KMAX];
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i)
+    if (i < K) rt[i] = add_mod(mul_shoup(src[(size_t)i * N], tb.A[i], tb.As[i], tb.q[i]), tb.B[i], tb.q[i]);
+  const uint32_t v = exact_v(rt, tb);
+
+  // y = (t d + h - r) / q exactly, in P (centred, |y| < P/4): y~_j = y_j (P/p_j)^-1
+  uint32_t yt[KPMAX];
+  uint64_t F = 0;
+#pragma unroll
+  for (int j = 0; j < KPMAX; ++j) {
+    if (j < KP) {
+      const uint32_t pj = tb.p[j];
+      const uint32_t rj = q_to_p(rt, v, j, tb);
+      const uint32_t dj = src[(size_t)(K + j) * N];
+      uint32_t acc = add_mod(mul_shoup(dj, tb.C[j], tb.Cs[j], pj), mul_shoup(pj - rj, tb.Ej[j], tb.Ejs[j], pj), pj);
+      acc = add_mod(acc, tb.F[j], pj);
+      yt[j] = acc;
+      F += frac60(acc, tb.pG[j], tb.pb[j]);
+    }
+  }
+  const uint32_t vp = (uint32_t)((F + (FRAC_ONE >> 1)) >> 60);
+
+  // back to Q: y_i = (sum_j y~_j (P/p_j) - vp P) mod q_i
+  uint32_t yq[KMAX];
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i) {
+    if (i < K) {
+      uint64_t acc = (uint64_t)vp * tb.negp_q[i];
+#pragma unroll
+      for (int j = 0; j < KPMAX; ++j)
+        if (j < KP) acc += (uint64_t)yt[j] * tb.phat_q[j][i];
+      yq[i] = reduce64(acc, tb.q[i], tb.qmu[i]);
+    }
+  }
+  uint32_t* dst = y3 + (size_t)blockIdx.y * K * N + n;
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i)
+    if (i < K) dst[(size_t)i * N] = yq[i];
+
+  if (part != 2 || dig == nullptr) return;
+  // canonical binary of y_2 mod q, then base-w digits
+  uint32_t xt[KMAX];
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i)
+    if (i < K) xt[i] = mul_shoup(yq[i], tb.qhi[i], tb.qhis[i], tb.q[i]);
+  uint64_t Fq = 0;
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i)
+    if (i < K) Fq += frac60(xt[i], tb.qG[i], tb.qb[i]);
+  uint32_t S[WMAX];
+  mw_lift(xt, tb, S);
+  mw_sub_mq(S, (uint32_t)(Fq >> 60), tb);  // S - V q >= 0, V <= v
+  {
+    // if S >= q subtract q once more
+    uint32_t T[WMAX];
+#pragma unroll
+    for (int w = 0; w < WMAX; ++w) T[w] = S[w];
+    if (!mw_sub_mq(T, 1, tb)) {
+#pragma unroll
+      for (int w = 0; w < WMAX; ++w) S[w] = T[w];
+    }
+  }
+  uint32_t* dd = dig + ct * tb.D * N + n;
+  const int db = tb.digit_bits;
+  const uint32_t mask = db == 32 ? 0xffffffffu : ((1u << db) - 1);
+  for (int k = 0; k < tb.D; ++k) {
+    const int bit = k * db;
+    const int wi = bit >> 5, sh = bit & 31;
+    uint32_t word = 0;
+#pragma unroll
+    for (int w = 0; w < WMAX; ++w)
+      if (w == wi) word = S[w];
+    dd[(size_t)k * N] = (word >> sh) & mask;
+  }
+}
+
+// ------------------------------------------------ plaintext-weight MAC
+// Residues < 2^30 and weights reduced mod p_i < 2^30: 15 lazy 64-bit products
+// fit before a reduction (15 * (2^30-1)^2 + 2^30 < 2^64).
+struct ConvGeom {
+  int h, w, c, f, kh, kw, cg, sh, sw, ph, pw, oh, ow, per_group;
+};
+
+DI void mac4(uint64_t* a, uint32_t wv, uint4 x) {
+  a[0] += (uint64_t)wv * x.x;
+  a[1] += (uint64_t)wv * x.y;
+  a[2] += (uint64_t)wv * x.z;
+  a[3] += (uint64_t)wv * x.w;
+}
+
+// grid: x = coefficient quads, y = part*K + limb, z = out position * nfb + filter block
+// wred: [F][kh][kw][cg][K] weights mod p_i.
+template <int FB>
+__global__ void k_conv(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                       const uint32_t* __restrict__ wred, ConvGeom g, int K, int N,
+                       const uint32_t* __restrict__ primes, const uint64_t* __restrict__ mus) {
+  const int quad = blockIdx.x * blockDim.x + threadIdx.x;
+  if (quad * 4 >= N) return;
+  const int limb = blockIdx.y % K, part = blockIdx.y / K;
+  const int nfb = g.f / FB;
+  const int pos = blockIdx.z / nfb, fbk = blockIdx.z % nfb;
+  const int oy = pos / g.ow, ox = pos % g.ow;
+  const int f0 = fbk * FB;
+  const int grp = f0 / g.per_group;
+  const uint32_t p = primes[limb];
+  const uint64_t mu = mus[limb];
+  uint64_t acc[FB][4];
+#pragma unroll
+  for (int f = 0; f < FB; ++f) acc[f][0] = acc[f][1] = acc[f][2] = acc[f][3] = 0;
+  int cnt = 0;
+  for (int ky = 0; ky < g.kh; ++ky) {
+    const int iy = oy * g.sh + ky - g.ph;
+    if (iy < 0 || iy >= g.h) continue;
+    for (int kx = 0; kx < g.kw; ++kx) {
+      const int ix = ox * g.sw + kx - g.pw;
+      if (ix < 0 || ix >= g.w) continue;
+      for (int ci = 0; ci < g.cg; ++ci) {
+        const size_t in_ct = ((size_t)iy * g.w + ix) * g.c + grp * g.cg + ci;
+        const uint4 xv = *reinterpret_cast<const uint4*>(in + ((in_ct * 2 + part) * K + limb) * N + quad * 4);
+        const size_t wbase = (((size_t)f0 * g.kh + ky) * g.kw + kx) * g.cg + ci;
+        const size_t fstride = (size_t)g.kh * g.kw * g.cg;
+#pragma unroll
+        for (int f = 0; f < FB; ++f) mac4(acc[f], __ldg(&wred[(wbase + f * fstride) * K + limb]), xv);
+        if (++cnt == 15) {
+          cnt = 0;
+#pragma unroll
+          for (int f = 0; f < FB; ++f)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[f][v] = reduce64(acc[f][v], p, mu);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int f = 0; f < FB; ++f) {
+    const size_t out_ct = (size_t)pos * g.f + f0 + f;
+    uint4 r;
+    r.x = reduce64(acc[f][0], p, mu);
+    r.y = reduce64(acc[f][1], p, mu);
+    r.z = reduce64(acc[f][2], p, mu);
+    r.w = reduce64(acc[f][3], p, mu);
+    *reinterpret_cast<uint4*>(out + ((out_ct * 2 + part) * K + limb) * N + quad * 4) = r;
+  }
+}
+
+// dense: out[o] = sum_i W[o][i] in[i]; wred: [O][I][K]; grid z = output block
+template <int OB>
+__global__ void k_fc(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                     const uint32_t* __restrict__ wred, int n_in, int n_out, int K, int N,
+                     const uint32_t* __restrict__ primes, const uint64_t* __restrict__ mus) {
+  const int quad = blockIdx.x * blockDim.x + threadIdx.x;
+  if (quad * 4 >= N) return;
+  const int limb = blockIdx.y % K, part = blockIdx.y / K;
+  const int o0 = blockIdx.z * OB;
+  const uint32_t p = primes[limb];
+  const uint64_t mu = mus[limb];
+  uint64_t acc[OB][4];
+#pragma unroll
+  for (int o = 0; o < OB; ++o) acc[o][0] = acc[o][1] = acc[o][2] = acc[o][3] = 0;
+  int cnt = 0;
+  for (int i = 0; i < n_in; ++i) {
+    const uint4 xv = *reinterpret_cast<const uint4*>(in + (((size_t)i * 2 + part) * K + limb) * N + quad * 4);
+#pragma unroll
+    for (int o = 0; o < OB; ++o)
+      if (o0 + o < n_out) mac4(acc[o], __ldg(&wred[((size_t)(o0 + o) * n_in + i) * K + limb]), xv);
+    if (++cnt == 15) {
+      cnt = 0;
+#pragma unroll
+      for (int o = 0; o < OB; ++o)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[o][v] = reduce64(acc[o][v], p, mu);
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < OB; ++o) {
+    if (o0 + o >= n_out) break;
+    uint4 r;
+    r.x = reduce64(acc[o][0], p, mu);
+    r.y = reduce64(acc[o][1], p, mu);
+    r.z = reduce64(acc[o][2], p, mu);
+    r.w = reduce64(acc[o][3], p, mu);
+    *reinterpret_cast<uint4*>(out + (((size_t)(o0 + o) * 2 + part) * K + limb) * N + quad * 4) = r;
+  }
+}
+
+// sum-pool: grid x = quads, y = part*K + limb, z = output ct
+__global__ void k_pool(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int h, int w,
+                       int c, int e, int sh, int sw, int ow, int K, int N,
+                       const uint32_t* __restrict__ primes, const uint64_t* __restrict__ mus) {
+  const int quad = blockIdx.x * blockDim.x + threadIdx.x;
+  if (quad * 4 >= N) return;
+  const int limb = blockIdx.y % K, part = blockIdx.y / K;
+  const int o = blockIdx.z;
+  const int ch = o % c, pos = o / c;
+  const int oy = pos / ow, ox = pos % ow;
+  uint64_t a[4] = {0, 0, 0, 0};
+  for (int dy = 0; dy < e; ++dy)
+    for (int dx = 0; dx < e; ++dx) {
+      const size_t ict = ((size_t)(oy * sh + dy) * w + (ox * sw + dx)) * c + ch;
+      const uint4 x = *reinterpret_cast<const uint4*>(in + ((ict * 2 + part) * K + limb) * N + quad * 4);
+      a[0] += x.x;
+      a[1] += x.y;
+      a[2] += x.z;
+      a[3] += x.w;
+    }
+  const uint32_t p = primes[limb];
+  const uint64_t mu = mus[limb];
+  uint4 r;
+  r.x = reduce64(a[0], p, mu);
+  r.y = reduce64(a[1], p, mu);
+  r.z = reduce64(a[2], p, mu);
+  r.w = reduce64(a[3], p, mu);
+  *reinterpret_cast<uint4*>(out + (((size_t)o * 2 + part) * K + limb) * N + quad * 4) = r;
+}
+
+// weights (int64, any sign) -> [n][K] residues mod q_i
+__global__ void k_reduce_weights(const int64_t* __restrict__ w, size_t n, uint32_t* __restrict__ out,
+                                 const uint32_t* __restrict__ primes, int K) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int64_t v = w[t];
+  for (int i = 0; i < K; ++i) {
+    int64_t r = v % (int64_t)primes[i];
+    if (r < 0) r += primes[i];
+    out[t * K + i] = (uint32_t)r;
+  }
+}
+
+// reference-order NTT (natural, a(psi^(2k+1))) -> device spectral order
+// in place on [rows][N] via a temp: dst[i] = src[brv(i)]
+__global__ void k_bitrev_rows(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, int N,
+                              int logn) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const size_t row = blockIdx.y;
+  const int r = __brev(i) >> (32 - logn);
+  dst[row * N + i] = src[row * N + r];
+}
+
+// u64 residues -> u32
+__global__ void k_narrow(const uint64_t* __restrict__ src, uint32_t* __restrict__ dst, size_t n) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = (uint32_t)src[i];
+}
+__global__ void k_widen(const uint32_t* __restrict__ src, uint64_t* __restrict__ dst, size_t n) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[i];
+}
+
+}  // namespace hcnn

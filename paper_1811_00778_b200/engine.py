@@ -1,0 +1,636 @@
+"""GPU drop-in for the reference's homomorphic network evaluator.
+
+Same functions, signatures, error behaviour, OpCounter and layer_hook
+semantics as hefir.engine (engine.py:61-85, 199-423); the arithmetic runs in
+libhcnn_b200.so (sm_100a) on device-resident limb-major u32 tensors.
+
+    eval_network(tensor, model, rlk, params, counter=None, workers=1,
+                 capacity=None, layer_hook=None)          engine.py:400-423
+    eval_conv / eval_fc / eval_square / eval_pool       engine.py:237-397
+
+`tensor` may be the reference's CipherTensor (host; uploaded, and the result
+downloaded back into the caller's own classes) or a GpuCipherTensor (stays on
+the device; `.cts` downloads lazily).  `workers` and `capacity` are accepted
+for signature compatibility; the GPU grid replaces the thread pool and the
+row-band blocking (capacity is still validated like plan_blocks,
+engine.py:109-112).  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import threading
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import (
+    CapacityError,
+    HefirError,
+    IncompleteResultError,
+    MissingKeyError,
+    ParameterMismatchError,
+)
+from .nn import kind_of
+
+_COUNTER_LOCK = threading.Lock()
+
+
+# ---------------------------------------------------------------- host types
+
+
+@dataclass
+class OpCounter:
+    """Scheduled multiply-accumulate work, matching the static audit
+    (engine.py:61-85)."""
+
+    mult_plain_scheduled: int = 0
+    mult_plain_executed: int = 0
+    mult_plain_skipped: int = 0
+    hsquare: int = 0
+    hadd: int = 0
+
+    def merge(self, other):
+        with _COUNTER_LOCK:
+            self.mult_plain_scheduled += other.mult_plain_scheduled
+            self.mult_plain_executed += other.mult_plain_executed
+            self.mult_plain_skipped += other.mult_plain_skipped
+            self.hsquare += other.hsquare
+            self.hadd += other.hadd
+
+
+@dataclass
+class CipherTensor:
+    """Host feature map: one ciphertext per (y, x, channel) (engine.py:42-58)."""
+
+    shape: tuple
+    cts: list
+    delta: int
+    channel_modulus: int
+
+    def __post_init__(self):
+        h, w, c = self.shape
+        if len(self.cts) != h * w * c:
+            raise HefirError("ciphertext count != h*w*c")
+
+    def at(self, y: int, x: int, ch: int):
+        h, w, c = self.shape
+        return self.cts[(y * w + x) * c + ch]
+
+
+@dataclass(frozen=True)
+class PackingLayout:
+    batch_size: int
+    slot_count: int
+
+    def __post_init__(self):
+        if self.batch_size > self.slot_count:
+            raise CapacityError(f"batch {self.batch_size} exceeds slot capacity {self.slot_count}")
+
+
+# ---------------------------------------------------------------- device context
+
+
+def _device_index(device) -> int:
+    if device is None:
+        return torch.cuda.current_device()
+    return torch.device(device).index or 0
+
+
+class GpuContext:
+    """libhcnn_b200 context for one BFV parameter set on one GPU."""
+
+    def __init__(self, params, device=None):
+        if not torch.cuda.is_available():
+            raise _lib.BackendError("CUDA device required: the evaluator has no CPU path")
+        self.device = _device_index(device)
+        self.params = params
+        ctx = params.ctx
+        self.primes = [int(pm.value) for pm in ctx.primes]
+        self.N = int(ctx.ring_degree)
+        self.K = len(self.primes)
+        self.t = int(params.t)
+        self.fingerprint = params.fingerprint
+        log2w = int(params.w).bit_length() - 1
+        arr = (_lib.C.c_uint64 * self.K)(*self.primes)
+        h = _lib.C.c_void_p()
+        L = _lib.lib()
+        with torch.cuda.device(self.device):
+            _lib.check(L.hcnn_ctx_create(_lib.C.byref(h), self.N, self.K, arr, self.t, log2w,
+                                         self.device), "hcnn_ctx_create")
+        self.handle = h
+        self.KP = int(L.hcnn_ctx_query(h, 2))
+        self.D = int(L.hcnn_ctx_query(h, 3))
+        self._rlk_ref = None
+        self._weights = {}
+        self._finalizer = weakref.finalize(self, L.hcnn_ctx_destroy, h)
+
+    # -- plumbing
+    def bind_stream(self):
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        _lib.check(_lib.lib().hcnn_ctx_set_stream(self.handle, _lib.C.c_void_p(s)))
+
+    def launches(self) -> int:
+        return int(_lib.lib().hcnn_ctx_query(self.handle, 6))
+
+    def empty(self, n: int, parts: int = 2) -> torch.Tensor:
+        return torch.empty((n, parts, self.K, self.N), dtype=torch.int32, device=f"cuda:{self.device}")
+
+    def set_workspace_limit(self, nbytes: int):
+        _lib.check(_lib.lib().hcnn_ctx_set_workspace_limit(self.handle, int(nbytes)))
+
+    # -- keys and weights
+    def set_relin_key(self, rlk):
+        """Upload RelinKey.components (NTT domain, reference order) once."""
+        if rlk is None:
+            raise MissingKeyError("relinearization key required")
+        if getattr(rlk, "fingerprint", self.fingerprint) != self.fingerprint:
+            raise ParameterMismatchError("object does not match parameter set")
+        if self._rlk_ref is not None and self._rlk_ref() is rlk:
+            return
+        comps = rlk.components
+        if len(comps) != self.D:
+            raise ParameterMismatchError("relinearization key has the wrong digit count")
+        host = np.ascontiguousarray(
+            np.stack([np.stack([k0.residues, k1.residues]) for k0, k1 in comps]).astype(np.uint64)
+        )
+        domain = 1
+        first = comps[0][0]
+        if getattr(first, "domain", None) is not None and getattr(first.domain, "value", "ntt") != "ntt":
+            domain = 0
+        self.bind_stream()
+        _lib.check(_lib.lib().hcnn_set_relin_key(self.handle, host.ctypes.data, domain),
+                   "hcnn_set_relin_key")
+        try:
+            self._rlk_ref = weakref.ref(rlk)
+        except TypeError:
+            self._rlk_ref = lambda r=rlk: r
+
+    def set_public_key(self, pk):
+        """Upload PublicKey (b_ntt, a_ntt; reference NTT order) once."""
+        if getattr(pk, "fingerprint", self.fingerprint) != self.fingerprint:
+            raise ParameterMismatchError("object does not match parameter set")
+        if getattr(self, "_pk_ref", None) is not None and self._pk_ref() is pk:
+            return
+        host = np.ascontiguousarray(np.stack([pk.b_ntt.residues, pk.a_ntt.residues]).astype(np.uint64))
+        self.bind_stream()
+        _lib.check(_lib.lib().hcnn_set_public_key(self.handle, host.ctypes.data, 1),
+                   "hcnn_set_public_key")
+        self._pk_ref = weakref.ref(pk)
+
+    def reduced_weights(self, weights) -> torch.Tensor:
+        """int weights -> device [count][K] residues mod q_i (cached)."""
+        w = np.asarray(weights)
+        if w.dtype == object:
+            w = np.array([int(x) for x in w.reshape(-1)], dtype=object)
+            big = max((abs(int(x)) for x in w), default=0)
+            if big >= (1 << 62):
+                w = np.array([[int(x) % p for p in self.primes] for x in w], dtype=np.int64)
+                key = ("pre", w.shape, hashlib.blake2b(w.tobytes(), digest_size=16).digest())
+                if key not in self._weights:
+                    self._weights[key] = torch.from_numpy(w.astype(np.int32)).to(f"cuda:{self.device}")
+                return self._weights[key]
+        w = np.ascontiguousarray(w.reshape(-1), dtype=np.int64)
+        key = (w.shape, hashlib.blake2b(w.tobytes(), digest_size=16).digest())
+        out = self._weights.get(key)
+        if out is None:
+            out = torch.empty((w.size, self.K), dtype=torch.int32, device=f"cuda:{self.device}")
+            self.bind_stream()
+            _lib.check(_lib.lib().hcnn_reduce_weights(self.handle, w.ctypes.data, w.size,
+                                                      out.data_ptr()), "hcnn_reduce_weights")
+            if len(self._weights) > 64:
+                self._weights.clear()
+            self._weights[key] = out
+        return out
+
+
+_CTXS: dict = {}
+
+
+def context_for(params, device=None) -> GpuContext:
+    key = (params.fingerprint, _device_index(device))
+    c = _CTXS.get(key)
+    if c is None:
+        c = GpuContext(params, device)
+        _CTXS[key] = c
+    return c
+
+
+# ---------------------------------------------------------------- device tensors
+
+
+class GpuCipherTensor:
+    """Feature map resident on the GPU: int32 view of u32 residues
+    [ct][part][limb][N], (y, x, c) row-major like CipherTensor."""
+
+    def __init__(self, shape, data: torch.Tensor, delta: int, channel_modulus: int, params,
+                 host_types=None):
+        h, w, c = shape
+        if data.shape[0] != h * w * c:
+            raise HefirError("ciphertext count != h*w*c")
+        self.shape = tuple(shape)
+        self.data = data
+        self.delta = delta
+        self.channel_modulus = channel_modulus
+        self.params = params
+        self.host_types = host_types
+        self._cts = None
+
+    def __len__(self):
+        return self.data.shape[0]
+
+    def residues(self) -> np.ndarray:
+        """u64 residues [ct][part][limb][N] on the host."""
+        torch.cuda.current_stream(self.data.device).synchronize()
+        return self.data.cpu().numpy().view(np.uint32).astype(np.uint64)
+
+    @property
+    def cts(self) -> list:
+        if self._cts is None:
+            self._cts = _to_host_cts(self.residues(), self.params, self.host_types)
+        return self._cts
+
+    def at(self, y: int, x: int, ch: int):
+        h, w, c = self.shape
+        return self.cts[(y * w + x) * c + ch]
+
+    def to_host(self):
+        cls = self.host_types[0] if self.host_types else CipherTensor
+        return cls(shape=self.shape, cts=self.cts, delta=self.delta,
+                   channel_modulus=self.channel_modulus)
+
+
+def _host_types_of(tensor, params):
+    if tensor.cts:
+        ct = tensor.cts[0]
+        elem = ct.parts[0]
+        return (type(tensor), type(ct), type(elem), elem.domain, elem.ctx)
+    return (type(tensor), None, None, None, params.ctx)
+
+
+def _to_host_cts(res: np.ndarray, params, host_types) -> list:
+    if host_types and host_types[1] is not None:
+        _, ct_cls, el_cls, dom, ctx = host_types
+    else:
+        from . import bfv as _b
+
+        ct_cls, el_cls, dom, ctx = _b.Ciphertext, _b.RingElem, _b.Domain.COEFF, params.ctx
+    res = res.astype(np.int64)
+    out = []
+    for i in range(res.shape[0]):
+        parts = tuple(el_cls(ctx, np.ascontiguousarray(res[i, p]), dom) for p in range(res.shape[1]))
+        out.append(ct_cls(parts=parts, fingerprint=params.fingerprint))
+    return out
+
+
+def upload(tensor, params, device=None) -> GpuCipherTensor:
+    """Host CipherTensor -> GpuCipherTensor (u64 residues narrowed to u32)."""
+    if isinstance(tensor, GpuCipherTensor):
+        return tensor
+    g = context_for(params, device)
+    for ct in tensor.cts:
+        if ct.fingerprint != params.fingerprint:
+            raise ParameterMismatchError("ciphertext does not match parameter set")
+        if len(ct.parts) != 2:
+            raise ParameterMismatchError("evaluator expects 2-part ciphertexts")
+    n = len(tensor.cts)
+    host = np.empty((n, 2, g.K, g.N), dtype=np.uint32)
+    for i, ct in enumerate(tensor.cts):
+        host[i, 0] = ct.parts[0].residues
+        host[i, 1] = ct.parts[1].residues
+    data = torch.from_numpy(host.view(np.int32)).pin_memory().to(f"cuda:{g.device}", non_blocking=True)
+    return GpuCipherTensor(tensor.shape, data, tensor.delta, tensor.channel_modulus, params,
+                           _host_types_of(tensor, params))
+
+
+def from_residues(res: np.ndarray, shape, delta, channel_modulus, params, device=None) -> GpuCipherTensor:
+    """u32/u64 residues [ct][2][K][N] (host) -> GpuCipherTensor."""
+    g = context_for(params, device)
+    host = np.ascontiguousarray(np.asarray(res).astype(np.uint32))
+    data = torch.from_numpy(host.view(np.int32)).to(f"cuda:{g.device}")
+    return GpuCipherTensor(shape, data, delta, channel_modulus, params)
+
+
+def _ptr(t: torch.Tensor):
+    return _lib.C.c_void_p(t.data_ptr())
+
+
+# ---------------------------------------------------------------- counters
+
+
+def _conv_counts(h, w, layer, weights):
+    f, kh, kw, cg = weights.shape
+    sh, sw = layer.stride
+    ph = (kh - 1) // 2 if layer.padded else 0
+    pw = (kw - 1) // 2 if layer.padded else 0
+    oh = (h + 2 * ph - kh) // sh + 1
+    ow = (w + 2 * pw - kw) // sw + 1
+    vy = np.array([[0 <= oy * sh + ky - ph < h for ky in range(kh)] for oy in range(oh)], dtype=np.int64)
+    vx = np.array([[0 <= ox * sw + kx - pw < w for kx in range(kw)] for ox in range(ow)], dtype=np.int64)
+    nz = (np.asarray(weights) != 0).sum(axis=3).astype(np.int64)
+    executed = np.einsum("ak,bl,fkl->abf", vy, vx, nz)
+    sched = int(np.einsum("ak,bl->", vy, vx)) * cg * f
+    ex = int(executed.sum())
+    hadd = int((executed[executed > 0] - 1).sum())
+    return sched, ex, hadd
+
+
+def _fc_counts(weights):
+    nz = (np.asarray(weights) != 0).sum(axis=1).astype(np.int64)
+    sched = int(np.asarray(weights).size)
+    ex = int(nz.sum())
+    hadd = int((nz[nz > 0] - 1).sum())
+    return sched, ex, hadd
+
+
+def _count(counter, sched, ex, hadd):
+    counter.mult_plain_scheduled += sched
+    counter.mult_plain_executed += ex
+    counter.mult_plain_skipped += sched - ex
+    counter.hadd += hadd
+
+
+# ---------------------------------------------------------------- layers
+
+
+def _as_gpu(tensor, params, device=None):
+    if tensor.channel_modulus != params.t:
+        raise ParameterMismatchError("tensor channel does not match params")
+    if isinstance(tensor, GpuCipherTensor):
+        return tensor, False
+    return upload(tensor, params, device), True
+
+
+def _ret(out: GpuCipherTensor, was_host: bool):
+    return out.to_host() if was_host else out
+
+
+def eval_conv(tensor, layer, weights, params, counter, workers: int = 1, capacity=None):
+    """Convolution layer (engine.py:237-303) on the GPU."""
+    h, w, c = tensor.shape
+    weights = np.asarray(weights)
+    f, kh, kw, cg = weights.shape
+    if c != cg * layer.groups:
+        raise ParameterMismatchError(f"{layer.name}: channel mismatch")
+    if tensor.channel_modulus != params.t:
+        raise ParameterMismatchError(f"{layer.name}: tensor channel != params")
+    if capacity is not None and capacity < kh * kw:
+        raise CapacityError(f"capacity {capacity} below filter size {kh * kw}")
+    src, was_host = _as_gpu(tensor, params)
+    g = context_for(params, src.data.device)
+    sh, sw = layer.stride
+    ph = (kh - 1) // 2 if layer.padded else 0
+    pw = (kw - 1) // 2 if layer.padded else 0
+    oh = (h + 2 * ph - kh) // sh + 1
+    ow = (w + 2 * pw - kw) // sw + 1
+    wred = g.reduced_weights(weights)
+    out = g.empty(oh * ow * f)
+    g.bind_stream()
+    _lib.check(_lib.lib().hcnn_conv(g.handle, _ptr(src.data), _ptr(out), h, w, c, _ptr(wred), f,
+                                    kh, kw, sh, sw, int(bool(layer.padded)), layer.groups),
+               layer.name)
+    _count(counter, *_conv_counts(h, w, layer, weights))
+    res = GpuCipherTensor((oh, ow, f), out, tensor.delta * layer.weight_scale, params.t, params,
+                          src.host_types)
+    return _ret(res, was_host)
+
+
+def eval_fc(tensor, layer, weights, params, counter, workers: int = 1):
+    """Dense layer over the (y, x, c)-flattened tensor (engine.py:306-334)."""
+    weights = np.asarray(weights)
+    outputs, in_count = weights.shape
+    n = tensor.shape[0] * tensor.shape[1] * tensor.shape[2]
+    if in_count != n:
+        raise ParameterMismatchError(f"{layer.name}: weight width != tensor size")
+    src, was_host = _as_gpu(tensor, params)
+    g = context_for(params, src.data.device)
+    wred = g.reduced_weights(weights)
+    out = g.empty(outputs)
+    g.bind_stream()
+    _lib.check(_lib.lib().hcnn_fc(g.handle, _ptr(src.data), _ptr(out), in_count, outputs, _ptr(wred)),
+               layer.name)
+    _count(counter, *_fc_counts(weights))
+    res = GpuCipherTensor((1, 1, outputs), out, tensor.delta * layer.weight_scale, params.t, params,
+                          src.host_types)
+    return _ret(res, was_host)
+
+
+def eval_square(tensor, rlk, params, counter, workers: int = 1):
+    """HSquare of every ciphertext: exact tensor, t/q rounding, base-w relin
+    (engine.py:337-364, bfv.py:435-443)."""
+    src, was_host = _as_gpu(tensor, params)
+    g = context_for(params, src.data.device)
+    n = len(src)
+    out = g.empty(n)
+    if n:
+        if rlk is None:
+            raise MissingKeyError("relinearization key required for hsquare")
+        g.set_relin_key(rlk)
+        g.bind_stream()
+        _lib.check(_lib.lib().hcnn_square(g.handle, _ptr(src.data), _ptr(out), n), "square")
+    counter.hsquare += n
+    res = GpuCipherTensor(src.shape, out, tensor.delta * tensor.delta, tensor.channel_modulus,
+                          params, src.host_types)
+    return _ret(res, was_host)
+
+
+def eval_pool(tensor, layer, params, counter):
+    """Sum-pool by window adds (engine.py:367-397)."""
+    h, w, c = tensor.shape
+    e = layer.extent
+    sh, sw = layer.stride
+    oh = (h - e) // sh + 1
+    ow = (w - e) // sw + 1
+    src, was_host = _as_gpu(tensor, params)
+    g = context_for(params, src.data.device)
+    out = g.empty(oh * ow * c)
+    g.bind_stream()
+    _lib.check(_lib.lib().hcnn_pool(g.handle, _ptr(src.data), _ptr(out), h, w, c, e, sh, sw),
+               layer.name)
+    counter.hadd += oh * ow * c * (e * e - 1)
+    res = GpuCipherTensor((oh, ow, c), out, tensor.delta * e * e, tensor.channel_modulus, params,
+                          src.host_types)
+    return _ret(res, was_host)
+
+
+def eval_network(tensor, model, rlk, params, counter=None, workers: int = 1, capacity=None,
+                 layer_hook=None):
+    """Evaluate every layer; returns the logits tensor (1, 1, outputs)
+    (engine.py:400-423).  Host input -> host output; GPU input -> GPU output;
+    layer_hook receives GpuCipherTensors (their .cts download on demand)."""
+    counter = counter if counter is not None else OpCounter()
+    x, was_host = _as_gpu(tensor, params)
+    for layer, weights in zip(model.spec.layers, model.weights):
+        k = kind_of(layer)
+        if k == "conv":
+            x = eval_conv(x, layer, weights, params, counter, workers, capacity)
+        elif k == "square":
+            x = eval_square(x, rlk, params, counter, workers)
+        elif k == "pool":
+            x = eval_pool(x, layer, params, counter)
+        elif k == "fc":
+            x = eval_fc(x, layer, weights, params, counter, workers)
+        if layer_hook is not None:
+            layer_hook(layer.name, x)
+    return _ret(x, was_host)
+
+
+# ---------------------------------------------------------------- client side
+
+
+def pack_images(images, layout: PackingLayout, encoder, pk, params, rng, delta: int):
+    """Encrypt position i of every image into slot-aligned ciphertext i
+    (engine.py:146-175); host client code, uses the bfv module's encrypt."""
+    from . import bfv as _b
+
+    if len(images) != layout.batch_size:
+        raise CapacityError("image count != layout batch size")
+    if layout.slot_count != params.ring_degree:
+        raise ParameterMismatchError("layout slots != ring degree")
+    shape = tuple(np.asarray(images[0]).shape)
+    stack = np.stack([np.asarray(im, dtype=np.int64) for im in images])
+    if stack.shape[1:] != shape:
+        raise HefirError("images disagree on shape")
+    t = params.t
+    flat = stack.reshape(layout.batch_size, -1) % t
+    slots = np.zeros((flat.shape[1], layout.slot_count), dtype=np.int64)
+    slots[:, : layout.batch_size] = flat.T
+    if hasattr(encoder, "encode_many"):
+        polys = encoder.encode_many(slots)
+    else:
+        polys = np.stack([encoder.encode(s).poly for s in slots])
+    cts = [_b.encrypt(pk, _b.Plaintext(polys[i], t), params, rng) for i in range(len(polys))]
+    h, w = shape[0], shape[1]
+    c = shape[2] if len(shape) == 3 else 1
+    return CipherTensor(shape=(h, w, c), cts=cts, delta=delta, channel_modulus=t)
+
+
+def draw_encryption_noise(rng, count: int, n: int):
+    """(u, e1, e2) for `count` successive encryptions, in the reference's draw
+    order (bfv.py:205-209)."""
+    from .bfv import _gauss
+
+    u = np.empty((count, n), dtype=np.int8)
+    e1 = np.empty((count, n), dtype=np.int8)
+    e2 = np.empty((count, n), dtype=np.int8)
+    for i in range(count):
+        u[i] = rng.integers(0, 2, n, dtype=np.int64)
+        e1[i] = _gauss(rng, n)
+        e2[i] = _gauss(rng, n)
+    return u, e1, e2
+
+
+def encrypt_device(pk, polys, params, rng, device=None) -> torch.Tensor:
+    """Encrypt plaintext polys [P][N] (in [0, t)) on the GPU; same bytes as P
+    successive bfv.encrypt calls with this rng (bfv.py:201-216)."""
+    g = context_for(params, device)
+    g.set_public_key(pk)
+    polys = np.ascontiguousarray(np.asarray(polys, dtype=np.int64))
+    if polys.ndim != 2 or polys.shape[1] != g.N:
+        raise ParameterMismatchError("plaintext length != ring degree")
+    if (polys < 0).any() or (polys >= params.t).any():
+        from .errors import EncodingError
+
+        raise EncodingError("plaintext coefficient outside [0, t)")
+    u, e1, e2 = draw_encryption_noise(rng, polys.shape[0], g.N)
+    out = g.empty(polys.shape[0])
+    g.bind_stream()
+    _lib.check(_lib.lib().hcnn_encrypt(g.handle, u.ctypes.data, e1.ctypes.data, e2.ctypes.data,
+                                       polys.ctypes.data, _ptr(out), polys.shape[0]), "hcnn_encrypt")
+    return out
+
+
+def pack_images_device(images, layout: PackingLayout, encoder, pk, params, rng, delta: int,
+                       device=None) -> GpuCipherTensor:
+    """pack_images (engine.py:146-175) with the encryption on the GPU: returns
+    the same ciphertexts, resident on the device."""
+    if len(images) != layout.batch_size:
+        raise CapacityError("image count != layout batch size")
+    if layout.slot_count != params.ring_degree:
+        raise ParameterMismatchError("layout slots != ring degree")
+    shape = tuple(np.asarray(images[0]).shape)
+    stack = np.stack([np.asarray(im, dtype=np.int64) for im in images])
+    flat = stack.reshape(layout.batch_size, -1) % params.t
+    slots = np.zeros((flat.shape[1], layout.slot_count), dtype=np.int64)
+    slots[:, : layout.batch_size] = flat.T
+    polys = encoder.encode_many(slots)
+    data = encrypt_device(pk, polys, params, rng, device)
+    h, w = shape[0], shape[1]
+    c = shape[2] if len(shape) == 3 else 1
+    return GpuCipherTensor((h, w, c), data, delta, params.t, params)
+
+
+def unpack_tensor(tensor, sk, encoder, params, batch_size: int) -> np.ndarray:
+    """Decrypt and decode to per-image values (batch, h*w*c) (engine.py:178-192)."""
+    from . import bfv as _b
+
+    if tensor.channel_modulus != params.t:
+        raise ParameterMismatchError("tensor channel does not match params")
+    out = np.zeros((batch_size, len(tensor.cts)), dtype=np.int64)
+    for pos, ct in enumerate(tensor.cts):
+        out[:, pos] = encoder.decode(_b.decrypt(sk, ct, params)).values[:batch_size]
+    return out
+
+
+def reduce_model(model, t: int):
+    """Weights centred mod t (engine.py:442-456)."""
+    from .nn import QuantizedModel
+
+    half = t // 2
+    reduced = []
+    for w in model.weights:
+        if w is None:
+            reduced.append(None)
+            continue
+        r = np.asarray(w, dtype=np.int64) % t
+        reduced.append(np.where(r > half, r - t, r))
+    return QuantizedModel(spec=model.spec, bit_width=model.bit_width, weights=reduced)
+
+
+@dataclass
+class ChannelResult:
+    moduli: tuple
+    batch_size: int
+    residues: dict = None
+
+    def __post_init__(self):
+        if self.residues is None:
+            self.residues = {}
+
+    def add(self, t: int, logits: np.ndarray):
+        self.residues[t] = logits
+
+
+def reconstruct_logits(result, crt_moduli) -> np.ndarray:
+    """Signed logits from per-channel residues (engine.py:494-506)."""
+    moduli = tuple(getattr(crt_moduli, "moduli", crt_moduli))
+    for t in moduli:
+        if t not in result.residues:
+            raise IncompleteResultError(f"missing CRT channel t={t}")
+    total = 1
+    for t in moduli:
+        total *= t
+    any_mat = next(iter(result.residues.values()))
+    outputs, batch = any_mat.shape
+    logit = np.zeros((batch, outputs), dtype=object)
+    for o in range(outputs):
+        for b in range(batch):
+            acc = 0
+            for t in moduli:
+                big = total // t
+                acc += int(result.residues[t][o, b]) * big * pow(big % t, -1, t)
+            v = acc % total
+            logit[b, o] = v if v <= total // 2 else v - total
+    return logit
+
+
+def classify_logits(logits) -> list:
+    """Per-image argmax, lowest index on ties (engine.py:509-515)."""
+    out = []
+    for row in logits:
+        vals = list(row)
+        out.append(vals.index(max(vals)))
+    return out
