@@ -1,0 +1,102 @@
+#!/usr/bin/env python3
+"""Kernel microbenchmark (BASELINE.json config 2): RNS NTT/INTT and ct x ct
+multiply + relinearise over N = 2^13..2^15 and RNS limb counts, on 1 B200.
+
+Each line is one JSON object: per-kernel CUDA-event times (hcnn_profile) and
+achieved rates.  Primes: the reference pool (= 1 mod 2^15) for N <= 2^14 and
+primes = 1 mod 2^16 below 2^30 for N = 2^15 (the pool does not qualify).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+POOL = (1073643521, 1073479681, 1073184769, 1073053697, 1072857089, 1072496641,
+        1071513601, 1071415297, 1071087617, 1070727169, 1070432257, 1069219841)
+
+
+def primes_1mod(two_n: int, count: int, avoid=()):
+    from paper_1811_00778_b200.bfv import is_prime
+
+    out, k = [], 1
+    while len(out) < count:
+        p = (1 << 30) - k * two_n + 1
+        k += 1
+        if p not in avoid and is_prime(p):
+            out.append(p)
+    return out
+
+
+def main():
+    import torch
+
+    from paper_1811_00778_b200 import bfv as B
+    from paper_1811_00778_b200 import engine as E
+    from paper_1811_00778_b200 import ops
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--ns", default="8192,16384,32768")
+    ap.add_argument("--ks", default="6,11,12")
+    ap.add_argument("--cts", type=int, default=128)
+    ap.add_argument("--rows", type=int, default=4096)
+    ap.add_argument("--variants", default="0")
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    t = 5522259017729
+    for n in [int(x) for x in a.ns.split(",")]:
+        for k in [int(x) for x in a.ks.split(",")]:
+            primes = list(POOL[:k]) if n <= 16384 else primes_1mod(2 * n, k)
+            tt = t if (t - 1) % (2 * n) == 0 else 65537 if n <= 32768 else 65537
+            params = B.BfvParams(B.RnsContext(n, primes), tt)
+            for variant in [int(v) for v in a.variants.split(",")]:
+                os.environ["HCNN_NTT_VARIANT"] = str(variant)
+                E._CTXS.clear()
+                g = E.context_for(params)
+                sk, pk, rlk = B.keygen(params, np.random.default_rng(1))
+                rng = np.random.default_rng(2)
+                x = torch.from_numpy(
+                    np.stack([np.stack([rng.integers(0, p, n) for p in primes]) for _ in range(2 * a.cts)])
+                    .reshape(a.cts, 2, k, n).astype(np.uint32).view(np.int32)).cuda()
+                rows = torch.from_numpy(
+                    np.stack([rng.integers(0, primes[i % k], n) for i in range(a.rows)]).astype(np.uint32).view(np.int32)).cuda()
+                ops.square_device(g, x, rlk)  # warm-up + key upload
+                ops.ntt_device(g, rows, k)
+                torch.cuda.synchronize()
+                g.profile(True)
+                for _ in range(a.reps):
+                    ops.ntt_device(g, rows, k)
+                    ops.ntt_device(g, rows, k, inverse=True)
+                    ops.square_device(g, x, rlk)
+                torch.cuda.synchronize()
+                prof = g.profile_read()
+                g.profile(False)
+                logn = n.bit_length() - 1
+                bfly = n // 2 * logn
+                line = {"n": n, "k": k, "kp": g.KP, "digits": g.D, "variant": variant, "cts": a.cts,
+                        "ntt_rows": a.rows}
+                cnt, tot = prof["k_ntt_rows"]
+                per = tot / cnt  # ms per launch (fwd or inv of `rows` rows)
+                line["ntt_row_us"] = round(per * 1e3 / a.rows, 4)
+                line["ntt_gbfly_s"] = round(a.rows * bfly / (per * 1e-3) / 1e9, 1)
+                line["ntt_hbm_gbs"] = round(a.rows * n * 8 / (per * 1e-3) / 1e9, 1)
+                hsq = 0.0
+                for name in ("k_extend", "k_tensor", "k_scale", "k_relin"):
+                    c_, t_ = prof[name]
+                    us = t_ / a.reps / a.cts * 1e3
+                    line[name + "_us_per_ct"] = round(us, 3)
+                    hsq += us
+                line["hsquare_us_per_ct"] = round(hsq, 3)
+                line["hsquare_bfly_gs"] = round((5 * (k + g.KP) + (g.D + 2) * k) * bfly / (hsq * 1e-6) / 1e9, 1)
+                print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -60,8 +60,13 @@ enum {
   HCNN_Q_DIGITS = 3,   /* l + 1 relinearisation digits (bfv.py:70-76) */
   HCNN_Q_LOG2W = 4,
   HCNN_Q_WS_BYTES = 5, /* workspace currently held */
-  HCNN_Q_KERNELS = 6   /* kernels launched since creation */
+  HCNN_Q_KERNELS = 6,  /* kernels launched since creation */
+  HCNN_Q_NTT_VARIANT = 7
 };
+/* Tuning options.  HCNN_OPT_NTT_VARIANT: log2 of the residues each thread
+ * keeps in the fused NTT kernels (0 = default per ring degree, 4 or 5). */
+enum { HCNN_OPT_NTT_VARIANT = 1 };
+int hcnn_ctx_set_option(hcnn_ctx* ctx, int key, int64_t value);
 int64_t hcnn_ctx_query(hcnn_ctx* ctx, int what);
 /* psi (primitive 2N-th root) of prime i, i < K + KP (ntt.py:50-60) */
 uint64_t hcnn_ctx_prime(hcnn_ctx* ctx, int i, uint64_t* psi);

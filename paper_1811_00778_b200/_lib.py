@@ -23,6 +23,7 @@ _SIGS = {
     "hcnn_ctx_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "hcnn_ctx_query": (C.c_int64, [C.c_void_p, C.c_int]),
     "hcnn_ctx_prime": (C.c_uint64, [C.c_void_p, C.c_int, C.POINTER(C.c_uint64)]),
+    "hcnn_ctx_set_option": (C.c_int, [C.c_void_p, C.c_int, C.c_int64]),
     "hcnn_ctx_set_workspace_limit": (C.c_int, [C.c_void_p, C.c_size_t]),
     "hcnn_set_relin_key": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
     "hcnn_set_public_key": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),

@@ -16,6 +16,7 @@ CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(os.path.dirname(PKG), "build", "hcnn")
 LIB = os.path.join(PKG, "libhcnn_b200.so")
 LOGNS = list(range(2, 16))
+KS = list(range(1, 17))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -50,8 +51,14 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
     for L in LOGNS:
         units.append((os.path.join(CSRC, "ntt_inst.cu"), os.path.join(BUILD, f"ntt_{L}.o"),
                       [f"-DHCNN_LOGN={L}"]))
+    for K in KS:
+        units.append((os.path.join(CSRC, "conv_inst.cu"), os.path.join(BUILD, f"conv_{K}.o"),
+                      [f"-DHCNN_K={K}"]))
     # biggest units first
     units.sort(key=lambda u: -int(u[2][0].split("=")[1]) if u[2] else -99)
+    for stale in os.listdir(BUILD):
+        if stale.endswith(".o") and os.path.join(BUILD, stale) not in [u[1] for u in units]:
+            os.remove(os.path.join(BUILD, stale))
     jobs = jobs or os.cpu_count() or 4
     with concurrent.futures.ThreadPoolExecutor(jobs) as ex:
         objs = list(ex.map(_compile, units))

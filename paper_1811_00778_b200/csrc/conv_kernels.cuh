@@ -1,0 +1,185 @@
+// Exact RNS base-conversion kernels of the multiplication path, templated on
+// the number of primes of q (K) and of the auxiliary base (KP = K+2 or K+3),
+// one translation unit per K (conv_inst.cu).
+//
+//   k_extend  Q -> P extension of canonical lifts            (ring.py:286-295)
+//   k_scale   exact round(t d / q) mod q of the 3-part tensor (bfv.py:325-328)
+//             + base-w digits of the canonical c2           (bfv.py:350-365)
+//   k_digits  base-w digits of part 2 of a 3-part ct         (bfv.py:350-365)
+#pragma once
+#include "common.cuh"
+
+namespace hcnn {
+
+struct ConvLaunch {
+  cudaStream_t stream;
+  dim3 grid, block;
+  const uint32_t* in;
+  uint32_t* out;
+  uint32_t* dig;
+  int N;
+};
+
+// write the D base-2^db digits of the canonical value held in S
+template <int K>
+DI void store_digits(const uint32_t (&S)[words_for(K)], uint32_t* __restrict__ dd, int N,
+                     const ConvTabs& tb) {
+  const int db = tb.digit_bits;
+  const uint32_t mask = db == 32 ? 0xffffffffu : ((1u << db) - 1);
+  if (db == 16) {
+#pragma unroll
+    for (int w = 0; w < words_for(K); ++w) {
+      if (2 * w < tb.D) dd[(size_t)(2 * w) * N] = S[w] & 0xffffu;
+      if (2 * w + 1 < tb.D) dd[(size_t)(2 * w + 1) * N] = S[w] >> 16;
+    }
+    return;
+  }
+#pragma unroll
+  for (int w = 0; w < words_for(K); ++w) {
+    const int per = 32 / db;
+#pragma unroll 4
+    for (int k = 0; k < per; ++k) {
+      const int d = w * per + k;
+      if (d < tb.D) dd[(size_t)d * N] = (S[w] >> (k * db)) & mask;
+    }
+  }
+}
+
+// in: [B][2][K][N] canonical residues; ext: [B][2][KP][N]
+template <int K, int KP>
+__global__ void __launch_bounds__(128)
+    k_extend(const uint32_t* __restrict__ in, uint32_t* __restrict__ ext, int N,
+             const __grid_constant__ ConvTabs tb) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  const size_t poly = blockIdx.y;  // ct * 2 + part
+  const uint32_t* src = in + poly * K * N + n;
+  uint32_t x[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) x[i] = src[(size_t)i * N];
+  uint32_t xt[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) xt[i] = mul_shoup(x[i], tb.qhi[i], tb.qhis[i], tb.q[i]);
+  const uint32_t v = exact_v<K>(xt, tb);
+  uint32_t* dst = ext + poly * KP * N + n;
+#pragma unroll
+  for (int j = 0; j < KP; ++j) dst[(size_t)j * N] = q_to_p<K>(xt, v, j, tb);
+}
+
+// d: [B][3][K+KP][N] exact tensor residues (coefficient domain).
+// y3: [B][3][K][N] = round(t d / q) mod q per part; dig (optional): [B][D][N].
+template <int K, int KP>
+__global__ void __launch_bounds__(128)
+    k_scale(const uint32_t* __restrict__ d, uint32_t* __restrict__ y3, uint32_t* __restrict__ dig,
+            int N, const __grid_constant__ ConvTabs tb) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  const int part = blockIdx.y % 3;
+  const size_t ct = blockIdx.y / 3;
+  const uint32_t* src = d + (size_t)blockIdx.y * (K + KP) * N + n;
+  uint32_t dq[K], dp[KP];
+#pragma unroll
+  for (int i = 0; i < K; ++i) dq[i] = src[(size_t)i * N];
+#pragma unroll
+  for (int j = 0; j < KP; ++j) dp[j] = src[(size_t)(K + j) * N];
+
+  // r = (t d + h) mod q, h = (q-1)/2, held as r~_i = r_i (q/q_i)^-1 mod q_i
+  uint32_t rt[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) rt[i] = add_mod(mul_shoup(dq[i], tb.A[i], tb.As[i], tb.q[i]), tb.B[i], tb.q[i]);
+  const uint32_t v = exact_v<K>(rt, tb);
+
+  // y = (t d + h - r) / q exactly, in P (centred, |y| < P/4): y~_j = y_j (P/p_j)^-1
+  uint32_t yt[KP];
+  uint64_t F = 0;
+#pragma unroll
+  for (int j = 0; j < KP; ++j) {
+    const uint32_t pj = tb.p[j];
+    const uint32_t rj = q_to_p<K>(rt, v, j, tb);
+    uint32_t acc = add_mod(mul_shoup(dp[j], tb.C[j], tb.Cs[j], pj), mul_shoup(pj - rj, tb.Ej[j], tb.Ejs[j], pj), pj);
+    acc = add_mod(acc, tb.F[j], pj);
+    yt[j] = acc;
+    F += frac60(acc, tb.pG[j], tb.pb[j]);
+  }
+  const uint32_t vp = (uint32_t)((F + (FRAC_ONE >> 1)) >> 60);
+
+  // back to Q: y_i = (sum_j y~_j (P/p_j) - vp P) mod q_i
+  uint32_t yq[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    uint64_t acc = (uint64_t)vp * tb.negp_q[i];
+#pragma unroll
+    for (int j = 0; j < KP; ++j) acc += (uint64_t)yt[j] * tb.phat_q[j][i];
+    yq[i] = reduce64(acc, tb.q[i], tb.qmu[i]);
+  }
+  uint32_t* dst = y3 + (size_t)blockIdx.y * K * N + n;
+#pragma unroll
+  for (int i = 0; i < K; ++i) dst[(size_t)i * N] = yq[i];
+
+  if (part != 2 || dig == nullptr) return;
+  // canonical binary of y_2 mod q, then base-w digits
+  uint32_t xt[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) xt[i] = mul_shoup(yq[i], tb.qhi[i], tb.qhis[i], tb.q[i]);
+  uint64_t Fq = 0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) Fq += frac60(xt[i], tb.qG[i], tb.qb[i]);
+  uint32_t S[words_for(K)];
+  mw_lift<K>(xt, tb, S);
+  mw_sub_mq<K>(S, (uint32_t)(Fq >> 60), tb);  // S - V q >= 0 with V in {v-1, v}
+  {
+    uint32_t Tq[words_for(K)];
+#pragma unroll
+    for (int w = 0; w < words_for(K); ++w) Tq[w] = S[w];
+    if (!mw_sub_mq<K>(Tq, 1, tb)) {
+#pragma unroll
+      for (int w = 0; w < words_for(K); ++w) S[w] = Tq[w];
+    }
+  }
+  store_digits<K>(S, dig + ct * tb.D * N + n, N, tb);
+}
+
+// digits of part 2 of a 3-part tensor in3: [B][3][K][N] -> dig [B][D][N]
+template <int K>
+__global__ void __launch_bounds__(128)
+    k_digits(const uint32_t* __restrict__ in3, uint32_t* __restrict__ dig, int N,
+             const __grid_constant__ ConvTabs tb) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  const size_t ct = blockIdx.y;
+  const uint32_t* src = in3 + (ct * 3 + 2) * K * N + n;
+  uint32_t xt[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) xt[i] = mul_shoup(src[(size_t)i * N], tb.qhi[i], tb.qhis[i], tb.q[i]);
+  const uint32_t v = exact_v<K>(xt, tb);
+  uint32_t S[words_for(K)];
+  mw_lift<K>(xt, tb, S);
+  mw_sub_mq<K>(S, v, tb);
+  store_digits<K>(S, dig + ct * tb.D * N + n, N, tb);
+}
+
+// op: 0 extend, 1 scale, 2 digits
+template <int K, int KP>
+cudaError_t conv_launch(int op, const ConvLaunch& a, const ConvTabs& tb) {
+  switch (op) {
+    case 0:
+      k_extend<K, KP><<<a.grid, a.block, 0, a.stream>>>(a.in, a.out, a.N, tb);
+      break;
+    case 1:
+      k_scale<K, KP><<<a.grid, a.block, 0, a.stream>>>(a.in, a.out, a.dig, a.N, tb);
+      break;
+    case 2:
+      k_digits<K><<<a.grid, a.block, 0, a.stream>>>(a.in, a.dig, a.N, tb);
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace hcnn
+
+#define HCNN_K_LIST(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
+#define HCNN_DECLARE_CONV(K) \
+  cudaError_t hcnn_conv_launch_##K(int op, int kp, const hcnn::ConvLaunch& a, const hcnn::ConvTabs& tb);
+HCNN_K_LIST(HCNN_DECLARE_CONV)

@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "../../include/hcnn_b200.h"
+#include "conv_kernels.cuh"
 #include "kernels.cuh"
 #include "ntt_kernels.cuh"
 #include "tables.hpp"
@@ -60,8 +61,15 @@ struct hcnn_ctx {
   uint2* d_tw = nullptr;
   uint2* d_itw = nullptr;
   uint2* d_ninv = nullptr;
-  uint32_t* d_rlk = nullptr;
+  uint32_t* d_pinv = nullptr;
+  uint32_t* d_rlk = nullptr;      // NTT domain, tiled layout of `keys_variant`
+  uint32_t* d_rlk_raw = nullptr;  // as uploaded (domain rlk_domain)
+  int rlk_domain = 0;
   uint32_t* d_pk = nullptr;
+  uint32_t* d_pk_raw = nullptr;
+  int pk_domain = 0;
+  int variant = 0;       // NTT radix variant of the fused kernels (0 = default)
+  int keys_variant = -1; // variant the tiled keys were laid out for
   uint2* d_delta = nullptr;
   bool rlk_reduce = false;
   uint8_t* ws = nullptr;
@@ -143,20 +151,21 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
   }
   if (c->D > (uint32_t)DMAX) fail(HCNN_ERR_UNSUPPORTED, "too many relinearisation digits");
   // auxiliary base: P > 8 t N q + 4 so that round(t d / q) is centred in P
-  // with |y| < P/4 (exact rounding, no ambiguity)
+  // with |y| < P/4 (exact rounding, no ambiguity).  KP = K+2 covers t below
+  // ~2^45 with 30-bit primes; K+3 is always enough (t < 2^64, N <= 2^15).
   Big bound = mul_small(mul_small(mul_small(Q, t), N), 8);
   bound = add(bound, Big(4));
   std::vector<u64> P;
   Big Pp(1);
   {
-    std::vector<u64> cand = aux_primes(q, KPMAX + 1);
+    std::vector<u64> cand = aux_primes(q, c->K + 3);
     for (u64 p : cand) {
-      if (cmp(Pp, bound) > 0) break;
+      if (P.size() >= c->K + 2 && cmp(Pp, bound) > 0) break;
       P.push_back(p);
       Pp = mul_small(Pp, p);
     }
     if (cmp(Pp, bound) <= 0 || P.size() > (size_t)KPMAX)
-      fail(HCNN_ERR_UNSUPPORTED, "auxiliary base would need more than 16 primes");
+      fail(HCNN_ERR_UNSUPPORTED, "auxiliary base too small for this t");
   }
   c->KP = (uint32_t)P.size();
   c->primes = q;
@@ -167,6 +176,7 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
   std::vector<uint32_t> hp(L);
   std::vector<uint64_t> hmu(L);
   std::vector<uint2> htw((size_t)L * N), hitw((size_t)L * N), hninv(L);
+  std::vector<uint32_t> hpinv(L);
   c->psi.resize(L);
   for (uint32_t j = 0; j < L; ++j) {
     const u64 p = c->primes[j];
@@ -175,6 +185,11 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
     c->psi[j] = psi;
     hp[j] = (uint32_t)p;
     hmu[j] = (uint64_t)(((u128)1 << 64) / p);
+    {
+      uint32_t inv = 1;  // Newton iteration for p^-1 mod 2^32
+      for (int it = 0; it < 5; ++it) inv *= 2u - (uint32_t)p * inv;
+      hpinv[j] = (uint32_t)(0u - inv);
+    }
     std::vector<u64> pw(N), ipw(N);
     pw[0] = ipw[0] = 1;
     for (uint32_t i = 1; i < N; ++i) {
@@ -251,18 +266,32 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
   CK(cudaMalloc(&c->d_tw, (size_t)L * N * sizeof(uint2)));
   CK(cudaMalloc(&c->d_itw, (size_t)L * N * sizeof(uint2)));
   CK(cudaMalloc(&c->d_ninv, L * sizeof(uint2)));
+  CK(cudaMalloc(&c->d_pinv, L * sizeof(uint32_t)));
+  CK(cudaMemcpy(c->d_pinv, hpinv.data(), L * sizeof(uint32_t), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_prime, hp.data(), L * sizeof(uint32_t), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_mu, hmu.data(), L * sizeof(uint64_t), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_tw, htw.data(), (size_t)L * N * sizeof(uint2), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_itw, hitw.data(), (size_t)L * N * sizeof(uint2), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_ninv, hninv.data(), L * sizeof(uint2), cudaMemcpyHostToDevice));
-  c->nt = NttTabs{c->d_prime, c->d_mu, c->d_tw, c->d_itw, c->d_ninv};
+  c->nt = NttTabs{c->d_prime, c->d_mu, c->d_tw, c->d_itw, c->d_ninv, c->d_pinv};
 }
 
 // ---------------------------------------------------------------- dispatch
+int variant_mont(hcnn_ctx* c, int v) {
+  switch (c->logN) {
+#define X(L) \
+  case L:    \
+    return hcnn_ntt_mont_##L(v);
+    HCNN_LOGN_LIST(X)
+#undef X
+  }
+  return 0;
+}
+
 void ntt_dispatch(hcnn_ctx* c, int op, NttLaunch& a, const char* what) {
   a.stream = c->stream;
   a.nt = c->nt;
+  a.variant = c->variant;
   cudaError_t e;
   switch (c->logN) {
 #define X(L)                              \
@@ -275,7 +304,7 @@ void ntt_dispatch(hcnn_ctx* c, int op, NttLaunch& a, const char* what) {
       fail(HCNN_ERR_UNSUPPORTED, "ring degree");
   }
   c->launched(what);
-  (void)e;
+  check_cuda(e, what);
 }
 
 void launch_ntt_rows(hcnn_ctx* c, uint32_t* rows, size_t n_rows, int limbs, int off, int inverse) {
@@ -304,8 +333,12 @@ void launch_tensor(hcnn_ctx* c, const uint32_t* a_, const uint32_t* ae, const ui
   ntt_dispatch(c, 1, a, "k_tensor");
 }
 
+void prepare_keys(hcnn_ctx* c);
+
 void launch_relin(hcnn_ctx* c, const uint32_t* dig, const uint32_t* y3, uint32_t* out, size_t nct) {
+  prepare_keys(c);
   NttLaunch a{};
+  a.rlk_mont = variant_mont(c, c->variant);
   a.grid = dim3(c->K, (unsigned)nct);
   a.dig = dig;
   a.y3 = y3;
@@ -337,6 +370,24 @@ size_t chunk_cts(hcnn_ctx* c, size_t n, bool general) {
   return ch < n ? ch : n;
 }
 
+void conv_dispatch(hcnn_ctx* c, int op, ConvLaunch& a, const char* what) {
+  a.stream = c->stream;
+  a.N = (int)c->N;
+  cudaError_t e = cudaErrorInvalidValue;
+  switch (c->K) {
+#define X(KK)                                                \
+  case KK:                                                   \
+    e = hcnn_conv_launch_##KK(op, (int)c->KP, a, c->tabs);   \
+    break;
+    HCNN_K_LIST(X)
+#undef X
+    default:
+      fail(HCNN_ERR_UNSUPPORTED, "prime count");
+  }
+  c->launched(what);
+  check_cuda(e, what);
+}
+
 // a (and b) -> out3 (3-part scaled) and, if dig, the digits of part 2
 void mul_chunk(hcnn_ctx* c, const uint32_t* a, const uint32_t* b, size_t nct, uint32_t* y3,
                uint32_t* dig, uint8_t* ws) {
@@ -346,15 +397,23 @@ void mul_chunk(hcnn_ctx* c, const uint32_t* a, const uint32_t* b, size_t nct, ui
   uint32_t* be = square ? ae : ae + nct * 2 * KP * N;
   uint32_t* d = be + nct * 2 * KP * N;
   const unsigned tpb = 128;
-  k_extend<<<dim3(cdiv(N, tpb), (unsigned)(nct * 2)), tpb, 0, c->stream>>>(a, ae, (int)N, c->tabs);
-  c->launched("k_extend");
+  ConvLaunch ca{};
+  ca.block = dim3(tpb);
+  ca.grid = dim3(cdiv(N, tpb), (unsigned)(nct * 2));
+  ca.in = a;
+  ca.out = ae;
+  conv_dispatch(c, 0, ca, "k_extend");
   if (!square) {
-    k_extend<<<dim3(cdiv(N, tpb), (unsigned)(nct * 2)), tpb, 0, c->stream>>>(b, be, (int)N, c->tabs);
-    c->launched("k_extend");
+    ca.in = b;
+    ca.out = be;
+    conv_dispatch(c, 0, ca, "k_extend");
   }
   launch_tensor(c, a, ae, b, be, d, nct, square ? 1 : 0);
-  k_scale<<<dim3(cdiv(N, tpb), (unsigned)(nct * 3)), tpb, 0, c->stream>>>(d, y3, dig, (int)N, c->tabs);
-  c->launched("k_scale");
+  ca.grid = dim3(cdiv(N, tpb), (unsigned)(nct * 3));
+  ca.in = d;
+  ca.out = y3;
+  ca.dig = dig;
+  conv_dispatch(c, 1, ca, "k_scale");
   (void)K;
 }
 
@@ -383,35 +442,6 @@ void multiply(hcnn_ctx* c, const uint32_t* a, const uint32_t* b, size_t n, uint3
   }
 }
 
-// digits of part 2 of a 3-part tensor (for hcnn_relinearize)
-__global__ void k_digits(const uint32_t* __restrict__ in3, uint32_t* __restrict__ dig, int N,
-                         const __grid_constant__ ConvTabs tb) {
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= N) return;
-  const size_t ct = blockIdx.y;
-  const uint32_t* src = in3 + (ct * 3 + 2) * tb.K * N + n;
-  uint32_t xt[KMAX];
-#pragma unroll
-  for (int i = 0; i < KMAX; ++i)
-    if (i < tb.K) xt[i] = mul_shoup(src[(size_t)i * N], tb.qhi[i], tb.qhis[i], tb.q[i]);
-  const uint32_t v = exact_v(xt, tb);
-  uint32_t S[WMAX];
-  mw_lift(xt, tb, S);
-  mw_sub_mq(S, v, tb);
-  uint32_t* dd = dig + ct * tb.D * N + n;
-  const int db = tb.digit_bits;
-  const uint32_t mask = db == 32 ? 0xffffffffu : ((1u << db) - 1);
-  for (int k = 0; k < tb.D; ++k) {
-    const int bit = k * db;
-    const int wi = bit >> 5, sh = bit & 31;
-    uint32_t word = 0;
-#pragma unroll
-    for (int w = 0; w < WMAX; ++w)
-      if (w == wi) word = S[w];
-    dd[(size_t)k * N] = (word >> sh) & mask;
-  }
-}
-
 __global__ void k_hadd(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
                        uint32_t* __restrict__ out, int K, int N, size_t total,
                        const uint32_t* __restrict__ primes) {
@@ -434,9 +464,17 @@ __global__ void k_int_peak(uint32_t* out, uint32_t a, uint32_t b, int iters) {
         x[i] = x[i] * a + b;
       } else if (KIND == 1) {
         x[i] = __umulhi(x[i], a) + b;
-      } else {
+      } else if (KIND == 2) {
         const uint64_t w = (uint64_t)x[i] * a + b;
         x[i] = (uint32_t)(w >> 32) + (uint32_t)w;
+      } else if (KIND == 3) {  // add + unsigned min (VIADDMNMX)
+        const uint32_t y = x[i] - a;
+        x[i] = (y < x[i] ? y : x[i]) + b;
+      } else if (KIND == 4) {  // conditional subtract via sign mask
+        const uint32_t y = x[i] - a;
+        x[i] = y + (a & (uint32_t)((int32_t)y >> 31)) + b;
+      } else {  // plain IADD3 chain
+        x[i] = x[i] + a + b;
       }
     }
   }
@@ -444,6 +482,61 @@ __global__ void k_int_peak(uint32_t* out, uint32_t a, uint32_t b, int iters) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc ^= x[i];
   if (acc == 0x9e3779b9u) out[0] = acc;
+}
+
+// host u64 key rows -> device raw u32 copy (kept so the tiled layout can be
+// rebuilt for another NTT variant)
+void upload_raw_key(hcnn_ctx* c, const uint64_t* host, size_t rows, uint32_t** raw) {
+  const size_t count = rows * c->N;
+  uint64_t* stage = nullptr;
+  CK(cudaMallocAsync((void**)&stage, count * sizeof(uint64_t), c->stream));
+  if (!*raw) CK(cudaMalloc((void**)raw, count * sizeof(uint32_t)));
+  CK(cudaMemcpyAsync(stage, host, count * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
+  k_narrow<<<cdiv(count, 256), 256, 0, c->stream>>>(stage, *raw, count);
+  c->launched("k_narrow");
+  CK(cudaFreeAsync(stage, c->stream));
+}
+
+// raw key rows -> NTT domain, tiled layout of the current variant (Montgomery
+// form for the relinearisation key when the variant accumulates in u32)
+void layout_key(hcnn_ctx* c, const uint32_t* raw, int domain, size_t rows, uint32_t** dst, int mont) {
+  const size_t count = rows * c->N;
+  if (!*dst) CK(cudaMalloc((void**)dst, count * sizeof(uint32_t)));
+  if (domain == HCNN_DOMAIN_REF_NTT) {
+    NttLaunch a{};
+    a.grid = dim3((unsigned)rows);
+    a.a = raw;
+    a.out = *dst;
+    a.limbs = (int)c->K;
+    a.rlk_mont = mont;
+    ntt_dispatch(c, 4, a, "k_ref_to_tiled");
+  } else if (domain == HCNN_DOMAIN_COEFF) {
+    CK(cudaMemcpyAsync(*dst, raw, count * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->stream));
+    NttLaunch a{};
+    a.grid = dim3((unsigned)rows);
+    a.rows = *dst;
+    a.limbs = (int)c->K;
+    a.prime_off = 0;
+    a.inverse = 2;
+    ntt_dispatch(c, 0, a, "k_ntt_rows");
+    if (mont) {
+      NttLaunch m{};
+      m.grid = dim3((unsigned)rows);
+      m.rows = *dst;
+      m.limbs = (int)c->K;
+      ntt_dispatch(c, 5, m, "k_to_mont");
+    }
+  } else {
+    fail(HCNN_ERR_DOMAIN, "unknown key domain");
+  }
+}
+
+void prepare_keys(hcnn_ctx* c) {
+  if (c->keys_variant == c->variant) return;
+  if (c->d_rlk_raw)
+    layout_key(c, c->d_rlk_raw, c->rlk_domain, (size_t)c->D * 2 * c->K, &c->d_rlk, variant_mont(c, c->variant));
+  if (c->d_pk_raw) layout_key(c, c->d_pk_raw, c->pk_domain, 2 * (size_t)c->K, &c->d_pk, 0);
+  c->keys_variant = c->variant;
 }
 
 }  // namespace
@@ -467,7 +560,10 @@ int hcnn_int_peak(int device, int kind, double* ops_per_s) {
       switch (kind) {
         case 0: k_int_peak<0><<<blocks, tpb>>>(out, 0x9e3779b1u, 12345u, iters); break;
         case 1: k_int_peak<1><<<blocks, tpb>>>(out, 0x9e3779b1u, 12345u, iters); break;
-        default: k_int_peak<2><<<blocks, tpb>>>(out, 0x9e3779b1u, 12345u, iters); break;
+        case 2: k_int_peak<2><<<blocks, tpb>>>(out, 0x9e3779b1u, 12345u, iters); break;
+        case 3: k_int_peak<3><<<blocks, tpb>>>(out, 0x3e3779b1u, 12345u, iters); break;
+        case 4: k_int_peak<4><<<blocks, tpb>>>(out, 0x3e3779b1u, 12345u, iters); break;
+        default: k_int_peak<5><<<blocks, tpb>>>(out, 0x3e3779b1u, 12345u, iters); break;
       }
     };
     run();
@@ -536,6 +632,9 @@ int hcnn_ctx_destroy(hcnn_ctx* c) {
     cudaFree(c->d_itw);
     cudaFree(c->d_ninv);
     if (c->d_rlk) cudaFree(c->d_rlk);
+    if (c->d_rlk_raw) cudaFree(c->d_rlk_raw);
+    if (c->d_pk_raw) cudaFree(c->d_pk_raw);
+    cudaFree(c->d_pinv);
     if (c->d_pk) cudaFree(c->d_pk);
     if (c->d_delta) cudaFree(c->d_delta);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -587,6 +686,20 @@ int hcnn_ctx_set_stream(hcnn_ctx* c, void* stream) {
   return guarded([&] { c->stream = (cudaStream_t)stream; });
 }
 
+int hcnn_ctx_set_option(hcnn_ctx* c, int key, int64_t value) {
+  return guarded([&] {
+    if (key == HCNN_OPT_NTT_VARIANT) {
+      if (value != 0 && value != 3 && value != 4 && value != 5) fail(HCNN_ERR_PARAM, "NTT variant must be 0, 3, 4 or 5");
+      if (value && c->logN < 10) fail(HCNN_ERR_UNSUPPORTED, "NTT variants need N >= 1024");
+      if (value == 3 && c->logN > 13) fail(HCNN_ERR_UNSUPPORTED, "NTT variant 3 needs N <= 8192");
+      if (value && c->logN > (uint32_t)value + 10) fail(HCNN_ERR_UNSUPPORTED, "NTT variant needs more than 1024 threads");
+      c->variant = (int)value;
+    } else {
+      fail(HCNN_ERR_PARAM, "unknown option");
+    }
+  });
+}
+
 int hcnn_ctx_set_workspace_limit(hcnn_ctx* c, size_t bytes) {
   return guarded([&] { c->ws_limit = bytes; });
 }
@@ -600,6 +713,7 @@ int64_t hcnn_ctx_query(hcnn_ctx* c, int what) {
     case HCNN_Q_LOG2W: return c->log2w;
     case HCNN_Q_WS_BYTES: return (int64_t)c->ws_bytes;
     case HCNN_Q_KERNELS: return c->launches;
+    case HCNN_Q_NTT_VARIANT: return c->variant;
     default: return -1;
   }
 }
@@ -613,28 +727,12 @@ uint64_t hcnn_ctx_prime(hcnn_ctx* c, int i, uint64_t* psi) {
 int hcnn_set_relin_key(hcnn_ctx* c, const uint64_t* rlk, int domain) {
   return guarded([&] {
     if (!rlk) fail(HCNN_ERR_MISSING_KEY, "relinearization key required");
+    if (domain != HCNN_DOMAIN_REF_NTT && domain != HCNN_DOMAIN_COEFF) fail(HCNN_ERR_DOMAIN, "unknown key domain");
     CK(cudaSetDevice(c->device));
-    const size_t rows = (size_t)c->D * 2 * c->K;
-    const size_t count = rows * c->N;
-    uint64_t* stage = nullptr;
-    uint32_t* tmp = nullptr;
-    CK(cudaMallocAsync((void**)&stage, count * sizeof(uint64_t), c->stream));
-    CK(cudaMallocAsync((void**)&tmp, count * sizeof(uint32_t), c->stream));
-    if (!c->d_rlk) CK(cudaMalloc((void**)&c->d_rlk, count * sizeof(uint32_t)));
-    CK(cudaMemcpyAsync(stage, rlk, count * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
-    k_narrow<<<cdiv(count, 256), 256, 0, c->stream>>>(stage, tmp, count);
-    c->launched("k_narrow");
-    if (domain == HCNN_DOMAIN_REF_NTT) {
-      k_bitrev_rows<<<dim3(cdiv(c->N, 256), (unsigned)rows), 256, 0, c->stream>>>(tmp, c->d_rlk, (int)c->N, (int)c->logN);
-      c->launched("k_bitrev_rows");
-    } else if (domain == HCNN_DOMAIN_COEFF) {
-      CK(cudaMemcpyAsync(c->d_rlk, tmp, count * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->stream));
-      launch_ntt_rows(c, c->d_rlk, rows, (int)c->K, 0, 0);
-    } else {
-      fail(HCNN_ERR_DOMAIN, "unknown key domain");
-    }
-    CK(cudaFreeAsync(stage, c->stream));
-    CK(cudaFreeAsync(tmp, c->stream));
+    upload_raw_key(c, rlk, (size_t)c->D * 2 * c->K, &c->d_rlk_raw);
+    c->rlk_domain = domain;
+    c->keys_variant = -1;
+    prepare_keys(c);
     // digits of w = 2^32 may exceed a prime; 2^8 / 2^16 digits never do here
     c->rlk_reduce = false;
     for (uint32_t i = 0; i < c->K; ++i)
@@ -646,26 +744,12 @@ int hcnn_set_relin_key(hcnn_ctx* c, const uint64_t* rlk, int domain) {
 int hcnn_set_public_key(hcnn_ctx* c, const uint64_t* pk, int domain) {
   return guarded([&] {
     if (!pk) fail(HCNN_ERR_MISSING_KEY, "public key required");
+    if (domain != HCNN_DOMAIN_REF_NTT && domain != HCNN_DOMAIN_COEFF) fail(HCNN_ERR_DOMAIN, "unknown key domain");
     CK(cudaSetDevice(c->device));
-    const size_t rows = 2 * (size_t)c->K;
-    const size_t count = rows * c->N;
-    uint64_t* stage = nullptr;
-    uint32_t* tmp = nullptr;
-    CK(cudaMallocAsync((void**)&stage, count * sizeof(uint64_t), c->stream));
-    CK(cudaMallocAsync((void**)&tmp, count * sizeof(uint32_t), c->stream));
-    if (!c->d_pk) CK(cudaMalloc((void**)&c->d_pk, count * sizeof(uint32_t)));
-    CK(cudaMemcpyAsync(stage, pk, count * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
-    k_narrow<<<cdiv(count, 256), 256, 0, c->stream>>>(stage, tmp, count);
-    c->launched("k_narrow");
-    if (domain == HCNN_DOMAIN_REF_NTT) {
-      k_bitrev_rows<<<dim3(cdiv(c->N, 256), (unsigned)rows), 256, 0, c->stream>>>(tmp, c->d_pk, (int)c->N, (int)c->logN);
-      c->launched("k_bitrev_rows");
-    } else if (domain == HCNN_DOMAIN_COEFF) {
-      CK(cudaMemcpyAsync(c->d_pk, tmp, count * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->stream));
-      launch_ntt_rows(c, c->d_pk, rows, (int)c->K, 0, 0);
-    } else {
-      fail(HCNN_ERR_DOMAIN, "unknown key domain");
-    }
+    upload_raw_key(c, pk, 2 * (size_t)c->K, &c->d_pk_raw);
+    c->pk_domain = domain;
+    c->keys_variant = -1;
+    prepare_keys(c);
     // Delta = floor(q / t) mod q_i (bfv.py:77)
     if (!c->d_delta) {
       Big Q = product(std::vector<u64>(c->primes.begin(), c->primes.begin() + c->K));
@@ -687,8 +771,6 @@ int hcnn_set_public_key(hcnn_ctx* c, const uint64_t* pk, int domain) {
       CK(cudaMalloc((void**)&c->d_delta, c->K * sizeof(uint2)));
       CK(cudaMemcpy(c->d_delta, hd.data(), c->K * sizeof(uint2), cudaMemcpyHostToDevice));
     }
-    CK(cudaFreeAsync(stage, c->stream));
-    CK(cudaFreeAsync(tmp, c->stream));
     CK(cudaStreamSynchronize(c->stream));
   });
 }
@@ -696,9 +778,10 @@ int hcnn_set_public_key(hcnn_ctx* c, const uint64_t* pk, int domain) {
 int hcnn_encrypt(hcnn_ctx* c, const int8_t* u, const int8_t* e1, const int8_t* e2, const int64_t* msg,
                  uint32_t* out, size_t n) {
   return guarded([&] {
-    if (!c->d_pk) fail(HCNN_ERR_MISSING_KEY, "public key required");
+    if (!c->d_pk_raw) fail(HCNN_ERR_MISSING_KEY, "public key required");
     CK(cudaSetDevice(c->device));
     if (n == 0) return;
+    prepare_keys(c);
     c->mark();
     const size_t N = c->N;
     const size_t ch = n < 4096 ? n : 4096;
@@ -905,8 +988,12 @@ int hcnn_relinearize(hcnn_ctx* c, const uint32_t* in3, uint32_t* out, size_t n) 
     const size_t K = c->K, N = c->N;
     for (size_t s = 0; s < n; s += ch) {
       const size_t m = (n - s < ch) ? n - s : ch;
-      k_digits<<<dim3(cdiv(N, 128), (unsigned)m), 128, 0, c->stream>>>(in3 + s * 3 * K * N, dig, (int)N, c->tabs);
-      c->launched("k_digits");
+      ConvLaunch ca{};
+      ca.block = dim3(128);
+      ca.grid = dim3(cdiv(N, 128), (unsigned)m);
+      ca.in = in3 + s * 3 * K * N;
+      ca.dig = dig;
+      conv_dispatch(c, 2, ca, "k_digits");
       launch_relin(c, dig, in3 + s * 3 * K * N, out + s * 2 * K * N, m);
     }
   });

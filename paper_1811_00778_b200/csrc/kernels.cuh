@@ -4,116 +4,6 @@
 
 namespace hcnn {
 
-// --------------------------------------------------------- Q -> P extension
-// in: [B][2][K][N] canonical residues; ext: [B][2][KP][N]
-__global__ void k_extend(const uint32_t* __restrict__ in, uint32_t* __restrict__ ext, int N,
-                         const __grid_constant__ ConvTabs tb) {
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= N) return;
-  const size_t poly = blockIdx.y;  // ct * 2 + part
-  const uint32_t* src = in + poly * tb.K * N + n;
-  uint32_t xt[KMAX];
-#pragma unroll
-  for (int i = 0; i < KMAX; ++i)
-    if (i < tb.K) xt[i] = mul_shoup(src[(size_t)i * N], tb.qhi[i], tb.qhis[i], tb.q[i]);
-  const uint32_t v = exact_v(xt, tb);
-  uint32_t* dst = ext + poly * tb.KP * N + n;
-#pragma unroll
-  for (int j = 0; j < KPMAX; ++j)
-    if (j < tb.KP) dst[(size_t)j * N] = q_to_p(xt, v, j, tb);
-}
-
-// ------------------------------------------------------- scale and round
-// d: [B][3][K+KP][N] exact tensor residues (coefficient domain).
-// y3: [B][3][K][N] = round(t d / q) mod q for each part (bfv.py:325-328);
-// dig (if not null): [B][D][N] base-w digits of canonical y_2 (bfv.py:350-365).
-__global__ void k_scale(const uint32_t* __restrict__ d, uint32_t* __restrict__ y3,
-                        uint32_t* __restrict__ dig, int N, const __grid_constant__ ConvTabs tb) {
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= N) return;
-  const int part = blockIdx.y % 3;
-  const size_t ct = blockIdx.y / 3;
-  const int K = tb.K, KP = tb.KP;
-  const uint32_t* src = d + (size_t)blockIdx.y * (K + KP) * N + n;
-
-  // r = (t d + h) mod q, h = (q-1)/2, as r~_i = r_i (q/q_i)^-1 mod q_i
-  uint32_t rt[KMAX];
-#pragma unroll
-  for (int i = 0; i < KMAX; ++i)
-    if (i < K) rt[i] = add_mod(mul_shoup(src[(size_t)i * N], tb.A[i], tb.As[i], tb.q[i]), tb.B[i], tb.q[i]);
-  const uint32_t v = exact_v(rt, tb);
-
-  // y = (t d + h - r) / q exactly, in P (centred, |y| < P/4): y~_j = y_j (P/p_j)^-1
-  uint32_t yt[KPMAX];
-  uint64_t F = 0;
-#pragma unroll
-  for (int j = 0; j < KPMAX; ++j) {
-    if (j < KP) {
-      const uint32_t pj = tb.p[j];
-      const uint32_t rj = q_to_p(rt, v, j, tb);
-      const uint32_t dj = src[(size_t)(K + j) * N];
-      uint32_t acc = add_mod(mul_shoup(dj, tb.C[j], tb.Cs[j], pj), mul_shoup(pj - rj, tb.Ej[j], tb.Ejs[j], pj), pj);
-      acc = add_mod(acc, tb.F[j], pj);
-      yt[j] = acc;
-      F += frac60(acc, tb.pG[j], tb.pb[j]);
-    }
-  }
-  const uint32_t vp = (uint32_t)((F + (FRAC_ONE >> 1)) >> 60);
-
-  // back to Q: y_i = (sum_j y~_j (P/p_j) - vp P) mod q_i
-  uint32_t yq[KMAX];
-#pragma unroll
-  for (int i = 0; i < KMAX; ++i) {
-    if (i < K) {
-      uint64_t acc = (uint64_t)vp * tb.negp_q[i];
-#pragma unroll
-      for (int j = 0; j < KPMAX; ++j)
-        if (j < KP) acc += (uint64_t)yt[j] * tb.phat_q[j][i];
-      yq[i] = reduce64(acc, tb.q[i], tb.qmu[i]);
-    }
-  }
-  uint32_t* dst = y3 + (size_t)blockIdx.y * K * N + n;
-#pragma unroll
-  for (int i = 0; i < KMAX; ++i)
-    if (i < K) dst[(size_t)i * N] = yq[i];
-
-  if (part != 2 || dig == nullptr) return;
-  // canonical binary of y_2 mod q, then base-w digits
-  uint32_t xt[KMAX];
-#pragma unroll
-  for (int i = 0; i < KMAX; ++i)
-    if (i < K) xt[i] = mul_shoup(yq[i], tb.qhi[i], tb.qhis[i], tb.q[i]);
-  uint64_t Fq = 0;
-#pragma unroll
-  for (int i = 0; i < KMAX; ++i)
-    if (i < K) Fq += frac60(xt[i], tb.qG[i], tb.qb[i]);
-  uint32_t S[WMAX];
-  mw_lift(xt, tb, S);
-  mw_sub_mq(S, (uint32_t)(Fq >> 60), tb);  // S - V q >= 0, V <= v
-  {
-    // if S >= q subtract q once more
-    uint32_t T[WMAX];
-#pragma unroll
-    for (int w = 0; w < WMAX; ++w) T[w] = S[w];
-    if (!mw_sub_mq(T, 1, tb)) {
-#pragma unroll
-      for (int w = 0; w < WMAX; ++w) S[w] = T[w];
-    }
-  }
-  uint32_t* dd = dig + ct * tb.D * N + n;
-  const int db = tb.digit_bits;
-  const uint32_t mask = db == 32 ? 0xffffffffu : ((1u << db) - 1);
-  for (int k = 0; k < tb.D; ++k) {
-    const int bit = k * db;
-    const int wi = bit >> 5, sh = bit & 31;
-    uint32_t word = 0;
-#pragma unroll
-    for (int w = 0; w < WMAX; ++w)
-      if (w == wi) word = S[w];
-    dd[(size_t)k * N] = (word >> sh) & mask;
-  }
-}
-
 // ------------------------------------------------ plaintext-weight MAC
 // Residues < 2^30 and weights reduced mod p_i < 2^30: 15 lazy 64-bit products
 // fit before a reduction (15 * (2^30-1)^2 + 2^30 < 2^64).

@@ -13,10 +13,15 @@
 // NTT-domain keys are permuted once at upload.
 //
 // How.  One CTA owns one row of N residues: T = N/E threads each keep E = 2^LOGE
-// residues in registers, run LOGE butterfly stages locally, and exchange
-// through padded shared memory between passes.  Butterflies are Harvey's lazy
-// ones: forward values live in [0, 4p), inverse values in [0, 2p), Shoup
-// twiddles (w, floor(w 2^32 / p)) are read through the read-only path.
+// residues in registers.  The top LOGN - REM butterfly bits are done in
+// radix-E passes (LOGE stages in registers, then an exchange through padded
+// shared memory); the REM = LOGN mod LOGE lowest bits are done with warp
+// shuffles (the partner element lives in lane ^ 2^b), so there is no radix-2
+// shared-memory tail.  Butterflies are Harvey's lazy ones: forward values in
+// [0, 4p), inverse values in [0, 2p).  Twiddles are Shoup pairs
+// (w, floor(w 2^32/p)) indexed like SEAL's psi^brv table; each thread loads
+// the 2^ss twiddles of stage ss as one contiguous vector (15 per radix-16 pass
+// in 8 loads instead of 32).
 #pragma once
 #include "modarith.cuh"
 
@@ -26,162 +31,400 @@ __host__ __device__ constexpr int pick_loge(int logn) {
   return logn >= 15 ? 5 : logn >= 9 ? 4 : logn >= 6 ? logn - 5 : 1;
 }
 
-template <int LOGN>
+// SHFL_TAIL: the REM = LOGN mod LOGE lowest butterfly bits are done with warp
+// shuffles (radix-16 geometry) or in registers after one more exchange
+// (E/2^REM independent groups per thread; radix-32 geometry).
+template <int LOGN_, int LOGE_ = pick_loge(LOGN_), bool SHFL_TAIL_ = (LOGE_ <= 4)>
 struct NttGeom {
+  static constexpr int LOGN = LOGN_;
   static constexpr int N = 1 << LOGN;
-  static constexpr int LOGE = pick_loge(LOGN);
+  static constexpr int LOGE = LOGE_;
   static constexpr int E = 1 << LOGE;
   static constexpr int LOGT = LOGN - LOGE;
   static constexpr int T = 1 << LOGT;
-  static constexpr int NFULL = LOGN / LOGE;
-  static constexpr int REM = LOGN % LOGE;
-  static constexpr int NPASS = NFULL + (REM ? 1 : 0);
+  static constexpr int NFULL = LOGN / LOGE;  // radix-E passes
+  static constexpr int REM = LOGN % LOGE;    // low bits of the tail
+  static constexpr bool SHFL_TAIL = SHFL_TAIL_ && REM > 0;
+  static constexpr bool REG_TAIL = !SHFL_TAIL_ && REM > 0;
+  static_assert(!SHFL_TAIL || T >= 32, "shuffle stages need full warps");
   // shared-memory words for one padded row
   static constexpr int SMEM_WORDS = N + 2 * (N >> 5) + 2;
-  // forward pass P covers butterfly bits [lo(P), lo(P) + kb(P))
-  __host__ __device__ static constexpr int lo(int P) { return P < NFULL ? LOGN - (P + 1) * LOGE : 0; }
-  __host__ __device__ static constexpr int kb(int P) { return P < NFULL ? LOGE : REM; }
+  // pass P covers butterfly bits [lo(P), lo(P) + LOGE), from the top
+  __host__ __device__ static constexpr int lo(int P) { return LOGN - (P + 1) * LOGE; }
 };
 
-// padded shared-memory slot of element idx (2 words every 32: no bank conflicts
-// for the pass layouts used here except a 2-way one in the radix-2 tail pass)
+// padded shared-memory slot of element idx (2 words every 32)
 DI int sidx(int idx) { return idx + ((idx >> 5) << 1); }
 
 // Element index held in register e of thread tid during a pass covering
-// butterfly bits [LO, LO+KB).  The low KB bits of e select the butterfly
-// position, the rest of e and tid fill the other bits, tid lowest.
-template <int LOGN, int LO, int KB>
+// butterfly bits [LO, LO+KB): e supplies those bits, tid the others.
+template <int LO, int KB>
 DI int pass_index(int tid, int e) {
-  constexpr int T = NttGeom<LOGN>::T;
-  const int elo = e & ((1 << KB) - 1);
-  const int o = (e >> KB) * T + tid;
-  return ((o >> LO) << (LO + KB)) | (elo << LO) | (o & ((1 << LO) - 1));
+  return ((tid >> LO) << (LO + KB)) | (e << LO) | (tid & ((1 << LO) - 1));
 }
 
-// forward (CT) butterfly stages of one pass; values in [0, 4p)
-template <int LOGN, int LO, int KB>
-DI void fwd_pass(uint32_t* x, const uint2* __restrict__ tw, uint32_t p, int tid) {
-  constexpr int E = NttGeom<LOGN>::E;
-  const uint32_t p2 = 2 * p;
+DI uint32_t umin32(uint32_t a, uint32_t b) { return a < b ? a : b; }
+
+// register-tail mapping: bits [0, REM) from e's low bits, group e >> REM and
+// tid fill the rest
+template <class G>
+DI int tail_index(int tid, int e) {
+  return ((((e >> G::REM) * G::T) + tid) << G::REM) | (e & ((1 << G::REM) - 1));
+}
+
+// COUNT consecutive twiddles starting at an index aligned to COUNT
+template <int COUNT>
+DI void load_tw(uint2* w, const uint2* __restrict__ tw, int base) {
+  if constexpr (COUNT == 1) {
+    w[0] = __ldg(&tw[base]);
+  } else {
+    const uint4* v = reinterpret_cast<const uint4*>(tw + base);
 #pragma unroll
-  for (int ss = 0; ss < KB; ++ss) {
-    const int bpos = LO + KB - 1 - ss;
-    const int s = LOGN - 1 - bpos;
-    const int half = 1 << (KB - 1 - ss);
+    for (int k = 0; k < COUNT / 2; ++k) {
+      const uint4 q = __ldg(&v[k]);
+      w[2 * k] = make_uint2(q.x, q.y);
+      w[2 * k + 1] = make_uint2(q.z, q.w);
+    }
+  }
+}
+
+// forward (CT) stage SS of a radix-E pass at bits [LO, LO+LOGE); values in [0, 4p)
+template <class G, int LO, int SS>
+DI void fwd_stage(uint32_t* x, const uint2* __restrict__ tw, uint32_t p, int tid) {
+  constexpr int KB = G::LOGE;
+  if constexpr (SS < KB) {
+    constexpr int E = G::E;
+    constexpr int bpos = LO + KB - 1 - SS;
+    constexpr int s = G::LOGN - 1 - bpos;
+    constexpr int half = 1 << (KB - 1 - SS);
+    const uint32_t p2 = 2 * p;
+    uint2 w[1 << SS];
+    load_tw<(1 << SS)>(w, tw, (1 << s) + ((tid >> LO) << SS));
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       if (e & half) continue;
-      const int j = pass_index<LOGN, LO, KB>(tid, e);
-      const uint2 w = __ldg(&tw[(1 << s) + (j >> (bpos + 1))]);
+      const uint2 ww = w[e >> (KB - SS)];
       uint32_t X = x[e];
-      X = X >= p2 ? X - p2 : X;
-      const uint32_t Tt = mul_shoup_lazy(x[e | half], w.x, w.y, p);
+      X = umin32(X, X - p2);
+      const uint32_t Tt = mul_shoup_lazy(x[e | half], ww.x, ww.y, p);
       x[e] = X + Tt;
       x[e | half] = X - Tt + p2;
     }
+    fwd_stage<G, LO, SS + 1>(x, tw, p, tid);
   }
 }
 
-// inverse (GS) butterfly stages of one pass, bits ascending; values in [0, 2p)
-template <int LOGN, int LO, int KB>
-DI void inv_pass(uint32_t* x, const uint2* __restrict__ itw, uint32_t p, int tid) {
-  constexpr int E = NttGeom<LOGN>::E;
-  const uint32_t p2 = 2 * p;
-#pragma unroll
-  for (int ss = 0; ss < KB; ++ss) {
-    const int bpos = LO + ss;
-    const int s = LOGN - 1 - bpos;
-    const int half = 1 << ss;
+template <class G, int LO>
+DI void fwd_pass(uint32_t* x, const uint2* __restrict__ tw, uint32_t p, int tid) {
+  fwd_stage<G, LO, 0>(x, tw, p, tid);
+}
+
+// inverse (GS) stage SS of a radix-E pass (SS descending = bits ascending);
+// values in [0, 2p)
+template <class G, int LO, int SS>
+DI void inv_stage(uint32_t* x, const uint2* __restrict__ itw, uint32_t p, int tid) {
+  constexpr int KB = G::LOGE;
+  if constexpr (SS >= 0) {
+    constexpr int E = G::E;
+    constexpr int bpos = LO + KB - 1 - SS;
+    constexpr int s = G::LOGN - 1 - bpos;
+    constexpr int half = 1 << (KB - 1 - SS);
+    const uint32_t p2 = 2 * p;
+    uint2 w[1 << SS];
+    load_tw<(1 << SS)>(w, itw, (1 << s) + ((tid >> LO) << SS));
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       if (e & half) continue;
-      const int j = pass_index<LOGN, LO, KB>(tid, e);
-      const uint2 w = __ldg(&itw[(1 << s) + (j >> (bpos + 1))]);
+      const uint2 ww = w[e >> (KB - SS)];
       const uint32_t X = x[e], Y = x[e | half];
-      uint32_t U = X + Y;
-      U = U >= p2 ? U - p2 : U;
-      x[e] = U;
-      x[e | half] = mul_shoup_lazy(X - Y + p2, w.x, w.y, p);
+      const uint32_t U = X + Y;
+      x[e] = umin32(U, U - p2);
+      x[e | half] = mul_shoup_lazy(X - Y + p2, ww.x, ww.y, p);
     }
+    inv_stage<G, LO, SS - 1>(x, itw, p, tid);
   }
 }
 
-template <int LOGN, int LO, int KB>
+template <class G, int LO>
+DI void inv_pass(uint32_t* x, const uint2* __restrict__ itw, uint32_t p, int tid) {
+  inv_stage<G, LO, G::LOGE - 1>(x, itw, p, tid);
+}
+
+// register tail, forward stage SS (bits REM-1-SS), all E/2^REM groups
+template <class G, int SS>
+DI void fwd_tail(uint32_t* x, const uint2* __restrict__ tw, uint32_t p, int tid) {
+  if constexpr (SS < G::REM) {
+    constexpr int R = G::REM;
+    constexpr int bpos = R - 1 - SS;
+    constexpr int s = G::LOGN - 1 - bpos;
+    constexpr int half = 1 << (R - 1 - SS);
+    const uint32_t p2 = 2 * p;
+#pragma unroll
+    for (int grp = 0; grp < (G::E >> R); ++grp) {
+      uint2 w[1 << SS];
+      load_tw<(1 << SS)>(w, tw, (1 << s) + ((grp * G::T + tid) << SS));
+#pragma unroll
+      for (int el = 0; el < (1 << R); ++el) {
+        if (el & half) continue;
+        const int e = (grp << R) | el;
+        const uint2 ww = w[el >> (R - SS)];
+        uint32_t X = x[e];
+        X = umin32(X, X - p2);
+        const uint32_t Tt = mul_shoup_lazy(x[e | half], ww.x, ww.y, p);
+        x[e] = X + Tt;
+        x[e | half] = X - Tt + p2;
+      }
+    }
+    fwd_tail<G, SS + 1>(x, tw, p, tid);
+  }
+}
+
+template <class G, int SS>
+DI void inv_tail(uint32_t* x, const uint2* __restrict__ itw, uint32_t p, int tid) {
+  if constexpr (SS >= 0) {
+    constexpr int R = G::REM;
+    constexpr int bpos = R - 1 - SS;
+    constexpr int s = G::LOGN - 1 - bpos;
+    constexpr int half = 1 << (R - 1 - SS);
+    const uint32_t p2 = 2 * p;
+#pragma unroll
+    for (int grp = 0; grp < (G::E >> R); ++grp) {
+      uint2 w[1 << SS];
+      load_tw<(1 << SS)>(w, itw, (1 << s) + ((grp * G::T + tid) << SS));
+#pragma unroll
+      for (int el = 0; el < (1 << R); ++el) {
+        if (el & half) continue;
+        const int e = (grp << R) | el;
+        const uint2 ww = w[el >> (R - SS)];
+        const uint32_t X = x[e], Y = x[e | half];
+        const uint32_t U = X + Y;
+        x[e] = umin32(U, U - p2);
+        x[e | half] = mul_shoup_lazy(X - Y + p2, ww.x, ww.y, p);
+      }
+    }
+    inv_tail<G, SS - 1>(x, itw, p, tid);
+  }
+}
+
+// twiddle index of the shuffle stage at butterfly bit b < REM for register e,
+// in the spectral layout (last pass LO = REM): (1 << s) + (j >> (b + 1))
+template <class G>
+DI int shfl_tw_index(int tid, int e, int b) {
+  const int j = pass_index<G::REM, G::LOGE>(tid, e);
+  return (1 << (G::LOGN - 1 - b)) + (j >> (b + 1));
+}
+
+template <class G, int B>
+DI void load_shfl_tw(uint2* w, const uint2* __restrict__ tw, int tid) {
+  if constexpr (B == G::REM - 1) {
+    // consecutive in e: one aligned vector of E pairs
+    load_tw<G::E>(w, tw, shfl_tw_index<G>(tid, 0, B));
+  } else {
+#pragma unroll
+    for (int e = 0; e < G::E; ++e) w[e] = __ldg(&tw[shfl_tw_index<G>(tid, e, B)]);
+  }
+}
+
+// forward butterflies on the REM lowest bits through warp shuffles
+template <class G, int B>
+DI void fwd_shfl(uint32_t* x, const uint2* __restrict__ tw, uint32_t p, int tid) {
+  if constexpr (B >= 0) {
+    const uint32_t p2 = 2 * p;
+    const bool upper = (tid >> B) & 1;
+    uint2 w[G::E];
+    load_shfl_tw<G, B>(w, tw, tid);
+#pragma unroll
+    for (int e = 0; e < G::E; ++e) {
+      const uint32_t v = x[e];
+      const uint32_t u = __shfl_xor_sync(0xffffffffu, v, 1 << B);
+      uint32_t X = upper ? u : v;
+      const uint32_t Y = upper ? v : u;
+      X = umin32(X, X - p2);
+      const uint32_t Tt = mul_shoup_lazy(Y, w[e].x, w[e].y, p);
+      x[e] = upper ? X - Tt + p2 : X + Tt;
+    }
+    fwd_shfl<G, B - 1>(x, tw, p, tid);
+  }
+}
+
+template <class G, int B>
+DI void inv_shfl(uint32_t* x, const uint2* __restrict__ itw, uint32_t p, int tid) {
+  if constexpr (B < G::REM) {
+    const uint32_t p2 = 2 * p;
+    const bool upper = (tid >> B) & 1;
+    uint2 w[G::E];
+    load_shfl_tw<G, B>(w, itw, tid);
+#pragma unroll
+    for (int e = 0; e < G::E; ++e) {
+      const uint32_t v = x[e];
+      const uint32_t u = __shfl_xor_sync(0xffffffffu, v, 1 << B);
+      const uint32_t X = upper ? u : v;
+      const uint32_t Y = upper ? v : u;
+      const uint32_t U = X + Y;
+      x[e] = upper ? mul_shoup_lazy(X - Y + p2, w[e].x, w[e].y, p) : umin32(U, U - p2);
+    }
+    inv_shfl<G, B + 1>(x, itw, p, tid);
+  }
+}
+
+template <class G, int LO>
 DI void regs_to_smem(const uint32_t* x, uint32_t* s, int tid) {
 #pragma unroll
-  for (int e = 0; e < NttGeom<LOGN>::E; ++e) s[sidx(pass_index<LOGN, LO, KB>(tid, e))] = x[e];
+  for (int e = 0; e < G::E; ++e)
+    s[sidx(pass_index<LO, G::LOGE>(tid, e))] = x[e];
 }
 
-template <int LOGN, int LO, int KB>
+template <class G, int LO>
 DI void smem_to_regs(uint32_t* x, const uint32_t* s, int tid) {
 #pragma unroll
-  for (int e = 0; e < NttGeom<LOGN>::E; ++e) x[e] = s[sidx(pass_index<LOGN, LO, KB>(tid, e))];
+  for (int e = 0; e < G::E; ++e)
+    x[e] = s[sidx(pass_index<LO, G::LOGE>(tid, e))];
 }
 
-template <int LOGN, int P>
+template <class G, int P>
 DI void fwd_from(uint32_t* x, uint32_t* s, const uint2* __restrict__ tw, uint32_t p, int tid) {
-  using G = NttGeom<LOGN>;
-  if constexpr (P < G::NPASS) {
+  if constexpr (P < G::NFULL) {
     if constexpr (P > 0) {
-      regs_to_smem<LOGN, G::lo(P - 1), G::kb(P - 1)>(x, s, tid);
+      regs_to_smem<G, G::lo(P - 1)>(x, s, tid);
       __syncthreads();
-      smem_to_regs<LOGN, G::lo(P), G::kb(P)>(x, s, tid);
+      smem_to_regs<G, G::lo(P)>(x, s, tid);
       __syncthreads();
     }
-    fwd_pass<LOGN, G::lo(P), G::kb(P)>(x, tw, p, tid);
-    fwd_from<LOGN, P + 1>(x, s, tw, p, tid);
+    fwd_pass<G, G::lo(P)>(x, tw, p, tid);
+    fwd_from<G, P + 1>(x, s, tw, p, tid);
   }
 }
 
-template <int LOGN, int P>
+template <class G, int P>
 DI void inv_from(uint32_t* x, uint32_t* s, const uint2* __restrict__ itw, uint32_t p, int tid) {
-  using G = NttGeom<LOGN>;
   if constexpr (P >= 0) {
-    if constexpr (P < G::NPASS - 1) {
-      regs_to_smem<LOGN, G::lo(P + 1), G::kb(P + 1)>(x, s, tid);
+    if constexpr (P < G::NFULL - 1) {
+      regs_to_smem<G, G::lo(P + 1)>(x, s, tid);
       __syncthreads();
-      smem_to_regs<LOGN, G::lo(P), G::kb(P)>(x, s, tid);
+      smem_to_regs<G, G::lo(P)>(x, s, tid);
       __syncthreads();
     }
-    inv_pass<LOGN, G::lo(P), G::kb(P)>(x, itw, p, tid);
-    inv_from<LOGN, P - 1>(x, s, itw, p, tid);
+    inv_pass<G, G::lo(P)>(x, itw, p, tid);
+    inv_from<G, P - 1>(x, s, itw, p, tid);
   }
 }
 
 // Register layouts at the boundaries:
-//   natural layout  : x[e] = a[e * T + tid]            (coalesced global access)
-//   spectral layout : x[e] = A[pass_index<last pass>]  (what the forward leaves)
-template <int LOGN>
-DI int natural_index(int tid, int e) { return e * NttGeom<LOGN>::T + tid; }
+//   natural  : x[e] = a[e * T + tid]                     (coalesced global access)
+//   spectral : x[e] = A[pass_index<REM, LOGE>(tid, e)]   (what the forward leaves)
+//   tiled    : spectral values in 16-byte groups (device key layout, below)
+template <class G>
+DI int natural_index(int tid, int e) { return e * G::T + tid; }
 
-template <int LOGN>
+template <class G>
 DI int spectral_index(int tid, int e) {
-  using G = NttGeom<LOGN>;
-  return pass_index<LOGN, G::lo(G::NPASS - 1), G::kb(G::NPASS - 1)>(tid, e);
+  if constexpr (G::REG_TAIL) return tail_index<G>(tid, e);
+  else return pass_index<G::REM, G::LOGE>(tid, e);
+}
+
+// tiled: groups of 4 spectral values, group-major then thread:
+//   element e of thread tid at ((e/4) * T + tid) * 4 + e%4
+// so each thread moves 16-byte vectors and a warp's vectors are contiguous
+// (coalesced in global memory, conflict-free in shared memory).
+template <class G>
+DI int tiled_index(int tid, int e) {
+  if constexpr (G::E >= 4) return (((e >> 2) * G::T + tid) << 2) | (e & 3);
+  else return e * G::T + tid;
+}
+
+template <class G>
+DI void load_tiled(uint32_t* x, const uint32_t* __restrict__ row, int tid) {
+  if constexpr (G::E >= 4) {
+    const uint4* v = reinterpret_cast<const uint4*>(row) + tid;
+#pragma unroll
+    for (int k = 0; k < G::E / 4; ++k) {
+      const uint4 q = __ldg(&v[k * G::T]);
+      x[4 * k] = q.x;
+      x[4 * k + 1] = q.y;
+      x[4 * k + 2] = q.z;
+      x[4 * k + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < G::E; ++e) x[e] = __ldg(&row[tiled_index<G>(tid, e)]);
+  }
+}
+
+// same, from shared memory
+template <class G>
+DI void load_tiled_smem(uint32_t* x, const uint32_t* row, int tid) {
+  if constexpr (G::E >= 4) {
+    const uint4* v = reinterpret_cast<const uint4*>(row) + tid;
+#pragma unroll
+    for (int k = 0; k < G::E / 4; ++k) {
+      const uint4 q = v[k * G::T];
+      x[4 * k] = q.x;
+      x[4 * k + 1] = q.y;
+      x[4 * k + 2] = q.z;
+      x[4 * k + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < G::E; ++e) x[e] = row[tiled_index<G>(tid, e)];
+  }
+}
+
+template <class G>
+DI void store_tiled(const uint32_t* x, uint32_t* __restrict__ row, int tid) {
+  if constexpr (G::E >= 4) {
+    uint4* v = reinterpret_cast<uint4*>(row) + tid;
+#pragma unroll
+    for (int k = 0; k < G::E / 4; ++k)
+      v[k * G::T] = make_uint4(x[4 * k], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < G::E; ++e) row[tiled_index<G>(tid, e)] = x[e];
+  }
 }
 
 // Forward negacyclic NTT: natural layout in (any values < 4p), spectral layout
 // out, fully reduced to [0, p).
-template <int LOGN>
+template <class G>
 DI void ntt_fwd(uint32_t* x, uint32_t* s, const uint2* __restrict__ tw, uint32_t p, int tid) {
-  fwd_from<LOGN, 0>(x, s, tw, p, tid);
+  fwd_from<G, 0>(x, s, tw, p, tid);
+  if constexpr (G::SHFL_TAIL) {
+    fwd_shfl<G, G::REM - 1>(x, tw, p, tid);
+  } else if constexpr (G::REG_TAIL) {
+#pragma unroll
+    for (int e = 0; e < G::E; ++e) s[sidx(pass_index<G::REM, G::LOGE>(tid, e))] = x[e];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < G::E; ++e) x[e] = s[sidx(tail_index<G>(tid, e))];
+    __syncthreads();
+    fwd_tail<G, 0>(x, tw, p, tid);
+  }
   const uint32_t p2 = 2 * p;
 #pragma unroll
-  for (int e = 0; e < NttGeom<LOGN>::E; ++e) {
-    uint32_t v = x[e];
-    v = v >= p2 ? v - p2 : v;
-    x[e] = v >= p ? v - p : v;
+  for (int e = 0; e < G::E; ++e) {
+    const uint32_t v = umin32(x[e], x[e] - p2);
+    x[e] = umin32(v, v - p);
   }
 }
 
 // Inverse negacyclic NTT: spectral layout in (values < 2p), natural layout out,
 // times N^-1, reduced to [0, p).
-template <int LOGN>
+template <class G>
 DI void ntt_inv(uint32_t* x, uint32_t* s, const uint2* __restrict__ itw, uint32_t p, uint2 ninv,
                 int tid) {
-  inv_from<LOGN, NttGeom<LOGN>::NPASS - 1>(x, s, itw, p, tid);
+  if constexpr (G::SHFL_TAIL) {
+    inv_shfl<G, 0>(x, itw, p, tid);
+  } else if constexpr (G::REG_TAIL) {
+    inv_tail<G, G::REM - 1>(x, itw, p, tid);
 #pragma unroll
-  for (int e = 0; e < NttGeom<LOGN>::E; ++e) x[e] = mul_shoup(x[e], ninv.x, ninv.y, p);
+    for (int e = 0; e < G::E; ++e) s[sidx(tail_index<G>(tid, e))] = x[e];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < G::E; ++e) x[e] = s[sidx(pass_index<G::REM, G::LOGE>(tid, e))];
+    __syncthreads();
+  }
+  inv_from<G, G::NFULL - 1>(x, s, itw, p, tid);
+#pragma unroll
+  for (int e = 0; e < G::E; ++e) x[e] = mul_shoup(x[e], ninv.x, ninv.y, p);
 }
 
 }  // namespace hcnn

@@ -11,3 +11,5 @@
 cudaError_t HCNN_CAT(hcnn_ntt_launch_, HCNN_LOGN)(int op, const hcnn::NttLaunch& a) {
   return hcnn::ntt_launch<HCNN_LOGN>(op, a);
 }
+
+int HCNN_CAT(hcnn_ntt_mont_, HCNN_LOGN)(int variant) { return hcnn::ntt_variant_mont<HCNN_LOGN>(variant); }

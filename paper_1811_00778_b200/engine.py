@@ -19,6 +19,7 @@ engine.py:109-112).  There is no CPU fallback.
 from __future__ import annotations
 
 import hashlib
+import os
 import threading
 import weakref
 from dataclasses import dataclass
@@ -124,6 +125,9 @@ class GpuContext:
         self.handle = h
         self.KP = int(L.hcnn_ctx_query(h, 2))
         self.D = int(L.hcnn_ctx_query(h, 3))
+        variant = int(os.environ.get("HCNN_NTT_VARIANT", "0"))
+        if variant and self.N >= 1024:
+            _lib.check(L.hcnn_ctx_set_option(h, 1, variant), "hcnn_ctx_set_option")
         self._rlk_ref = None
         self._weights = {}
         self._finalizer = weakref.finalize(self, L.hcnn_ctx_destroy, h)
@@ -138,6 +142,24 @@ class GpuContext:
 
     def empty(self, n: int, parts: int = 2) -> torch.Tensor:
         return torch.empty((n, parts, self.K, self.N), dtype=torch.int32, device=f"cuda:{self.device}")
+
+    def set_variant(self, variant: int):
+        """NTT radix variant of the fused kernels (0 default, 4 or 5)."""
+        _lib.check(_lib.lib().hcnn_ctx_set_option(self.handle, 1, int(variant)), "ntt variant")
+
+    def profile(self, enable: bool):
+        _lib.check(_lib.lib().hcnn_profile(self.handle, int(bool(enable))))
+
+    def profile_read(self) -> dict:
+        import ctypes
+
+        buf = ctypes.create_string_buffer(1 << 16)
+        _lib.lib().hcnn_profile_dump(self.handle, buf, len(buf))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, cnt, tot = line.split()
+            out[name] = (int(cnt), float(tot))
+        return out
 
     def set_workspace_limit(self, nbytes: int):
         _lib.check(_lib.lib().hcnn_ctx_set_workspace_limit(self.handle, int(nbytes)))
