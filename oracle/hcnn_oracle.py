@@ -175,6 +175,16 @@ def mul_scalar(ctx: Context, res: np.ndarray, w: int) -> np.ndarray:
     return res * ctx.scalar_col(int(w)) % ctx.mods
 
 
+def crt_combine(residues, moduli) -> int:
+    """Unique integer in [0, prod m) with the given residues (ring.py:276-283)."""
+    total = prod(int(m) for m in moduli)
+    acc = 0
+    for r, m in zip(residues, moduli):
+        big = total // int(m)
+        acc += int(r) * big * pow(big % int(m), -1, int(m))
+    return acc % total
+
+
 def crt_lift(ctx: Context, res: np.ndarray) -> list:
     """Canonical [0, q) integers from residues (ring.py:286-295)."""
     acc = [0] * ctx.n
@@ -549,6 +559,50 @@ def square(pr, x: Tensor, rlk_ntt, counter) -> Tensor:
     out = [hsquare(pr, ct, rlk_ntt) for ct in x.cts]
     counter.hsquare += len(out)
     return Tensor(x.shape, out, x.delta * x.delta)
+
+
+def plain_forward(layers, image):
+    """Plaintext integer network (nn_oracle.py:230-311): conv, square, pool, fc
+    on exact Python ints; `layers` as for `network`."""
+    x = np.asarray(image, dtype=object)
+    for L in layers:
+        k = L["kind"]
+        if k == "conv":
+            w = np.asarray(L["weights"], dtype=object)
+            f, kh, kw, cg = w.shape
+            h, wd, c = x.shape
+            sh, sw = L["stride"]
+            ph = (kh - 1) // 2 if L["padded"] else 0
+            pw = (kw - 1) // 2 if L["padded"] else 0
+            xp = np.zeros((h + 2 * ph, wd + 2 * pw, c), dtype=object)
+            xp[ph:ph + h, pw:pw + wd] = x
+            oh = (h + 2 * ph - kh) // sh + 1
+            ow = (wd + 2 * pw - kw) // sw + 1
+            per = f // L["groups"]
+            out = np.zeros((oh, ow, f), dtype=object)
+            for oy in range(oh):
+                for ox in range(ow):
+                    win = xp[oy * sh:oy * sh + kh, ox * sw:ox * sw + kw]
+                    for fi in range(f):
+                        g = fi // per
+                        out[oy, ox, fi] = int((win[:, :, g * cg:(g + 1) * cg] * w[fi]).sum())
+            x = out
+        elif k == "square":
+            x = x * x
+        elif k == "pool":
+            e = L["extent"]
+            sh, sw = L["stride"]
+            h, wd, c = x.shape
+            oh, ow = (h - e) // sh + 1, (wd - e) // sw + 1
+            out = np.zeros((oh, ow, c), dtype=object)
+            for oy in range(oh):
+                for ox in range(ow):
+                    out[oy, ox] = x[oy * sh:oy * sh + e, ox * sw:ox * sw + e].sum(axis=(0, 1))
+            x = out
+        elif k == "fc":
+            w = np.asarray(L["weights"], dtype=object)
+            x = (w @ x.reshape(-1)).reshape(1, 1, -1)
+    return x
 
 
 def network(pr, x: Tensor, layers, rlk_ntt, counter=None, hook=None) -> Tensor:

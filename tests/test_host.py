@@ -1,0 +1,166 @@
+"""Host-side logic that needs no GPU: the C-ABI library loads and binds every
+declared symbol, counters follow the reference's OpCounter semantics,
+network tables and error mapping match the reference."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+import hcnn_oracle as O
+from conftest import ROOT
+
+from paper_1811_00778_b200 import _lib, errors, nn
+from paper_1811_00778_b200 import engine as E
+
+
+def header_symbols():
+    with open(os.path.join(ROOT, "include", "hcnn_b200.h")) as fh:
+        text = fh.read()
+    return sorted(set(re.findall(r"\b(hcnn_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.lib()
+    syms = header_symbols()
+    assert len(syms) >= 25
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_lib.EXPORTED)
+    assert lib.hcnn_version().startswith(b"hcnn_b200")
+
+
+def test_library_is_sm100a_native():
+    """The shared object carries sm_100a SASS only (no PTX JIT, no other arch)."""
+    import subprocess
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    arches = set(re.findall(r"sm_(\d+a?)", out))
+    assert arches == {"100a"}, arches
+
+
+def test_status_codes_map_onto_reference_exceptions():
+    assert errors.STATUS[1] is errors.ParameterMismatchError
+    assert errors.STATUS[2] is errors.MissingKeyError
+    assert errors.STATUS[3] is errors.CapacityError
+    assert issubclass(errors.BackendError, errors.HefirError)
+
+
+def test_network_shapes():
+    assert nn.mnist_hcnn().layer_shapes() == [(12, 12, 5), (12, 12, 5), (4, 4, 50), (4, 4, 50), (1, 1, 10)]
+    assert nn.cifar10_hcnn().layer_shapes()[-1] == (1, 1, 10)
+    assert nn.cifar10_hcnn().layer_shapes()[2] == (16, 16, 32)
+
+
+def _oracle_counts(h, w, c, layer, weights):
+    """scheduled / executed / hadd by the reference's loops (engine.py:206-303)."""
+    f, kh, kw, cg = weights.shape
+    sh, sw = layer.stride
+    ph = (kh - 1) // 2 if layer.padded else 0
+    pw = (kw - 1) // 2 if layer.padded else 0
+    oh = (h + 2 * ph - kh) // sh + 1
+    ow = (w + 2 * pw - kw) // sw + 1
+    per = f // layer.groups
+    sched = ex = hadd = 0
+    for oy in range(oh):
+        for ox in range(ow):
+            for fi in range(f):
+                used = 0
+                for ky in range(kh):
+                    if not 0 <= oy * sh + ky - ph < h:
+                        continue
+                    for kx in range(kw):
+                        if not 0 <= ox * sw + kx - pw < w:
+                            continue
+                        for ci in range(cg):
+                            sched += 1
+                            if weights[fi, ky, kx, ci] != 0:
+                                used += 1
+                ex += used
+                hadd += max(used - 1, 0)
+    _ = per
+    return sched, ex, hadd
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_conv_counters_match_reference_loops(seed):
+    rng = np.random.default_rng(seed)
+    h, w = int(rng.integers(3, 9)), int(rng.integers(3, 9))
+    groups = int(rng.choice([1, 2]))
+    c = groups * int(rng.integers(1, 3))
+    f = groups * int(rng.integers(1, 3))
+    k = int(rng.choice([1, 3, 5]))
+    if k > min(h, w):
+        k = 1
+    layer = nn.conv_layer("c", f, (k, k), (int(rng.integers(1, 3)),) * 2, bool(rng.integers(0, 2)), 15,
+                          groups=groups)
+    weights = rng.integers(-2, 3, (f, k, k, c // groups))
+    assert E._conv_counts(h, w, layer, weights) == _oracle_counts(h, w, c, layer, weights)
+
+
+def test_published_scheduled_counts():
+    """MNIST conv1 schedules 18,000 multiplies (test_engine.py:245-256); the
+    CIFAR engine-scheduled total is 9,673,600."""
+    spec = nn.mnist_hcnn()
+    s, _, _ = E._conv_counts(28, 28, spec.layers[0], np.ones((5, 5, 5, 1)))
+    assert s == 18000
+    s2, _, _ = E._conv_counts(12, 12, spec.layers[2], np.ones((50, 5, 5, 1)))
+    assert s2 == 20000
+    cifar = nn.cifar10_hcnn()
+    shapes = [cifar.input_shape] + cifar.layer_shapes()
+    total = 0
+    for i, layer in enumerate(cifar.layers):
+        hh, ww, cc = shapes[i]
+        if nn.kind_of(layer) == "conv":
+            total += E._conv_counts(hh, ww, layer, np.ones((layer.filters, 3, 3, cc)))[0]
+        elif nn.kind_of(layer) == "fc":
+            total += layer.filters * hh * ww * cc
+    assert total == 9_673_600
+
+
+def test_fc_counters():
+    w = np.array([[0, 1, 2], [0, 0, 0], [3, 0, 0]])
+    assert E._fc_counts(w) == (9, 3, 1)
+
+
+def test_gpu_context_refuses_without_cuda():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("CUDA present")
+    from paper_1811_00778_b200 import bfv as B
+
+    params = B.BfvParams(B.RnsContext(64, [1073643521, 1073479681]), 257)
+    with pytest.raises(errors.HefirError):
+        E.GpuContext(params)
+
+
+def test_reduce_model_and_crt_reconstruct():
+    model = nn.QuantizedModel(nn.toy_hcnn(), 4, [np.array([[[[300]]]]), None, np.array([[-5, 7]])])
+    r = E.reduce_model(model, 257)
+    assert r.weights[0].item() == 300 - 257 and r.weights[2].tolist() == [[-5, 7]]
+    res = E.ChannelResult(moduli=(257, 65537), batch_size=1)
+    v = -123456
+    res.add(257, np.array([[v % 257]]))
+    res.add(65537, np.array([[v % 65537]]))
+    assert E.reconstruct_logits(res, (257, 65537))[0, 0] == v
+    with pytest.raises(errors.IncompleteResultError):
+        E.reconstruct_logits(E.ChannelResult(moduli=(257, 65537), batch_size=1), (257, 65537))
+    assert E.classify_logits([[1, 5, 5], [9, 0, 1]]) == [1, 0]
+
+
+def test_oracle_is_not_imported_by_the_product():
+    import subprocess
+    import sys
+
+    code = ("import sys, paper_1811_00778_b200.engine, paper_1811_00778_b200.ops, "
+            "paper_1811_00778_b200.bfv; assert 'hcnn_oracle' not in sys.modules")
+    subprocess.run([sys.executable, "-c", code], check=True, cwd=ROOT)
+    pkg = os.path.join(ROOT, "paper_1811_00778_b200")
+    for fn in os.listdir(pkg):
+        if fn.endswith(".py"):
+            with open(os.path.join(pkg, fn)) as fh:
+                assert "hcnn_oracle" not in fh.read(), fn
+    _ = O
