@@ -95,18 +95,22 @@ int hcnn_upload_u64(hcnn_ctx* ctx, uint32_t* dst, const uint64_t* src, size_t co
 int hcnn_download_u64(hcnn_ctx* ctx, uint64_t* dst, const uint32_t* src, size_t count);
 int hcnn_sync(hcnn_ctx* ctx);
 
-/* Weights (host int64, any sign) reduced per prime of q into device
- * out[count][K] (the per-prime reduction of ring.accumulate_scaled,
- * ring.py:199-207 / RnsContext.reduce_scalar, ring.py:91-95). */
-int hcnn_reduce_weights(hcnn_ctx* ctx, const int64_t* w, size_t count, uint32_t* out);
+/* Layer weights (host int64, any sign) uploaded once.  Each weight w acts
+ * as w mod q_i on limb i, exactly like ring.accumulate_scaled (ring.py:199-207,
+ * RnsContext.reduce_scalar ring.py:91-95); weights below 2^15 in magnitude
+ * additionally get the lazy biased-u16 kernels. */
+typedef struct hcnn_weights hcnn_weights;
+int hcnn_weights_create(hcnn_ctx* ctx, const int64_t* w, size_t count, hcnn_weights** out);
+int hcnn_weights_destroy(hcnn_ctx* ctx, hcnn_weights* w);
 
 /* Convolution layer: engine.eval_conv (engine.py:237-303).
- * in: h*w*c cts, (y,x,c) row-major; weights wred [f][kh][kw][c/groups][K]. */
+ * in: h*w*c cts, (y,x,c) row-major; weights [f][kh][kw][c/groups]. */
 int hcnn_conv(hcnn_ctx* ctx, const uint32_t* in, uint32_t* out, int h, int w, int c,
-              const uint32_t* wred, int f, int kh, int kw, int sh, int sw, int padded, int groups);
-/* Dense layer: engine.eval_fc (engine.py:306-334); wred [n_out][n_in][K]. */
+              const hcnn_weights* wt, int f, int kh, int kw, int sh, int sw, int padded,
+              int groups);
+/* Dense layer: engine.eval_fc (engine.py:306-334); weights [n_out][n_in]. */
 int hcnn_fc(hcnn_ctx* ctx, const uint32_t* in, uint32_t* out, int n_in, int n_out,
-            const uint32_t* wred);
+            const hcnn_weights* wt);
 /* Sum-pool layer: engine.eval_pool (engine.py:367-397). */
 int hcnn_pool(hcnn_ctx* ctx, const uint32_t* in, uint32_t* out, int h, int w, int c, int extent,
               int sh, int sw);

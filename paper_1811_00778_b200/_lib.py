@@ -33,7 +33,8 @@ _SIGS = {
     "hcnn_upload_u64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]),
     "hcnn_download_u64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]),
     "hcnn_sync": (C.c_int, [C.c_void_p]),
-    "hcnn_reduce_weights": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "hcnn_weights_create": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
+    "hcnn_weights_destroy": (C.c_int, [C.c_void_p, C.c_void_p]),
     "hcnn_conv": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p] + [C.c_int] * 3
                   + [C.c_void_p] + [C.c_int] * 7),
     "hcnn_fc": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p]),

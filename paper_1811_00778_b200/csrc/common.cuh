@@ -17,6 +17,8 @@
 
 namespace hcnn {
 
+DI uint32_t umin_u32(uint32_t a, uint32_t b) { return a < b ? a : b; }
+
 constexpr int KMAX = 16;   // primes of q
 constexpr int KPMAX = 19;  // primes of the auxiliary base P (K+2 or K+3)
 constexpr int WMAX = 17;   // 32-bit words of (K+1) q
@@ -32,17 +34,17 @@ struct ConvTabs {
   uint64_t pmu[KPMAX];
   // Q -> P of a canonical [0, q) value
   uint32_t qhi[KMAX], qhis[KMAX];  // (q/q_i)^-1 mod q_i and its Shoup word
-  uint64_t qG[KMAX];               // floor(2^(60+qb) / q_i)
-  uint32_t qb[KMAX];               // bit length of q_i
-  uint32_t qhat_p[KMAX][KPMAX];    // (q/q_i) mod p_j
-  uint32_t negq_p[KPMAX];          // -q mod p_j
+  uint32_t qg[KMAX], qk[KMAX];     // fixed point: x/q_i ~ (x * qg_i << qk_i) / 2^59
+  uint32_t qpinv[KMAX];            // -q_i^-1 mod 2^32
+  uint32_t qhat_p[KMAX][KPMAX];    // (q/q_i) 2^32 mod p_j (Montgomery form)
+  uint32_t negq_p[KPMAX];          // -q 2^32 mod p_j (Montgomery form)
   uint32_t qhat_w[KMAX][WMAX];     // q/q_i, 32-bit words
   uint32_t q_w[WMAX];              // q, 32-bit words
   // P -> Q of a centred (-P/2, P/2) value
-  uint64_t pG[KPMAX];
-  uint32_t pb[KPMAX];
-  uint32_t phat_q[KPMAX][KMAX];  // (P/p_j) mod q_i
-  uint32_t negp_q[KMAX];         // -P mod q_i
+  uint32_t pg[KPMAX], pk[KPMAX];
+  uint32_t ppinv[KPMAX];         // -p_j^-1 mod 2^32
+  uint32_t phat_q[KPMAX][KMAX];  // (P/p_j) 2^32 mod q_i (Montgomery form)
+  uint32_t negp_q[KMAX];         // -P 2^32 mod q_i (Montgomery form)
   // scale-and-round: r~_i = d_i A_i + B_i  (mod q_i)
   //                  y~_j = d_j C_j + (p_j - r_j) E_j + F_j  (mod p_j)
   uint32_t A[KMAX], As[KMAX], B[KMAX];
@@ -59,17 +61,28 @@ struct NttTabs {
   const uint32_t* pinv;   // [K+KP]        -p^-1 mod 2^32 (Montgomery)
 };
 
-constexpr uint64_t FRAC_ONE = 1ull << 60;
+// fixed point of the CRT overflow estimates: 59 fractional bits
+constexpr int FRAC_BITS = 59;
+constexpr uint64_t FRAC_ONE = 1ull << FRAC_BITS;
 constexpr uint64_t FRAC_MASK = FRAC_ONE - 1;
+// per-term error bound of frac59 (units of 2^-59): below 2^30
+constexpr uint64_t FRAC_ERR = 1ull << 30;
 
 // words needed for (K+1) q with K primes below 2^30, plus one
 __host__ __device__ constexpr int words_for(int k) { return (30 * k + 5 + 31) / 32 + 1; }
 
-// floor(x * 2^60 / m) - e, e in [0, 2), from G = floor(2^(60+b)/m), b = bitlen(m)
-DI uint64_t frac60(uint32_t x, uint64_t G, uint32_t b) {
-  const uint64_t lo = (uint64_t)x * G;
-  const uint64_t hi = __umul64hi((uint64_t)x, G);
-  return (hi << (64 - b)) | (lo >> b);
+// x * 2^59 / m - e with 0 <= e < 2^30, for x < m: g = floor(2^(59-k)/m) < 2^32
+// (k = 0 for primes above 2^27), one 32x32->64 multiply
+DI uint64_t frac59(uint32_t x, uint32_t g, uint32_t k) { return ((uint64_t)x * g) << k; }
+
+// Montgomery reduction of a 64-bit sum: acc * 2^-32 mod p for acc < 3 * 2^62,
+// result fully reduced.  With constants pre-multiplied by 2^32 the sum of
+// products reduces to the plain value.
+DI uint32_t redc(uint64_t acc, uint32_t p, uint32_t pinv) {
+  const uint32_t m = (uint32_t)acc * pinv;
+  uint32_t r = (uint32_t)((acc + (uint64_t)m * p) >> 32);  // < acc/2^32 + p < 4p
+  r = umin_u32(r, r - 2 * p);
+  return umin_u32(r, r - p);
 }
 
 // S = sum_i xt_i * (q/q_i) as words, exact (column sums of 32-bit halves).
@@ -108,17 +121,17 @@ DI uint32_t mw_sub_mq(uint32_t (&S)[words_for(K)], uint32_t m, const ConvTabs& t
   return borrow;
 }
 
-// Exact v = floor(sum_i xt_i / q_i) for a canonical lift: 60-bit fixed point
-// (error in (-2K, 0] units of 2^-60), with an exact multiword decision when the
-// estimate is within that error of an integer (lifted value within ~2^-56 q of
-// q; astronomically rare for ciphertext data, but handled).
+// Exact v = floor(sum_i xt_i / q_i) for a canonical lift: 59-bit fixed point
+// (error in (-K 2^30, 0] units of 2^-59), with an exact multiword decision when
+// the estimate is within that error of an integer (lifted value within
+// ~K 2^-29 q of q: about one coefficient in 2^25, handled exactly).
 template <int K>
 DI uint32_t exact_v(const uint32_t (&xt)[K], const ConvTabs& tb) {
   uint64_t F = 0;
 #pragma unroll
-  for (int i = 0; i < K; ++i) F += frac60(xt[i], tb.qG[i], tb.qb[i]);
-  uint32_t V = (uint32_t)(F >> 60);
-  if ((F & FRAC_MASK) >= FRAC_ONE - 2 * (uint64_t)K - 2) {
+  for (int i = 0; i < K; ++i) F += frac59(xt[i], tb.qg[i], tb.qk[i]);
+  uint32_t V = (uint32_t)(F >> FRAC_BITS);
+  if ((F & FRAC_MASK) >= FRAC_ONE - K * FRAC_ERR) {
     uint32_t S[words_for(K)];
     mw_lift<K>(xt, tb, S);
     if (!mw_sub_mq<K>(S, V + 1, tb)) V += 1;
@@ -126,13 +139,25 @@ DI uint32_t exact_v(const uint32_t (&xt)[K], const ConvTabs& tb) {
   return V;
 }
 
+// sum_{i<K} x_i c_i (+ v c_v), c's in Montgomery form mod m, reduced:
+// one REDC per <= 11 products (3 * 2^62 headroom)
+template <int K, class Getc>
+DI uint32_t mont_dot(const uint32_t* x, Getc c, uint32_t v, uint32_t cv, uint32_t m, uint32_t minv) {
+  constexpr int H = K <= 11 ? K : (K + 1) / 2;
+  uint64_t a0 = (uint64_t)v * cv, a1 = 0;
+#pragma unroll
+  for (int i = 0; i < H; ++i) a0 += (uint64_t)x[i] * c(i);
+#pragma unroll
+  for (int i = H; i < K; ++i) a1 += (uint64_t)x[i] * c(i);
+  uint32_t r = redc(a0, m, minv);
+  if constexpr (H < K) r = add_mod(r, redc(a1, m, minv), m);
+  return r;
+}
+
 // x_j = (sum_i xt_i (q/q_i) - v q) mod p_j
 template <int K>
 DI uint32_t q_to_p(const uint32_t (&xt)[K], uint32_t v, int j, const ConvTabs& tb) {
-  uint64_t acc = (uint64_t)v * tb.negq_p[j];
-#pragma unroll
-  for (int i = 0; i < K; ++i) acc += (uint64_t)xt[i] * tb.qhat_p[i][j];
-  return reduce64(acc, tb.p[j], tb.pmu[j]);
+  return mont_dot<K>(xt, [&](int i) { return tb.qhat_p[i][j]; }, v, tb.negq_p[j], tb.p[j], tb.ppinv[j]);
 }
 
 }  // namespace hcnn

@@ -99,19 +99,15 @@ __global__ void __launch_bounds__(128)
     uint32_t acc = add_mod(mul_shoup(dp[j], tb.C[j], tb.Cs[j], pj), mul_shoup(pj - rj, tb.Ej[j], tb.Ejs[j], pj), pj);
     acc = add_mod(acc, tb.F[j], pj);
     yt[j] = acc;
-    F += frac60(acc, tb.pG[j], tb.pb[j]);
+    F += frac59(acc, tb.pg[j], tb.pk[j]);
   }
-  const uint32_t vp = (uint32_t)((F + (FRAC_ONE >> 1)) >> 60);
+  const uint32_t vp = (uint32_t)((F + (FRAC_ONE >> 1)) >> FRAC_BITS);
 
   // back to Q: y_i = (sum_j y~_j (P/p_j) - vp P) mod q_i
   uint32_t yq[K];
 #pragma unroll
-  for (int i = 0; i < K; ++i) {
-    uint64_t acc = (uint64_t)vp * tb.negp_q[i];
-#pragma unroll
-    for (int j = 0; j < KP; ++j) acc += (uint64_t)yt[j] * tb.phat_q[j][i];
-    yq[i] = reduce64(acc, tb.q[i], tb.qmu[i]);
-  }
+  for (int i = 0; i < K; ++i)
+    yq[i] = mont_dot<KP>(yt, [&](int j) { return tb.phat_q[j][i]; }, vp, tb.negp_q[i], tb.q[i], tb.qpinv[i]);
   uint32_t* dst = y3 + (size_t)blockIdx.y * K * N + n;
 #pragma unroll
   for (int i = 0; i < K; ++i) dst[(size_t)i * N] = yq[i];
@@ -123,10 +119,10 @@ __global__ void __launch_bounds__(128)
   for (int i = 0; i < K; ++i) xt[i] = mul_shoup(yq[i], tb.qhi[i], tb.qhis[i], tb.q[i]);
   uint64_t Fq = 0;
 #pragma unroll
-  for (int i = 0; i < K; ++i) Fq += frac60(xt[i], tb.qG[i], tb.qb[i]);
+  for (int i = 0; i < K; ++i) Fq += frac59(xt[i], tb.qg[i], tb.qk[i]);
   uint32_t S[words_for(K)];
   mw_lift<K>(xt, tb, S);
-  mw_sub_mq<K>(S, (uint32_t)(Fq >> 60), tb);  // S - V q >= 0 with V in {v-1, v}
+  mw_sub_mq<K>(S, (uint32_t)(Fq >> FRAC_BITS), tb);  // S - V q >= 0 with V in {v-1, v}
   {
     uint32_t Tq[words_for(K)];
 #pragma unroll

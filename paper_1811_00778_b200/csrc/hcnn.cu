@@ -46,6 +46,13 @@ void fail(int code, const std::string& m) { throw Error{code, m}; }
 
 }  // namespace
 
+struct hcnn_weights {
+  size_t count = 0;
+  int small = 0;          // all |w| < 2^15: biased u16 path
+  uint16_t* wb = nullptr; // [count] biased (small)
+  uint32_t* wred = nullptr;  // [count][K] residues mod q_i (general)
+};
+
 struct hcnn_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -133,6 +140,22 @@ struct hcnn_ctx {
 };
 
 namespace {
+
+// fixed point x/m ~ (x * g << k) / 2^59 with g = floor(2^(59-k)/m) < 2^32
+void fixed59(u64 m, uint32_t* g, uint32_t* k) {
+  uint32_t kk = 0;
+  while ((((u128)1 << (59 - kk)) / m) >> 32) ++kk;
+  *g = (uint32_t)(((u128)1 << (59 - kk)) / m);
+  *k = kk;
+}
+
+uint32_t neg_inv32(uint32_t p) {
+  uint32_t inv = 1;  // Newton: p^-1 mod 2^32
+  for (int it = 0; it < 5; ++it) inv *= 2u - p * inv;
+  return 0u - inv;
+}
+
+u64 mont_form(u64 x, u64 p) { return (u64)(((u128)x << 32) % p); }
 
 void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
   const uint32_t N = c->N;
@@ -225,12 +248,10 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
     const u64 qhi = invmod64(mod_small(qhat, qi), qi);
     tb.qhi[i] = (uint32_t)qhi;
     tb.qhis[i] = shoup_of((uint32_t)qhi, (uint32_t)qi);
-    int b = 0;
-    while ((1ull << b) <= qi) ++b;
-    tb.qb[i] = b;
-    tb.qG[i] = (uint64_t)(((u128)1 << (60 + b)) / qi);
+    fixed59(qi, &tb.qg[i], &tb.qk[i]);
+    tb.qpinv[i] = neg_inv32((uint32_t)qi);
     for (int w2 = 0; w2 < WMAX; ++w2) tb.qhat_w[i][w2] = qhat.word(w2);
-    for (uint32_t j = 0; j < c->KP; ++j) tb.qhat_p[i][j] = (uint32_t)mod_small(qhat, P[j]);
+    for (uint32_t j = 0; j < c->KP; ++j) tb.qhat_p[i][j] = (uint32_t)mont_form(mod_small(qhat, P[j]), P[j]);
     // scale: r~_i = (t d + h) qhi = d (t qhi) + h qhi
     const u64 A = mulmod64(t % qi, qhi, qi);
     tb.A[i] = (uint32_t)A;
@@ -241,14 +262,12 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
     const u64 pj = P[j];
     tb.p[j] = (uint32_t)pj;
     tb.pmu[j] = (uint64_t)(((u128)1 << 64) / pj);
-    tb.negq_p[j] = (uint32_t)((pj - mod_small(Q, pj)) % pj);
+    tb.negq_p[j] = (uint32_t)mont_form((pj - mod_small(Q, pj)) % pj, pj);
+    tb.ppinv[j] = neg_inv32((uint32_t)pj);
     const Big phat = div_small(Pp, pj);
     const u64 phi = invmod64(mod_small(phat, pj), pj);
-    int b = 0;
-    while ((1ull << b) <= pj) ++b;
-    tb.pb[j] = b;
-    tb.pG[j] = (uint64_t)(((u128)1 << (60 + b)) / pj);
-    for (uint32_t i = 0; i < c->K; ++i) tb.phat_q[j][i] = (uint32_t)mod_small(phat, q[i]);
+    fixed59(pj, &tb.pg[j], &tb.pk[j]);
+    for (uint32_t i = 0; i < c->K; ++i) tb.phat_q[j][i] = (uint32_t)mont_form(mod_small(phat, q[i]), q[i]);
     // y~_j = (t d + h - r) q^-1 phi = d C + (p - r) E + F
     const u64 E = mulmod64(invmod64(mod_small(Q, pj), pj), phi, pj);
     const u64 C = mulmod64(t % pj, E, pj);
@@ -258,7 +277,8 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
     tb.Ejs[j] = shoup_of((uint32_t)E, (uint32_t)pj);
     tb.F[j] = (uint32_t)mulmod64(mod_small(h, pj), E, pj);
   }
-  for (uint32_t i = 0; i < c->K; ++i) tb.negp_q[i] = (uint32_t)((q[i] - mod_small(Pp, q[i])) % q[i]);
+  for (uint32_t i = 0; i < c->K; ++i)
+    tb.negp_q[i] = (uint32_t)mont_form((q[i] - mod_small(Pp, q[i])) % q[i], q[i]);
 
   // upload
   CK(cudaMalloc(&c->d_prime, L * sizeof(uint32_t)));
@@ -862,25 +882,56 @@ int hcnn_sync(hcnn_ctx* c) {
   });
 }
 
-int hcnn_reduce_weights(hcnn_ctx* c, const int64_t* w, size_t count, uint32_t* out) {
+int hcnn_weights_create(hcnn_ctx* c, const int64_t* w, size_t count, hcnn_weights** out) {
   return guarded([&] {
-    if (count == 0) return;
+    if (!out || (!w && count)) fail(HCNN_ERR_PARAM, "null argument");
     CK(cudaSetDevice(c->device));
-    int64_t* stage = nullptr;
-    CK(cudaMallocAsync((void**)&stage, count * sizeof(int64_t), c->stream));
-    CK(cudaMemcpyAsync(stage, w, count * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
-    k_reduce_weights<<<cdiv(count, 256), 256, 0, c->stream>>>(stage, count, out, c->d_prime, (int)c->K);
-    c->launched("k_reduce_weights");
-    CK(cudaFreeAsync(stage, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    auto h = std::make_unique<hcnn_weights>();
+    h->count = count;
+    int64_t big = 0;
+    for (size_t i = 0; i < count; ++i) {
+      const int64_t a = w[i] < 0 ? -w[i] : w[i];
+      if (w[i] == INT64_MIN) big = INT64_MAX;
+      else if (a > big) big = a;
+    }
+    h->small = big < (int64_t)WBIAS;
+    if (count) {
+      int64_t* stage = nullptr;
+      CK(cudaMallocAsync((void**)&stage, count * sizeof(int64_t), c->stream));
+      CK(cudaMemcpyAsync(stage, w, count * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+      if (h->small) {
+        CK(cudaMalloc((void**)&h->wb, count * sizeof(uint16_t)));
+        k_bias_weights<<<cdiv(count, 256), 256, 0, c->stream>>>(stage, count, h->wb);
+        c->launched("k_bias_weights");
+      }
+      // residues mod q_i: the general path (and the fallback when a layer's
+      // small weights exceed the shared-memory stage)
+      CK(cudaMalloc((void**)&h->wred, count * c->K * sizeof(uint32_t)));
+      k_reduce_weights<<<cdiv(count, 256), 256, 0, c->stream>>>(stage, count, h->wred, c->d_prime, (int)c->K);
+      c->launched("k_reduce_weights");
+      CK(cudaFreeAsync(stage, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+    }
+    *out = h.release();
+  });
+}
+
+int hcnn_weights_destroy(hcnn_ctx* c, hcnn_weights* h) {
+  return guarded([&] {
+    if (!h) return;
+    cudaSetDevice(c->device);
+    if (h->wb) cudaFree(h->wb);
+    if (h->wred) cudaFree(h->wred);
+    delete h;
   });
 }
 
 int hcnn_conv(hcnn_ctx* c, const uint32_t* in, uint32_t* out, int h, int w, int ch,
-              const uint32_t* wred, int f, int kh, int kw, int sh, int sw, int padded, int groups) {
+              const hcnn_weights* wt, int f, int kh, int kw, int sh, int sw, int padded, int groups) {
   return guarded([&] {
     c->mark();
     if (groups < 1 || ch % groups || f % groups) fail(HCNN_ERR_PARAM, "conv: channel mismatch");
+    if (!wt || wt->count != (size_t)f * kh * kw * (ch / groups)) fail(HCNN_ERR_PARAM, "conv: weight count");
     ConvGeom g;
     g.h = h;
     g.w = w;
@@ -908,10 +959,24 @@ int hcnn_conv(hcnn_ctx* c, const uint32_t* in, uint32_t* out, int h, int w, int 
     const size_t zdim = (size_t)g.oh * g.ow * (f / fb);
     if (zdim > 65535) fail(HCNN_ERR_CAPACITY, "conv: too many output blocks for one launch");
     dim3 grid(cdiv(c->N / 4, tpb), 2 * c->K, (unsigned)zdim);
+    const size_t smem = (size_t)fb * kh * kw * g.cg * sizeof(uint16_t);
+    if (wt->small && smem <= 48 * 1024) {
+      switch (fb) {
+#define X(FB)                                                                                          \
+  case FB:                                                                                             \
+    k_conv_sw<FB><<<grid, tpb, smem, c->stream>>>(in, out, wt->wb, g, (int)c->K, (int)c->N, c->d_prime, c->d_mu); \
+    break;
+        X(1) X(2) X(4) X(5) X(8)
+#undef X
+      }
+      c->launched("k_conv");
+      return;
+    }
+    if (!wt->wred) fail(HCNN_ERR_CAPACITY, "conv: filter too large for the small-weight kernel");
     switch (fb) {
 #define X(FB)                                                                                       \
   case FB:                                                                                          \
-    k_conv<FB><<<grid, tpb, 0, c->stream>>>(in, out, wred, g, (int)c->K, (int)c->N, c->d_prime, c->d_mu); \
+    k_conv<FB><<<grid, tpb, 0, c->stream>>>(in, out, wt->wred, g, (int)c->K, (int)c->N, c->d_prime, c->d_mu); \
     break;
       X(1) X(2) X(4) X(5) X(8)
 #undef X
@@ -920,14 +985,22 @@ int hcnn_conv(hcnn_ctx* c, const uint32_t* in, uint32_t* out, int h, int w, int 
   });
 }
 
-int hcnn_fc(hcnn_ctx* c, const uint32_t* in, uint32_t* out, int n_in, int n_out, const uint32_t* wred) {
+int hcnn_fc(hcnn_ctx* c, const uint32_t* in, uint32_t* out, int n_in, int n_out, const hcnn_weights* wt) {
   return guarded([&] {
     c->mark();
+    if (!wt || wt->count != (size_t)n_in * n_out) fail(HCNN_ERR_PARAM, "fc: weight count");
     CK(cudaSetDevice(c->device));
     const unsigned tpb = c->N >= 512 ? 128 : (c->N / 4 >= 32 ? c->N / 4 : 32);
     constexpr int OB = 8;
     dim3 grid(cdiv(c->N / 4, tpb), 2 * c->K, cdiv(n_out, OB));
-    k_fc<OB><<<grid, tpb, 0, c->stream>>>(in, out, wred, n_in, n_out, (int)c->K, (int)c->N, c->d_prime, c->d_mu);
+    const size_t smem = (size_t)OB * n_in * sizeof(uint16_t);
+    if (wt->small && smem <= 48 * 1024) {
+      k_fc_sw<OB><<<grid, tpb, smem, c->stream>>>(in, out, wt->wb, n_in, n_out, (int)c->K, (int)c->N, c->d_prime, c->d_mu);
+      c->launched("k_fc");
+      return;
+    }
+    if (!wt->wred) fail(HCNN_ERR_CAPACITY, "fc: layer too wide for the small-weight kernel");
+    k_fc<OB><<<grid, tpb, 0, c->stream>>>(in, out, wt->wred, n_in, n_out, (int)c->K, (int)c->N, c->d_prime, c->d_mu);
     c->launched("k_fc");
   });
 }

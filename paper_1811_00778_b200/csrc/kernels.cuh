@@ -113,6 +113,116 @@ __global__ void k_fc(const uint32_t* __restrict__ in, uint32_t* __restrict__ out
   }
 }
 
+// ---- small-weight MAC: |w| < 2^15.  Weights enter biased, wb = w + 2^15 in
+// [0, 2^16), so every product wb * x < 2^46 is non-negative and 2^18 of them
+// fit a u64 with no intermediate reduction; out = (sum wb x - 2^15 sum x) mod p.
+constexpr uint32_t WBIAS = 1u << 15;
+
+DI uint32_t unbias(uint64_t acc, uint64_t xsum, uint32_t p, uint64_t mu) {
+  return sub_mod(reduce64(acc, p, mu), reduce64(xsum << 15, p, mu), p);
+}
+
+// grid: x = coefficient quads, y = part*K + limb, z = out position * nfb + filter block;
+// wb: [F][kh][kw][cg] biased u16; smem: FB * taps u16
+template <int FB>
+__global__ void __launch_bounds__(128)
+    k_conv_sw(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+              const uint16_t* __restrict__ wb, ConvGeom g, int K, int N,
+              const uint32_t* __restrict__ primes, const uint64_t* __restrict__ mus) {
+  extern __shared__ uint16_t wsm[];
+  const int taps = g.kh * g.kw * g.cg;
+  const int nfb = g.f / FB;
+  const int pos = blockIdx.z / nfb, fbk = blockIdx.z % nfb;
+  const int f0 = fbk * FB;
+  for (int idx = threadIdx.x; idx < FB * taps; idx += blockDim.x) wsm[idx] = wb[(size_t)f0 * taps + idx];
+  __syncthreads();
+  const int quad = blockIdx.x * blockDim.x + threadIdx.x;
+  if (quad * 4 >= N) return;
+  const int limb = blockIdx.y % K, part = blockIdx.y / K;
+  const int oy = pos / g.ow, ox = pos % g.ow;
+  const int grp = f0 / g.per_group;
+  uint64_t acc[FB][4], xs[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int f = 0; f < FB; ++f) acc[f][0] = acc[f][1] = acc[f][2] = acc[f][3] = 0;
+  for (int ky = 0; ky < g.kh; ++ky) {
+    const int iy = oy * g.sh + ky - g.ph;
+    if (iy < 0 || iy >= g.h) continue;
+    for (int kx = 0; kx < g.kw; ++kx) {
+      const int ix = ox * g.sw + kx - g.pw;
+      if (ix < 0 || ix >= g.w) continue;
+      const size_t in_ct0 = ((size_t)iy * g.w + ix) * g.c + grp * g.cg;
+      const int tap0 = (ky * g.kw + kx) * g.cg;
+      for (int ci = 0; ci < g.cg; ++ci) {
+        const uint4 xv = __ldg(reinterpret_cast<const uint4*>(in + (((in_ct0 + ci) * 2 + part) * K + limb) * N) + quad);
+        xs[0] += xv.x;
+        xs[1] += xv.y;
+        xs[2] += xv.z;
+        xs[3] += xv.w;
+#pragma unroll
+        for (int f = 0; f < FB; ++f) mac4(acc[f], wsm[f * taps + tap0 + ci], xv);
+      }
+    }
+  }
+  const uint32_t p = primes[limb];
+  const uint64_t mu = mus[limb];
+#pragma unroll
+  for (int f = 0; f < FB; ++f) {
+    const size_t out_ct = (size_t)pos * g.f + f0 + f;
+    uint4 r;
+    r.x = unbias(acc[f][0], xs[0], p, mu);
+    r.y = unbias(acc[f][1], xs[1], p, mu);
+    r.z = unbias(acc[f][2], xs[2], p, mu);
+    r.w = unbias(acc[f][3], xs[3], p, mu);
+    *(reinterpret_cast<uint4*>(out + ((out_ct * 2 + part) * K + limb) * N) + quad) = r;
+  }
+}
+
+// dense, small weights: wb [n_out][n_in] biased u16; smem OB * n_in u16
+template <int OB>
+__global__ void __launch_bounds__(128)
+    k_fc_sw(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+            const uint16_t* __restrict__ wb, int n_in, int n_out, int K, int N,
+            const uint32_t* __restrict__ primes, const uint64_t* __restrict__ mus) {
+  extern __shared__ uint16_t wsm[];
+  const int o0 = blockIdx.z * OB;
+  const int nob = min(OB, n_out - o0);
+  for (int idx = threadIdx.x; idx < nob * n_in; idx += blockDim.x) wsm[idx] = wb[(size_t)o0 * n_in + idx];
+  __syncthreads();
+  const int quad = blockIdx.x * blockDim.x + threadIdx.x;
+  if (quad * 4 >= N) return;
+  const int limb = blockIdx.y % K, part = blockIdx.y / K;
+  uint64_t acc[OB][4], xs[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int o = 0; o < OB; ++o) acc[o][0] = acc[o][1] = acc[o][2] = acc[o][3] = 0;
+  for (int i = 0; i < n_in; ++i) {
+    const uint4 xv = __ldg(reinterpret_cast<const uint4*>(in + (((size_t)i * 2 + part) * K + limb) * N) + quad);
+    xs[0] += xv.x;
+    xs[1] += xv.y;
+    xs[2] += xv.z;
+    xs[3] += xv.w;
+#pragma unroll
+    for (int o = 0; o < OB; ++o)
+      if (o < nob) mac4(acc[o], wsm[o * n_in + i], xv);
+  }
+  const uint32_t p = primes[limb];
+  const uint64_t mu = mus[limb];
+#pragma unroll
+  for (int o = 0; o < OB; ++o) {
+    if (o >= nob) break;
+    uint4 r;
+    r.x = unbias(acc[o][0], xs[0], p, mu);
+    r.y = unbias(acc[o][1], xs[1], p, mu);
+    r.z = unbias(acc[o][2], xs[2], p, mu);
+    r.w = unbias(acc[o][3], xs[3], p, mu);
+    *(reinterpret_cast<uint4*>(out + (((size_t)(o0 + o) * 2 + part) * K + limb) * N) + quad) = r;
+  }
+}
+
+__global__ void k_bias_weights(const int64_t* __restrict__ w, size_t n, uint16_t* __restrict__ out) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) out[t] = (uint16_t)(w[t] + (int64_t)WBIAS);
+}
+
 // sum-pool: grid x = quads, y = part*K + limb, z = output ct
 __global__ void k_pool(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int h, int w,
                        int c, int e, int sh, int sw, int ow, int K, int N,

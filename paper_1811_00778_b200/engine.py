@@ -203,30 +203,29 @@ class GpuContext:
                    "hcnn_set_public_key")
         self._pk_ref = weakref.ref(pk)
 
-    def reduced_weights(self, weights) -> torch.Tensor:
-        """int weights -> device [count][K] residues mod q_i (cached)."""
+    def weights(self, weights):
+        """Layer weights -> library weight handle (cached by content)."""
         w = np.asarray(weights)
-        if w.dtype == object:
-            w = np.array([int(x) for x in w.reshape(-1)], dtype=object)
-            big = max((abs(int(x)) for x in w), default=0)
-            if big >= (1 << 62):
-                w = np.array([[int(x) % p for p in self.primes] for x in w], dtype=np.int64)
-                key = ("pre", w.shape, hashlib.blake2b(w.tobytes(), digest_size=16).digest())
-                if key not in self._weights:
-                    self._weights[key] = torch.from_numpy(w.astype(np.int32)).to(f"cuda:{self.device}")
-                return self._weights[key]
+        if w.dtype == object or not np.issubdtype(w.dtype, np.integer):
+            ints = [int(x) for x in w.reshape(-1)]
+            if max((abs(x) for x in ints), default=0) >= (1 << 63):
+                raise ParameterMismatchError("weights must fit in int64")
+            w = np.array(ints, dtype=np.int64)
         w = np.ascontiguousarray(w.reshape(-1), dtype=np.int64)
         key = (w.shape, hashlib.blake2b(w.tobytes(), digest_size=16).digest())
-        out = self._weights.get(key)
-        if out is None:
-            out = torch.empty((w.size, self.K), dtype=torch.int32, device=f"cuda:{self.device}")
+        handle = self._weights.get(key)
+        if handle is None:
+            h = _lib.C.c_void_p()
             self.bind_stream()
-            _lib.check(_lib.lib().hcnn_reduce_weights(self.handle, w.ctypes.data, w.size,
-                                                      out.data_ptr()), "hcnn_reduce_weights")
+            _lib.check(_lib.lib().hcnn_weights_create(self.handle, w.ctypes.data, w.size, _lib.C.byref(h)),
+                       "hcnn_weights_create")
             if len(self._weights) > 64:
+                for old in self._weights.values():
+                    _lib.lib().hcnn_weights_destroy(self.handle, old)
                 self._weights.clear()
-            self._weights[key] = out
-        return out
+            self._weights[key] = h
+            handle = h
+        return handle
 
 
 _CTXS: dict = {}
@@ -408,10 +407,10 @@ def eval_conv(tensor, layer, weights, params, counter, workers: int = 1, capacit
     pw = (kw - 1) // 2 if layer.padded else 0
     oh = (h + 2 * ph - kh) // sh + 1
     ow = (w + 2 * pw - kw) // sw + 1
-    wred = g.reduced_weights(weights)
+    wt = g.weights(weights)
     out = g.empty(oh * ow * f)
     g.bind_stream()
-    _lib.check(_lib.lib().hcnn_conv(g.handle, _ptr(src.data), _ptr(out), h, w, c, _ptr(wred), f,
+    _lib.check(_lib.lib().hcnn_conv(g.handle, _ptr(src.data), _ptr(out), h, w, c, wt, f,
                                     kh, kw, sh, sw, int(bool(layer.padded)), layer.groups),
                layer.name)
     _count(counter, *_conv_counts(h, w, layer, weights))
@@ -429,10 +428,10 @@ def eval_fc(tensor, layer, weights, params, counter, workers: int = 1):
         raise ParameterMismatchError(f"{layer.name}: weight width != tensor size")
     src, was_host = _as_gpu(tensor, params)
     g = context_for(params, src.data.device)
-    wred = g.reduced_weights(weights)
+    wt = g.weights(weights)
     out = g.empty(outputs)
     g.bind_stream()
-    _lib.check(_lib.lib().hcnn_fc(g.handle, _ptr(src.data), _ptr(out), in_count, outputs, _ptr(wred)),
+    _lib.check(_lib.lib().hcnn_fc(g.handle, _ptr(src.data), _ptr(out), in_count, outputs, wt),
                layer.name)
     _count(counter, *_fc_counts(weights))
     res = GpuCipherTensor((1, 1, outputs), out, tensor.delta * layer.weight_scale, params.t, params,
