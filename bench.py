@@ -141,34 +141,41 @@ class ClockSampler:
 # ---------------------------------------------------------------- work model
 
 
-def kernel_work(name: str, K: int, KP: int, D: int, N: int, per_launch_cts: float):
-    """Algorithmic (bytes, IMAD-equivalents) of one launch of a hot kernel.
+def kernel_work(name: str, K: int, KP: int, D: int, N: int, cts: float):
+    """Algorithmic (HBM bytes, IMAD issue slots) of one launch over `cts`
+    ciphertexts.
 
-    IMAD-equivalents count 3 per Shoup/Barrett modular multiply (NTT
-    butterfly, pointwise product) and 1 per lazy 64-bit multiply-accumulate;
-    bytes are the compulsory HBM reads + writes of the kernel's operands
-    (u32 residues, each touched once).  DESIGN.md section 4 derives them.
+    IMAD slots: the integer multiplier (fmaheavy pipe) issues a 32-bit IMAD in
+    one slot and IMAD.HI / IMAD.WIDE in two (measured: 18.4 vs 9.0 T/s), so a
+    Shoup butterfly costs 4 slots, a lazy 64-bit multiply-accumulate 2, a
+    Shoup modmul 4, a Barrett-64 modmul 8, a Montgomery REDC 3.  Bytes are
+    the compulsory DRAM reads + writes of the kernel's operands (u32
+    residues); keys and twiddles are L2-resident and counted once per launch.
     """
     logn = N.bit_length() - 1
     bfly = (N // 2) * logn
     L = K + KP
-    if name == "k_tensor":  # per ct: 2 fwd + 3 inv NTT per prime, 3 products + N^-1
-        imad = L * (5 * bfly * 3 + 3 * N * 3 + 3 * N * 3)
+    if name == "k_tensor":  # 2 fwd + 3 inv NTT per prime, 3 products, N^-1 scaling
+        slots = L * (5 * bfly * 4 + 3 * N * 8 + 3 * N * 4)
         byts = L * N * 4 * (2 + 3)
-    elif name == "k_relin":  # per ct: D fwd + 2 inv NTT per prime, 2D MACs per coeff
-        imad = K * ((D + 2) * bfly * 3 + 2 * D * N + 2 * N * 3)
-        byts = 4 * N * (D + 2 * D * K + 2 * K + 2 * K)
-    elif name == "k_scale":  # per ct: 3 parts x (K + KP(K+2) + KP K) MACs + digits
-        imad = 3 * N * (K * 3 + KP * (K + 2 * 3 + 3) + K * KP) + N * (K * 3 + K * (K + 1) + 2 * K)
+        fixed = L * N * 16
+    elif name == "k_relin":  # D fwd + 2 inv NTT per prime, 2D lazy MACs, N^-1
+        slots = K * ((D + 2) * bfly * 4 + 2 * D * N * 2 + 2 * N * 4)
+        byts = 4 * N * (D + 2 * K + 2 * K)
+        fixed = 4 * N * 2 * D * K + K * N * 16
+    elif name == "k_scale":  # per part: K Shoup, Q->P (K MAC + REDC) x KP, 3 Shoup x KP, P->Q
+        part = K * 4 + KP * (K * 2 + 3 * 2) + KP * 4 * 2 + K * (KP * 2 + 3 * 2) + (K + KP) * 2
+        digits = K * 4 + K * 2 + (K + 1) * (K * 2 + 2)
+        slots = N * (3 * part + digits)
         byts = 4 * N * (3 * L + 3 * K + D)
-    elif name == "k_extend":  # per ct: 2 parts x (K Shoup + K*KP MACs + fixed point)
-        imad = 2 * N * (K * 3 + K * KP + KP * 3 + 2 * K)
+        fixed = 0
+    elif name == "k_extend":  # per part: K Shoup, fixed point, KP x (K MAC + REDC)
+        slots = 2 * N * (K * 4 + K * 2 + KP * (K * 2 + 3))
         byts = 4 * N * 2 * (K + KP)
-    elif name in ("k_conv", "k_fc"):
-        return None
+        fixed = 0
     else:
         return None
-    return byts * per_launch_cts, imad * per_launch_cts
+    return byts * cts + fixed, slots * cts
 
 
 # ---------------------------------------------------------------- our arm
@@ -314,14 +321,15 @@ def run_ours(args):
                 "bound": "int" if int_bound else "hbm",
                 "achieved": round(tops if int_bound else gbs, 3),
                 "peak": round(imad_peak if int_bound else hbm_peak, 3),
-                "unit": "TIMAD/s" if int_bound else "GB/s",
+                "unit": "T IMAD-slots/s" if int_bound else "GB/s",
                 "frac": round(int_frac if int_bound else hbm_frac, 4),
                 "traffic": traffic,
                 "hbm": {"achieved_gbs": round(gbs, 1), "peak_gbs": hbm_peak, "frac": round(hbm_frac, 4),
                         "peak_source": hbm_src, "algorithmic_bytes_per_launch": byts},
-                "int": {"achieved_timad_s": round(tops, 3), "peak_timad_s": round(imad_peak, 3),
-                        "frac": round(int_frac, 4), "peak_source": "measured in bench.py (hcnn_int_peak IMAD probe)",
-                        "imad_equiv_per_launch": ops},
+                "int": {"achieved_t_slots_s": round(tops, 3), "peak_t_slots_s": round(imad_peak, 3),
+                        "frac": round(int_frac, 4),
+                        "peak_source": "measured in bench.py (hcnn_int_peak: 32-bit IMAD issue rate, fmaheavy pipe)",
+                        "imad_slots_per_launch": ops},
                 "avg_launch_ms": round(avg_s * 1e3, 4),
                 "share_of_step": round(tot / total_ms, 4),
             }
