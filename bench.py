@@ -49,30 +49,60 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=2024)
     ap.add_argument("--profile-only", action="store_true", help="one step, no timing (for ncu)")
+    ap.add_argument("--workload", default="mnist", choices=["mnist", "mnist3", "cifar"])
     return ap.parse_args()
 
 
 # ---------------------------------------------------------------- workload
 
 
-def build_workload(rank: int, seed: int):
-    from paper_1811_00778_b200 import bfv as B
-    from paper_1811_00778_b200 import engine as E
-    from paper_1811_00778_b200 import nn
+WORKLOADS = {
+    "mnist": dict(preset="1", net="mnist_hcnn", image=(28, 28, 1), pix=5, delta=4,
+                  desc="MNIST HCNN, preset 1 (N=8192, 11x30-bit primes, log q 330, t=5522259017729), "
+                       "one 8192-image slot-batch per GPU"),
+    "mnist3": dict(preset="3", net="mnist_hcnn", image=(28, 28, 1), pix=5, delta=4,
+                   desc="MNIST HCNN, preset 3 (N=16384, 11 primes, t=5522259017729), one 16384-image slot-batch per GPU"),
+    "cifar": dict(preset="5", net="cifar10_hcnn", image=(32, 32, 3), pix=256, delta=255,
+                  desc="CIFAR-10 HCNN, preset 5 (N=8192, 10 primes, log q 300, 10 plaintext-CRT channels "
+                       "t_i ~ 2^22), one 8192-image batch; the 10 channels are dealt round-robin over the GPUs"),
+}
 
-    n = 8192
-    params = B.BfvParams(B.RnsContext(n, SET1_PRIMES), MNIST_T)
-    sk, pk, rlk = B.keygen(params, np.random.default_rng(seed))
-    model = nn.random_model(nn.mnist_hcnn(), np.random.default_rng(seed + 1))
-    irng = np.random.default_rng(seed + 100 + rank)
-    images = list(irng.integers(0, 5, (n, 28, 28, 1)))
-    enc = B.SlotEncoder(MNIST_T, n)
+
+def build_workload(name: str, rank: int, world: int, seed: int):
+    """This rank's units of one step: (params, rlk, model, device input) per
+    (slot-batch, CRT channel).  MNIST: one batch per rank (replicas);
+    CIFAR: the 10 channels of one batch shared by the ranks."""
+    from paper_1811_00778_b200 import bfv as B
+    from paper_1811_00778_b200 import distributed as D
+    from paper_1811_00778_b200 import engine as E
+    from paper_1811_00778_b200 import nn, presets
+
+    w = WORKLOADS[name]
+    preset = presets.load_preset(w["preset"])
+    n = preset.ring_degree
+    spec = nn.NETWORKS[w["net"]]()
+    model = nn.random_model(spec, np.random.default_rng(seed + 1))
+    if preset.channels == 1:
+        plan = [[D.Unit(r, 0)] for r in range(world)]
+        n_batches = world
+    else:
+        plan = D.shard_plan(1, preset.channels, world)
+        n_batches = 1
+    units = []
     t0 = time.time()
-    gin = E.pack_images_device(images, E.PackingLayout(n, n), enc, pk, params,
-                               np.random.default_rng(seed + 200 + rank), delta=4)
-    setup_s = time.time() - t0
-    return dict(params=params, sk=sk, pk=pk, rlk=rlk, model=model, images=images, enc=enc,
-                gin=gin, setup_s=setup_s)
+    for u in plan[rank]:
+        params = presets.build_context(preset, u.channel)
+        sk, pk, rlk = B.keygen(params, np.random.default_rng(seed + 10 * u.channel))
+        irng = np.random.default_rng(seed + 100 + u.batch)
+        images = list(irng.integers(0, w["pix"], (n,) + w["image"]))
+        enc = B.SlotEncoder(params.t, n)
+        gin = E.pack_images_device(images, E.PackingLayout(n, n), enc, pk, params,
+                                   np.random.default_rng(seed + 200 + 31 * u.batch + u.channel),
+                                   delta=w["delta"])
+        units.append(dict(unit=u, params=params, sk=sk, rlk=rlk, gin=gin, enc=enc,
+                          model=E.reduce_model(model, params.t), images=images))
+    return dict(units=units, plan=plan, n_batches=n_batches, images_per_step=n * n_batches,
+                setup_s=time.time() - t0, desc=w["desc"], spec=spec, preset=preset)
 
 
 # ---------------------------------------------------------------- clocks
@@ -186,6 +216,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_1811_00778_b200 import _lib
+    from paper_1811_00778_b200 import distributed as D
     from paper_1811_00778_b200 import engine as E
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -194,54 +225,60 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    W = build_workload(rank, args.seed)
-    params, rlk, model, gin = W["params"], W["rlk"], W["model"], W["gin"]
-    g = E.context_for(params)
+    W = build_workload(args.workload, rank, world, args.seed)
+    units = W["units"]
+    ctxs = [E.context_for(u["params"]) for u in units]
+    counters = []
 
-    def step(x):
+    def evaluate(u, x=None):
         counter = E.OpCounter()
-        out = E.eval_network(x, model, rlk, params, counter)
+        out = E.eval_network(x if x is not None else u["gin"], u["model"], u["rlk"], u["params"], counter)
+        counters.append(counter)
+        return out
+
+    def step(inputs=None):
+        counters.clear()
+        outs = [evaluate(u, None if inputs is None else inputs[i]) for i, u in enumerate(units)]
         if world > 1:
-            buf = [torch.empty_like(out.data) for _ in range(world)] if rank == 0 else None
-            dist.gather(out.data, buf, dst=0)
-        return out, counter
+            D.gather_units([o.data for o in outs], W["plan"], rank, world)
+        return outs
 
     if args.profile_only:
-        step(gin)
+        step()
         torch.cuda.synchronize()
         return
 
     for _ in range(max(args.warmup, 0)):
-        out, counter = step(gin)
+        step()
     torch.cuda.synchronize()
 
-    # ---- timed region (device resident inputs; 565 MB > L2 per step)
+    # ---- timed region (device-resident inputs, larger than L2 each step)
     stream = torch.cuda.current_stream()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     L = _lib.lib()
-    _lib.check(L.hcnn_profile(g.handle, 1))
-    launches0 = g.launches()
+    for g in ctxs:
+        _lib.check(L.hcnn_profile(g.handle, 1))
+    launches0 = sum(g.launches() for g in ctxs)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            out, counter = step(gin)
+            outs = step()
         ev1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    launches = g.launches() - launches0
+    launches = sum(g.launches() for g in ctxs) - launches0
     ms = ev0.elapsed_time(ev1) / args.steps
-    buf = __import__("ctypes").create_string_buffer(1 << 16)
-    L.hcnn_profile_dump(g.handle, buf, len(buf))
-    _lib.check(L.hcnn_profile(g.handle, 0))
     prof = {}
-    for line in buf.value.decode().splitlines():
-        name, cnt, tot = line.split()
-        prof[name] = (int(cnt), float(tot))
+    for g in ctxs:
+        for name, (cnt, tot) in g.profile_read().items():
+            c0, t0 = prof.get(name, (0, 0.0))
+            prof[name] = (c0 + cnt, t0 + tot)
+        _lib.check(L.hcnn_profile(g.handle, 0))
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -249,9 +286,12 @@ def run_ours(args):
 
     # ---- end to end through the public API: pinned host u32 ciphertexts in,
     # logits out, copies inside the timed region
-    host_in = torch.empty(gin.data.shape, dtype=torch.int32, pin_memory=True)
-    host_in.copy_(gin.data)
-    host_out = torch.empty((10, 2, g.K, g.N), dtype=torch.int32, pin_memory=True)
+    host_in = []
+    for u in units:
+        h = torch.empty(u["gin"].data.shape, dtype=torch.int32, pin_memory=True)
+        h.copy_(u["gin"].data)
+        host_in.append(h)
+    host_out = [torch.empty(o.data.shape, dtype=torch.int32, pin_memory=True) for o in outs]
     e2e_steps = max(2, min(args.steps, 5))
     torch.cuda.synchronize()
     if world > 1:
@@ -261,10 +301,11 @@ def run_ours(args):
     w0 = time.perf_counter()
     e0.record(stream)
     for _ in range(e2e_steps):
-        x = E.GpuCipherTensor(gin.shape, host_in.to("cuda", non_blocking=True), gin.delta,
-                              gin.channel_modulus, params)
-        o, _ = step(x)
-        host_out.copy_(o.data, non_blocking=True)
+        xs = [E.GpuCipherTensor(u["gin"].shape, h.to("cuda", non_blocking=True), u["gin"].delta,
+                                u["gin"].channel_modulus, u["params"]) for u, h in zip(units, host_in)]
+        os_ = step(xs)
+        for ho, o in zip(host_out, os_):
+            ho.copy_(o.data, non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
     wall_e2e = (time.perf_counter() - w0) / e2e_steps
@@ -287,20 +328,21 @@ def run_ours(args):
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     hbm_src = "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback"
-    imad = __import__("ctypes").c_double()
-    _lib.check(L.hcnn_int_peak(local, 0, __import__("ctypes").byref(imad)))
+    import ctypes
+
+    imad = ctypes.c_double()
+    _lib.check(L.hcnn_int_peak(local, 0, ctypes.byref(imad)))
     imad_peak = imad.value / 1e12
     total_ms = sum(v[1] for v in prof.values())
     dom = max(prof, key=lambda k: prof[k][1]) if prof else None
     roof = None
-    kernels = {}
-    for name, (cnt, tot) in prof.items():
-        kernels[name] = {"launches": cnt, "ms_total": round(tot, 4), "share": round(tot / total_ms, 4)}
+    kernels = {name: {"launches": cnt, "ms_total": round(tot, 4), "share": round(tot / total_ms, 4)}
+               for name, (cnt, tot) in prof.items()}
+    n_sq = sum(c.hsquare for c in counters) * args.steps
+    g0 = ctxs[0]
     if dom:
         cnt, tot = prof[dom]
-        # cts processed by this kernel over the timed region
-        n_sq = counter.hsquare * args.steps
-        work = kernel_work(dom, g.K, g.KP, g.D, g.N, n_sq / cnt)
+        work = kernel_work(dom, g0.K, g0.KP, g0.D, g0.N, n_sq / cnt)
         avg_s = tot / cnt / 1e3
         if work:
             byts, ops = work
@@ -311,8 +353,8 @@ def run_ours(args):
             traffic = None
             try:
                 with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-                    traffic = json.load(fh).get(dom)
-                    traffic = traffic * (n_sq / cnt) if traffic else None
+                    per_ct = json.load(fh).get(dom)
+                traffic = round(per_ct * (n_sq / cnt)) if per_ct and args.workload == "mnist" else None
             except Exception:
                 pass
             int_bound = int_frac >= hbm_frac
@@ -325,19 +367,21 @@ def run_ours(args):
                 "frac": round(int_frac if int_bound else hbm_frac, 4),
                 "traffic": traffic,
                 "hbm": {"achieved_gbs": round(gbs, 1), "peak_gbs": hbm_peak, "frac": round(hbm_frac, 4),
-                        "peak_source": hbm_src, "algorithmic_bytes_per_launch": byts},
+                        "peak_source": hbm_src + " (of measured)", "algorithmic_bytes_per_launch": byts},
                 "int": {"achieved_t_slots_s": round(tops, 3), "peak_t_slots_s": round(imad_peak, 3),
                         "frac": round(int_frac, 4),
                         "peak_source": "measured in bench.py (hcnn_int_peak: 32-bit IMAD issue rate, fmaheavy pipe)",
                         "imad_slots_per_launch": ops},
                 "avg_launch_ms": round(avg_s * 1e3, 4),
                 "share_of_step": round(tot / total_ms, 4),
+                "note": "integer-pipe kernel: tensor cores unused by design; DESIGN.md section 4",
             }
 
-    images = 8192 * world
+    images = W["images_per_step"]
     value = images / (ms / 1e3)
-    in_bytes = int(host_in.numel() * 4)
-    out_bytes = int(host_out.numel() * 4)
+    in_bytes = int(sum(h.numel() for h in host_in) * 4)
+    out_bytes = int(sum(h.numel() for h in host_out) * 4)
+    c0 = counters[0]
     line = {
         "metric": METRIC,
         "value": round(value, 2),
@@ -348,18 +392,19 @@ def run_ours(args):
         "ms_per_step": round(ms, 4),
         "latency_s": round(ms / 1e3, 6),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "weak" if W["preset"].channels == 1 else "strong",
         "vs_baseline": None,
         "dtype": "u32",
         "data": "synthetic",
         "config": {
-            "workload": "MNIST HCNN, preset 1 (N=8192, 11x30-bit primes, log q 330, t=5522259017729), one 8192-image slot-batch per GPU",
-            "model": "mnist_hcnn conv5x5s2(5)-square-conv5x5s2(50,g5)-square-fc10, dense random 4-bit weights",
+            "workload": W["desc"],
+            "model": f"{W['spec'].name}, dense random 4-bit weights (every tap executes)",
             "global_batch": images,
-            "parallelism": f"replicas{world}" if world > 1 else "single",
-            "hsquare_per_step": counter.hsquare,
-            "mult_plain_per_step": counter.mult_plain_scheduled,
-            "l2_policy": "inputs 565 MB per GPU > 126 MB L2 (no flush needed)",
+            "parallelism": (f"replicas{world}" if W["preset"].channels == 1 else f"crt-channels/{world}") if world > 1 else "single",
+            "units_on_rank0": len(units),
+            "hsquare_per_unit": c0.hsquare,
+            "mult_plain_per_unit": c0.mult_plain_scheduled,
+            "l2_policy": "inputs per GPU >= 565 MB > 126 MB L2 (no flush needed)",
             "setup_s": round(W["setup_s"], 2),
         },
         "e2e": {"value": round(images / (e2e_ms / 1e3), 2), "unit": "images/s",
@@ -371,8 +416,8 @@ def run_ours(args):
         "roofline": roof,
         "clocks": clk.summary(),
     }
-    if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_sample(W, threads=1)
+    if world == 1 and not args.no_cpu_baseline and args.workload == "mnist":
+        line["cpu_baseline"] = cpu_baseline_sample(units[0], threads=1)
     print(json.dumps(line), flush=True)
 
 
@@ -384,7 +429,7 @@ def _oracle_inputs(W):
     import hcnn_oracle as O
 
     params = W["params"]
-    op = O.Params(O.Context(params.ring_degree, SET1_PRIMES), params.t)
+    op = O.Params(O.Context(params.ring_degree, [pm.value for pm in params.ctx.primes]), params.t)
     rlk = [(k0.residues, k1.residues) for k0, k1 in W["rlk"].components]
     x = W["gin"].data[:1].cpu().numpy().view(np.uint32).astype(np.int64)[0]
     return op, rlk, (x[0], x[1])
