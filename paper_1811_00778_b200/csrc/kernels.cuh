@@ -218,6 +218,186 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// ---- FP64 MAC for small integer weights (|w| < 2^22).  Residues x < 2^30
+// and weights are exact doubles; a product is below 2^52, and `flush` taps of
+// them stay below 2^53, so DFMA accumulates the exact integer sum (on the FP64
+// pipe, twice the rate of 64-bit integer multiply-adds).  Every `flush` taps
+// the accumulator is reduced mod p exactly (|acc| < p afterwards).
+DI double u32_to_f64(uint32_t x) {  // exact, without a conversion instruction
+  return __hiloint2double(0x43300000, (int)x) - 4503599627370496.0;
+}
+
+DI double fold_mod(double acc, double p, double pinv) {
+  const double qd = floor(acc * pinv);
+  return fma(-qd, p, acc);  // exact: |result| < 2p
+}
+
+DI uint32_t f64_mod(double acc, double p, double pinv) {
+  double r = fold_mod(acc, p, pinv);
+  if (r < 0) r += p;
+  if (r >= p) r -= p;
+  return (uint32_t)__double2uint_rn(r);
+}
+
+// grid: x = coefficient quads, y = part, z = out position * nfb + filter block;
+// the block loops over the K limbs, reusing its staged weights (doubles, one
+// copy for all limbs) and tap table (input ciphertext per tap, -1 when the tap
+// falls in the padding).  smem: FB * taps doubles + taps ints.
+template <int FB>
+__global__ void __launch_bounds__(128)
+    k_conv_f64(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+               const double* __restrict__ wd, ConvGeom g, int K, int N, int flush,
+               const uint32_t* __restrict__ primes) {
+  extern __shared__ double wsd[];
+  const int taps = g.kh * g.kw * g.cg;
+  int* tct = reinterpret_cast<int*>(wsd + FB * taps);
+  const int nfb = g.f / FB;
+  const int pos = blockIdx.z / nfb, fbk = blockIdx.z % nfb;
+  const int f0 = fbk * FB;
+  const int oy = pos / g.ow, ox = pos % g.ow;
+  const int grp = f0 / g.per_group;
+  for (int idx = threadIdx.x; idx < FB * taps; idx += blockDim.x) wsd[idx] = wd[(size_t)f0 * taps + idx];
+  for (int t = threadIdx.x; t < taps; t += blockDim.x) {
+    const int ci = t % g.cg, kk = t / g.cg;
+    const int ky = kk / g.kw, kx = kk % g.kw;
+    const int iy = oy * g.sh + ky - g.ph, ix = ox * g.sw + kx - g.pw;
+    tct[t] = (iy < 0 || iy >= g.h || ix < 0 || ix >= g.w) ? -1 : (iy * g.w + ix) * g.c + grp * g.cg + ci;
+  }
+  __syncthreads();
+  const int quad = blockIdx.x * blockDim.x + threadIdx.x;
+  if (quad * 4 >= N) return;
+  const int part = blockIdx.y;
+  const size_t ct_stride = (size_t)2 * K * N / 4;  // uint4 per ciphertext
+  for (int limb = 0; limb < K; ++limb) {
+    const double p = (double)primes[limb];
+    const double pinv = 1.0 / p;
+    const uint4* base = reinterpret_cast<const uint4*>(in + ((size_t)part * K + limb) * N) + quad;
+    double acc[FB][4];
+#pragma unroll
+    for (int f = 0; f < FB; ++f) acc[f][0] = acc[f][1] = acc[f][2] = acc[f][3] = 0.0;
+    int since = 0;
+    constexpr int U = 8;
+    for (int t = 0; t < taps; t += U) {
+      uint4 xv[U];
+      int ok[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int ct = t + u < taps ? tct[t + u] : -1;
+        ok[u] = ct >= 0;
+        xv[u] = ok[u] ? __ldg(base + (size_t)ct * ct_stride) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!ok[u]) continue;
+        const double x0 = u32_to_f64(xv[u].x), x1 = u32_to_f64(xv[u].y);
+        const double x2 = u32_to_f64(xv[u].z), x3 = u32_to_f64(xv[u].w);
+#pragma unroll
+        for (int f = 0; f < FB; ++f) {
+          const double w = wsd[f * taps + t + u];
+          acc[f][0] = fma(w, x0, acc[f][0]);
+          acc[f][1] = fma(w, x1, acc[f][1]);
+          acc[f][2] = fma(w, x2, acc[f][2]);
+          acc[f][3] = fma(w, x3, acc[f][3]);
+        }
+      }
+      since += U;
+      if (since >= flush - U) {
+        since = 0;
+#pragma unroll
+        for (int f = 0; f < FB; ++f)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[f][v] = fold_mod(acc[f][v], p, pinv);
+      }
+    }
+#pragma unroll
+    for (int f = 0; f < FB; ++f) {
+      const size_t out_ct = (size_t)pos * g.f + f0 + f;
+      uint4 r;
+      r.x = f64_mod(acc[f][0], p, pinv);
+      r.y = f64_mod(acc[f][1], p, pinv);
+      r.z = f64_mod(acc[f][2], p, pinv);
+      r.w = f64_mod(acc[f][3], p, pinv);
+      *(reinterpret_cast<uint4*>(out + ((out_ct * 2 + part) * K + limb) * N) + quad) = r;
+    }
+  }
+}
+
+// dense: wd [n_out][n_in] doubles staged CH inputs at a time (smem OB * CH doubles)
+template <int OB, int CH>
+__global__ void __launch_bounds__(128)
+    k_fc_f64(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+             const double* __restrict__ wd, int n_in, int n_out, int K, int N, int flush,
+             const uint32_t* __restrict__ primes) {
+  __shared__ double wsd[OB * CH];
+  const int o0 = blockIdx.z * OB;
+  const int nob = min(OB, n_out - o0);
+  const int quad = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = quad * 4 < N;
+  const int limb = blockIdx.y % K, part = blockIdx.y / K;
+  const double p = (double)primes[limb];
+  const double pinv = 1.0 / p;
+  double acc[OB][4];
+#pragma unroll
+  for (int o = 0; o < OB; ++o) acc[o][0] = acc[o][1] = acc[o][2] = acc[o][3] = 0.0;
+  int cnt = 0;
+  for (int c0 = 0; c0 < n_in; c0 += CH) {
+    const int len = min(CH, n_in - c0);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < OB * CH; idx += blockDim.x) {
+      const int o = idx / CH, i = idx % CH;
+      wsd[idx] = (o < nob && i < len) ? wd[(size_t)(o0 + o) * n_in + c0 + i] : 0.0;
+    }
+    __syncthreads();
+    if (!active) continue;
+    const size_t ct_stride = (size_t)2 * K * N / 4;
+    const uint4* base = reinterpret_cast<const uint4*>(in + ((size_t)part * K + limb) * N) + quad;
+    constexpr int U = 4;
+    for (int i = 0; i < len; i += U) {
+      uint4 xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = __ldg(base + (size_t)(c0 + min(i + u, len - 1)) * ct_stride);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (i + u >= len) break;
+        const double x0 = u32_to_f64(xv[u].x), x1 = u32_to_f64(xv[u].y);
+        const double x2 = u32_to_f64(xv[u].z), x3 = u32_to_f64(xv[u].w);
+#pragma unroll
+        for (int o = 0; o < OB; ++o) {
+          const double w = wsd[o * CH + i + u];
+          acc[o][0] = fma(w, x0, acc[o][0]);
+          acc[o][1] = fma(w, x1, acc[o][1]);
+          acc[o][2] = fma(w, x2, acc[o][2]);
+          acc[o][3] = fma(w, x3, acc[o][3]);
+        }
+      }
+      cnt += U;
+      if (cnt >= flush - U) {
+        cnt = 0;
+#pragma unroll
+        for (int o = 0; o < OB; ++o)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[o][v] = fold_mod(acc[o][v], p, pinv);
+      }
+    }
+  }
+  if (!active) return;
+#pragma unroll
+  for (int o = 0; o < OB; ++o) {
+    if (o >= nob) break;
+    uint4 r;
+    r.x = f64_mod(acc[o][0], p, pinv);
+    r.y = f64_mod(acc[o][1], p, pinv);
+    r.z = f64_mod(acc[o][2], p, pinv);
+    r.w = f64_mod(acc[o][3], p, pinv);
+    *(reinterpret_cast<uint4*>(out + (((size_t)(o0 + o) * 2 + part) * K + limb) * N) + quad) = r;
+  }
+}
+
+__global__ void k_weights_f64(const int64_t* __restrict__ w, size_t n, double* __restrict__ out) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) out[t] = (double)w[t];
+}
+
 __global__ void k_bias_weights(const int64_t* __restrict__ w, size_t n, uint16_t* __restrict__ out) {
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t < n) out[t] = (uint16_t)(w[t] + (int64_t)WBIAS);
