@@ -47,8 +47,12 @@ struct NttGeom {
   static constexpr bool SHFL_TAIL = SHFL_TAIL_ && REM > 0;
   static constexpr bool REG_TAIL = !SHFL_TAIL_ && REM > 0;
   static_assert(!SHFL_TAIL || T >= 32, "shuffle stages need full warps");
-  // shared-memory words for one padded row
+  // shared-memory words for one padded row; the NTT alternates between two
+  // such buffers (one barrier per exchange)
   static constexpr int SMEM_WORDS = N + 2 * (N >> 5) + 2;
+  static constexpr int XW = (SMEM_WORDS + 3) & ~3;
+  static constexpr int NTT_SMEM_WORDS = 2 * XW;
+  static constexpr int FWD_EXCHANGES = NFULL - 1 + (REG_TAIL ? 1 : 0);
   // pass P covers butterfly bits [lo(P), lo(P) + LOGE), from the top
   __host__ __device__ static constexpr int lo(int P) { return LOGN - (P + 1) * LOGE; }
 };
@@ -285,10 +289,10 @@ template <class G, int P>
 DI void fwd_from(uint32_t* x, uint32_t* s, const uint2* __restrict__ tw, uint32_t p, int tid) {
   if constexpr (P < G::NFULL) {
     if constexpr (P > 0) {
-      regs_to_smem<G, G::lo(P - 1)>(x, s, tid);
+      uint32_t* b = s + ((P - 1) & 1) * G::XW;  // exchange P-1
+      regs_to_smem<G, G::lo(P - 1)>(x, b, tid);
       __syncthreads();
-      smem_to_regs<G, G::lo(P)>(x, s, tid);
-      __syncthreads();
+      smem_to_regs<G, G::lo(P)>(x, b, tid);
     }
     fwd_pass<G, G::lo(P)>(x, tw, p, tid);
     fwd_from<G, P + 1>(x, s, tw, p, tid);
@@ -299,10 +303,12 @@ template <class G, int P>
 DI void inv_from(uint32_t* x, uint32_t* s, const uint2* __restrict__ itw, uint32_t p, int tid) {
   if constexpr (P >= 0) {
     if constexpr (P < G::NFULL - 1) {
-      regs_to_smem<G, G::lo(P + 1)>(x, s, tid);
+      // exchange index continues after the register-tail exchange (if any)
+      constexpr int XI = (G::REG_TAIL ? 1 : 0) + (G::NFULL - 2 - P);
+      uint32_t* b = s + (XI & 1) * G::XW;
+      regs_to_smem<G, G::lo(P + 1)>(x, b, tid);
       __syncthreads();
-      smem_to_regs<G, G::lo(P)>(x, s, tid);
-      __syncthreads();
+      smem_to_regs<G, G::lo(P)>(x, b, tid);
     }
     inv_pass<G, G::lo(P)>(x, itw, p, tid);
     inv_from<G, P - 1>(x, s, itw, p, tid);
@@ -383,21 +389,23 @@ DI void store_tiled(const uint32_t* x, uint32_t* __restrict__ row, int tid) {
 }
 
 // Forward negacyclic NTT: natural layout in (any values < 4p), spectral layout
-// out, fully reduced to [0, p).
+// out, fully reduced to [0, p).  `s`: G::NTT_SMEM_WORDS of shared memory (two
+// padded buffers used alternately, one barrier per exchange).
 template <class G>
 DI void ntt_fwd(uint32_t* x, uint32_t* s, const uint2* __restrict__ tw, uint32_t p, int tid) {
   fwd_from<G, 0>(x, s, tw, p, tid);
   if constexpr (G::SHFL_TAIL) {
     fwd_shfl<G, G::REM - 1>(x, tw, p, tid);
   } else if constexpr (G::REG_TAIL) {
+    uint32_t* b = s + ((G::NFULL - 1) & 1) * G::XW;
 #pragma unroll
-    for (int e = 0; e < G::E; ++e) s[sidx(pass_index<G::REM, G::LOGE>(tid, e))] = x[e];
+    for (int e = 0; e < G::E; ++e) b[sidx(pass_index<G::REM, G::LOGE>(tid, e))] = x[e];
     __syncthreads();
 #pragma unroll
-    for (int e = 0; e < G::E; ++e) x[e] = s[sidx(tail_index<G>(tid, e))];
-    __syncthreads();
+    for (int e = 0; e < G::E; ++e) x[e] = b[sidx(tail_index<G>(tid, e))];
     fwd_tail<G, 0>(x, tw, p, tid);
   }
+  if constexpr (G::FWD_EXCHANGES & 1) __syncthreads();
   const uint32_t p2 = 2 * p;
 #pragma unroll
   for (int e = 0; e < G::E; ++e) {
@@ -420,9 +428,9 @@ DI void ntt_inv(uint32_t* x, uint32_t* s, const uint2* __restrict__ itw, uint32_
     __syncthreads();
 #pragma unroll
     for (int e = 0; e < G::E; ++e) x[e] = s[sidx(pass_index<G::REM, G::LOGE>(tid, e))];
-    __syncthreads();
   }
   inv_from<G, G::NFULL - 1>(x, s, itw, p, tid);
+  if constexpr (G::FWD_EXCHANGES & 1) __syncthreads();
 #pragma unroll
   for (int e = 0; e < G::E; ++e) x[e] = mul_shoup(x[e], ninv.x, ninv.y, p);
 }

@@ -164,11 +164,12 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
 // copies one digit ahead of the compute.
 template <class G>
 struct RelinSmem {
-  static constexpr int XW = (G::SMEM_WORDS + 3) & ~3;  // 16-byte aligned key rows
-  static constexpr int STAGE_WORDS = XW + 2 * G::N;
+  // [two NTT exchange buffers][STAGES digit rows streamed by TMA][mbarriers]
+  static constexpr int STAGE_WORDS = G::N;
   static constexpr int LIMIT = 220 * 1024;
-  static constexpr int STAGES = 2 * STAGE_WORDS * 4 <= LIMIT ? 2 : (STAGE_WORDS * 4 <= LIMIT ? 1 : 0);
-  static constexpr int BYTES = STAGES ? STAGES * STAGE_WORDS * 4 + 16 * 2 : G::SMEM_WORDS * 4;
+  static constexpr int BASE = G::NTT_SMEM_WORDS;
+  static constexpr int STAGES = (BASE + 2 * G::N) * 4 <= LIMIT ? 2 : ((BASE + G::N) * 4 <= LIMIT ? 1 : 0);
+  static constexpr int BYTES = (BASE + STAGES * G::N) * 4 + 16 * 2;
 };
 
 // One CTA per (ct, prime of q).  dig: [B][D][N] base-w digits of c2;
@@ -199,17 +200,13 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
 
   const uint32_t* dig_ct = dig + ct * D * G::N;
   auto krow = [&](int i, int part) { return rlk + ((size_t)(i * 2 + part) * K + j) * G::N; };
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s + (SM::STAGES ? SM::STAGES * SM::STAGE_WORDS : 0));
-  auto stage = [&](int st) { return s + st * SM::STAGE_WORDS; };
-  auto issue = [&](int i) {  // elected thread: digit i and its rlk rows
-    uint32_t* b = stage(i % SM::STAGES);
+  uint32_t* stage0 = s + SM::BASE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage0 + SM::STAGES * G::N);
+  auto issue = [&](int i) {  // elected thread: digit row i into its stage
     uint64_t* bar = &bars[i % SM::STAGES];
-    constexpr uint32_t RB = G::N * 4;
     fence_proxy_async();
-    mbar_expect_tx(bar, 3 * RB);
-    bulk_g2s(b, dig_ct + (size_t)i * G::N, RB, bar);
-    bulk_g2s(b + SM::XW, krow(i, 0), RB, bar);
-    bulk_g2s(b + SM::XW + G::N, krow(i, 1), RB, bar);
+    mbar_expect_tx(bar, G::N * 4);
+    bulk_g2s(stage0 + (i % SM::STAGES) * G::N, dig_ct + (size_t)i * G::N, G::N * 4, bar);
   };
   if constexpr (SM::STAGES > 0) {
     if (tid == 0) {
@@ -222,16 +219,20 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
 
   for (int i = 0; i < D; ++i) {
     uint32_t x[G::E];
-    uint32_t* xs = s;  // exchange buffer of this digit
     if constexpr (SM::STAGES > 0) {
+      // with two stages, digit i+1 streams in while digit i is transformed;
+      // its buffer was last read before this thread's previous-digit barriers
       if constexpr (SM::STAGES == 2) {
         if (tid == 0 && i + 1 < D) issue(i + 1);
       }
-      xs = stage(i % SM::STAGES);
+      const uint32_t* row = stage0 + (i % SM::STAGES) * G::N;
       mbar_wait(&bars[i % SM::STAGES], (uint32_t)(i / SM::STAGES) & 1);
 #pragma unroll
-      for (int e = 0; e < G::E; ++e) x[e] = xs[natural_index<G>(tid, e)];
-      __syncthreads();  // the row buffer becomes the exchange buffer
+      for (int e = 0; e < G::E; ++e) x[e] = row[natural_index<G>(tid, e)];
+      if constexpr (SM::STAGES == 1) {
+        __syncthreads();
+        if (tid == 0 && i + 1 < D) issue(i + 1);
+      }
     } else {
       load_natural<G>(x, dig_ct + (size_t)i * G::N, tid);
     }
@@ -239,13 +240,12 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
 #pragma unroll
       for (int e = 0; e < G::E; ++e) x[e] = reduce64(x[e], p, mu);
     }
-    ntt_fwd<G>(x, xs, tw, p, tid);
+    ntt_fwd<G>(x, s, tw, p, tid);
 #pragma unroll
     for (int part = 0; part < 2; ++part) {
       Acc* acc = part ? acc1 : acc0;
       uint32_t k[G::E];
-      if constexpr (SM::STAGES > 0) load_tiled_smem<G>(k, xs + SM::XW + part * G::N, tid);
-      else load_tiled<G>(k, krow(i, part), tid);
+      load_tiled<G>(k, krow(i, part), tid);
 #pragma unroll
       for (int e = 0; e < G::E; ++e) {
         if constexpr (ACC64) {
@@ -264,12 +264,6 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
           acc0[e] = reduce64(acc0[e], p, mu);
           acc1[e] = reduce64(acc1[e], p, mu);
         }
-      }
-    }
-    if constexpr (SM::STAGES > 0) {
-      __syncthreads();  // this stage's buffers are free for refilling
-      if constexpr (SM::STAGES == 1) {
-        if (tid == 0 && i + 1 < D) issue(i + 1);
       }
     }
   }
@@ -377,7 +371,7 @@ __global__ void k_to_mont(uint32_t* __restrict__ rows, int limbs, NttTabs nt) {
 
 template <class G>
 void configure_smem() {
-  const int smem = G::SMEM_WORDS * sizeof(uint32_t);
+  const int smem = G::NTT_SMEM_WORDS * sizeof(uint32_t);
   cudaFuncSetAttribute(k_ntt_rows<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_tensor<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_relin<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, RelinSmem<G>::BYTES);
@@ -397,7 +391,7 @@ cudaError_t launch_with(int op, const NttLaunch& a) {
     configure_smem<G>();
     configured = true;
   }
-  const size_t smem = G::SMEM_WORDS * sizeof(uint32_t);
+  const size_t smem = G::NTT_SMEM_WORDS * sizeof(uint32_t);
   switch (op) {
     case 0:
       k_ntt_rows<G><<<a.grid, G::T, smem, a.stream>>>(a.rows, a.limbs, a.prime_off, a.inverse, a.nt);
