@@ -68,71 +68,91 @@ __global__ void __launch_bounds__(128)
 
 // d: [B][3][K+KP][N] exact tensor residues (coefficient domain).
 // y3: [B][3][K][N] = round(t d / q) mod q per part; dig (optional): [B][D][N].
-template <int K, int KP>
+// Each thread handles V coefficients (n, n + blockDim, ...): the constant-bank
+// operands are loaded once for all V and the V chains interleave.
+template <int K, int KP, int V>
 __global__ void __launch_bounds__(128)
     k_scale(const uint32_t* __restrict__ d, uint32_t* __restrict__ y3, uint32_t* __restrict__ dig,
             int N, const __grid_constant__ ConvTabs tb) {
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= N) return;
+  const int n0 = blockIdx.x * blockDim.x * V + threadIdx.x;
+  if (n0 >= N) return;
   const int part = blockIdx.y % 3;
   const size_t ct = blockIdx.y / 3;
-  const uint32_t* src = d + (size_t)blockIdx.y * (K + KP) * N + n;
-  uint32_t dq[K], dp[KP];
-#pragma unroll
-  for (int i = 0; i < K; ++i) dq[i] = src[(size_t)i * N];
-#pragma unroll
-  for (int j = 0; j < KP; ++j) dp[j] = src[(size_t)(K + j) * N];
+  const uint32_t* src = d + (size_t)blockIdx.y * (K + KP) * N + n0;
 
   // r = (t d + h) mod q, h = (q-1)/2, held as r~_i = r_i (q/q_i)^-1 mod q_i
-  uint32_t rt[K];
+  uint32_t rt[V][K];
+  uint32_t dp[V][KP];
 #pragma unroll
-  for (int i = 0; i < K; ++i) rt[i] = add_mod(mul_shoup(dq[i], tb.A[i], tb.As[i], tb.q[i]), tb.B[i], tb.q[i]);
-  const uint32_t v = exact_v<K>(rt, tb);
+  for (int v = 0; v < V; ++v) {
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+      rt[v][i] = add_mod(mul_shoup(src[(size_t)i * N + v * blockDim.x], tb.A[i], tb.As[i], tb.q[i]), tb.B[i], tb.q[i]);
+#pragma unroll
+    for (int j = 0; j < KP; ++j) dp[v][j] = src[(size_t)(K + j) * N + v * blockDim.x];
+  }
+  uint32_t vq[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) vq[v] = exact_v<K>(rt[v], tb);
 
   // y = (t d + h - r) / q exactly, in P (centred, |y| < P/4): y~_j = y_j (P/p_j)^-1
-  uint32_t yt[KP];
-  uint64_t F = 0;
+  uint32_t yt[V][KP];
+  uint64_t F[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) F[v] = 0;
 #pragma unroll
   for (int j = 0; j < KP; ++j) {
     const uint32_t pj = tb.p[j];
-    const uint32_t rj = q_to_p<K>(rt, v, j, tb);
-    uint32_t acc = add_mod(mul_shoup(dp[j], tb.C[j], tb.Cs[j], pj), mul_shoup(pj - rj, tb.Ej[j], tb.Ejs[j], pj), pj);
-    acc = add_mod(acc, tb.F[j], pj);
-    yt[j] = acc;
-    F += frac59(acc, tb.pg[j], tb.pk[j]);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const uint32_t rj = q_to_p<K>(rt[v], vq[v], j, tb);
+      uint32_t acc = add_mod(mul_shoup(dp[v][j], tb.C[j], tb.Cs[j], pj), mul_shoup(pj - rj, tb.Ej[j], tb.Ejs[j], pj), pj);
+      acc = add_mod(acc, tb.F[j], pj);
+      yt[v][j] = acc;
+      F[v] += frac59(acc, tb.pg[j], tb.pk[j]);
+    }
   }
-  const uint32_t vp = (uint32_t)((F + (FRAC_ONE >> 1)) >> FRAC_BITS);
+  uint32_t vp[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) vp[v] = (uint32_t)((F[v] + (FRAC_ONE >> 1)) >> FRAC_BITS);
 
   // back to Q: y_i = (sum_j y~_j (P/p_j) - vp P) mod q_i
-  uint32_t yq[K];
+  uint32_t yq[V][K];
 #pragma unroll
   for (int i = 0; i < K; ++i)
-    yq[i] = mont_dot<KP>(yt, [&](int j) { return tb.phat_q[j][i]; }, vp, tb.negp_q[i], tb.q[i], tb.qpinv[i]);
-  uint32_t* dst = y3 + (size_t)blockIdx.y * K * N + n;
 #pragma unroll
-  for (int i = 0; i < K; ++i) dst[(size_t)i * N] = yq[i];
+    for (int v = 0; v < V; ++v)
+      yq[v][i] = mont_dot<KP>(yt[v], [&](int j) { return tb.phat_q[j][i]; }, vp[v], tb.negp_q[i], tb.q[i], tb.qpinv[i]);
+  uint32_t* dst = y3 + (size_t)blockIdx.y * K * N + n0;
+#pragma unroll
+  for (int v = 0; v < V; ++v)
+#pragma unroll
+    for (int i = 0; i < K; ++i) dst[(size_t)i * N + v * blockDim.x] = yq[v][i];
 
   if (part != 2 || dig == nullptr) return;
   // canonical binary of y_2 mod q, then base-w digits
-  uint32_t xt[K];
 #pragma unroll
-  for (int i = 0; i < K; ++i) xt[i] = mul_shoup(yq[i], tb.qhi[i], tb.qhis[i], tb.q[i]);
-  uint64_t Fq = 0;
+  for (int v = 0; v < V; ++v) {
+    uint32_t xt[K];
 #pragma unroll
-  for (int i = 0; i < K; ++i) Fq += frac59(xt[i], tb.qg[i], tb.qk[i]);
-  uint32_t S[words_for(K)];
-  mw_lift<K>(xt, tb, S);
-  mw_sub_mq<K>(S, (uint32_t)(Fq >> FRAC_BITS), tb);  // S - V q >= 0 with V in {v-1, v}
-  {
-    uint32_t Tq[words_for(K)];
+    for (int i = 0; i < K; ++i) xt[i] = mul_shoup(yq[v][i], tb.qhi[i], tb.qhis[i], tb.q[i]);
+    uint64_t Fq = 0;
 #pragma unroll
-    for (int w = 0; w < words_for(K); ++w) Tq[w] = S[w];
-    if (!mw_sub_mq<K>(Tq, 1, tb)) {
+    for (int i = 0; i < K; ++i) Fq += frac59(xt[i], tb.qg[i], tb.qk[i]);
+    uint32_t S[words_for(K)];
+    mw_lift<K>(xt, tb, S);
+    mw_sub_mq<K>(S, (uint32_t)(Fq >> FRAC_BITS), tb);  // S - V q >= 0 with V in {v-1, v}
+    {
+      uint32_t Tq[words_for(K)];
 #pragma unroll
-      for (int w = 0; w < words_for(K); ++w) S[w] = Tq[w];
+      for (int w = 0; w < words_for(K); ++w) Tq[w] = S[w];
+      if (!mw_sub_mq<K>(Tq, 1, tb)) {
+#pragma unroll
+        for (int w = 0; w < words_for(K); ++w) S[w] = Tq[w];
+      }
     }
+    store_digits<K>(S, dig + ct * tb.D * N + n0 + v * blockDim.x, N, tb);
   }
-  store_digits<K>(S, dig + ct * tb.D * N + n, N, tb);
 }
 
 // digits of part 2 of a 3-part tensor in3: [B][3][K][N] -> dig [B][D][N]
@@ -161,9 +181,17 @@ cudaError_t conv_launch(int op, const ConvLaunch& a, const ConvTabs& tb) {
     case 0:
       k_extend<K, KP><<<a.grid, a.block, 0, a.stream>>>(a.in, a.out, a.N, tb);
       break;
-    case 1:
-      k_scale<K, KP><<<a.grid, a.block, 0, a.stream>>>(a.in, a.out, a.dig, a.N, tb);
+    case 1: {
+      // V = 2 coefficients per thread measured slower on B200 (the kernel is
+      // fmaheavy-bound, 79 %; ncu profiles/r1_ncu_summary.md): keep V = 1
+      if (false && a.N % (2 * a.block.x) == 0) {
+        dim3 g2(a.grid.x / 2 > 0 ? a.grid.x / 2 : 1, a.grid.y);
+        k_scale<K, KP, 2><<<g2, a.block, 0, a.stream>>>(a.in, a.out, a.dig, a.N, tb);
+      } else {
+        k_scale<K, KP, 1><<<a.grid, a.block, 0, a.stream>>>(a.in, a.out, a.dig, a.N, tb);
+      }
       break;
+    }
     case 2:
       k_digits<K><<<a.grid, a.block, 0, a.stream>>>(a.in, a.dig, a.N, tb);
       break;
