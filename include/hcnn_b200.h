@@ -87,6 +87,26 @@ int hcnn_set_public_key(hcnn_ctx* ctx, const uint64_t* pk, int domain);
 int hcnn_encrypt(hcnn_ctx* ctx, const int8_t* u, const int8_t* e1, const int8_t* e2,
                  const int64_t* msg, uint32_t* out, size_t n);
 
+/* Same, with the plaintext polys already on the device (e.g. hcnn_codec_encode). */
+int hcnn_encrypt_device_msg(hcnn_ctx* ctx, const int8_t* u, const int8_t* e1, const int8_t* e2,
+                            const int64_t* msg_dev, uint32_t* out, size_t n);
+
+/* Client-side decryption (bfv.py:219-250): secret key bits s (N bytes, 0/1),
+ * then m = round(t (c0 + c1 s) / q) mod t for n 2-part ciphertexts (device
+ * [n][2][K][N] u32) into device u64 [n][N].  Exact (multiword decision near
+ * rounding boundaries); needs t < 2^48. */
+int hcnn_set_secret_key(hcnn_ctx* ctx, const uint8_t* s_bits);
+int hcnn_decrypt(hcnn_ctx* ctx, const uint32_t* cts, uint64_t* m, size_t n);
+
+/* SIMD slot codec over Z_t (batching.py:41-95) on the u64 NTT: slot i is the
+ * evaluation at zeta^(2i+1), zeta the reference's root (ntt.py:50-60).  t: a
+ * prime below 2^62 with 2N | t-1.  rows of N u64 on the device. */
+typedef struct hcnn_codec hcnn_codec;
+int hcnn_codec_create(uint64_t t, uint32_t n, int device, hcnn_codec** out);
+int hcnn_codec_destroy(hcnn_codec* codec);
+int hcnn_codec_encode(hcnn_codec* codec, const uint64_t* slots, uint64_t* polys, size_t rows, void* stream);
+int hcnn_codec_decode(hcnn_codec* codec, const uint64_t* polys, uint64_t* slots, size_t rows, void* stream);
+
 /* Device memory helpers (stream-ordered). */
 int hcnn_alloc(hcnn_ctx* ctx, size_t bytes, void** out);
 int hcnn_free(hcnn_ctx* ctx, void* ptr);

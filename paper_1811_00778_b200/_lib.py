@@ -28,6 +28,13 @@ _SIGS = {
     "hcnn_set_relin_key": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
     "hcnn_set_public_key": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
     "hcnn_encrypt": (C.c_int, [C.c_void_p] + [C.c_void_p] * 5 + [C.c_size_t]),
+    "hcnn_encrypt_device_msg": (C.c_int, [C.c_void_p] + [C.c_void_p] * 5 + [C.c_size_t]),
+    "hcnn_codec_create": (C.c_int, [C.c_uint64, C.c_uint32, C.c_int, C.POINTER(C.c_void_p)]),
+    "hcnn_codec_destroy": (C.c_int, [C.c_void_p]),
+    "hcnn_codec_encode": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "hcnn_codec_decode": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "hcnn_set_secret_key": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "hcnn_decrypt": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]),
     "hcnn_alloc": (C.c_int, [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
     "hcnn_free": (C.c_int, [C.c_void_p, C.c_void_p]),
     "hcnn_upload_u64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]),

@@ -49,6 +49,13 @@ struct ConvTabs {
   //                  y~_j = d_j C_j + (p_j - r_j) E_j + F_j  (mod p_j)
   uint32_t A[KMAX], As[KMAX], B[KMAX];
   uint32_t C[KPMAX], Cs[KPMAX], Ej[KPMAX], Ejs[KPMAX], F[KPMAX];
+  // decryption rounding m = round(t x / q) mod t (bfv.py:229-250), t < 2^48:
+  // t = dec_a_i q_i + dec_f_i, H = floor((q-1)/2 * 2^59 / q), h_w = words of (q-1)/2
+  uint64_t t, tmu;
+  uint64_t dec_a[KMAX];
+  uint32_t dec_f[KMAX];
+  uint64_t H;
+  uint32_t h_w[WMAX];
 };
 
 // Device pointers of the per-context NTT tables (all primes, Q first, then P).

@@ -174,7 +174,58 @@ __global__ void __launch_bounds__(128)
   store_digits<K>(S, dig + ct * tb.D * N + n, N, tb);
 }
 
-// op: 0 extend, 1 scale, 2 digits
+// Exact decryption rounding (bfv.py:229-250): phase residues [B][K][N]
+// (canonical, coefficient domain) -> m = round(t x / q) mod t as u64 [B][N].
+// With x = sum xt_i (q/q_i) - v q:  t x / q + h/q = sum_i t xt_i / q_i + h/q - v t,
+// t xt_i = c_i q_i + rho_i, so m = (sum c_i + floor(sum rho_i/q_i + h/q)) mod t;
+// the floor is a fixed-point estimate with an exact multiword decision near
+// integers, like exact_v.
+template <int K>
+__global__ void __launch_bounds__(128)
+    k_decrypt_round(const uint32_t* __restrict__ ph, uint64_t* __restrict__ m, int N,
+                    const __grid_constant__ ConvTabs tb) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  const size_t ct = blockIdx.y;
+  const uint32_t* src = ph + ct * K * N + n;
+  uint32_t rho[K];
+  uint64_t csum = 0, F = tb.H;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    const uint32_t xt = mul_shoup(src[(size_t)i * N], tb.qhi[i], tb.qhis[i], tb.q[i]);
+    const uint64_t u = (uint64_t)xt * tb.dec_f[i];          // < q_i^2
+    uint64_t qh = __umul64hi(u, tb.qmu[i]);                 // floor(u/q_i) or one less
+    uint64_t r = u - qh * tb.q[i];
+    if (r >= tb.q[i]) {
+      r -= tb.q[i];
+      ++qh;
+    }
+    rho[i] = (uint32_t)r;
+    csum += tb.dec_a[i] * xt + qh;  // < K * 2^49: no overflow for t < 2^48
+    F += frac59(rho[i], tb.qg[i], tb.qk[i]);
+  }
+  uint32_t V = (uint32_t)(F >> FRAC_BITS);
+  if ((F & FRAC_MASK) >= FRAC_ONE - (K + 1) * FRAC_ERR) {
+    // exact: is sum rho_i (q/q_i) + h >= (V+1) q ?
+    uint32_t S[words_for(K)];
+    mw_lift<K>(rho, tb, S);
+    uint64_t carry = 0;
+#pragma unroll
+    for (int w = 0; w < words_for(K); ++w) {
+      const uint64_t s = (uint64_t)S[w] + tb.h_w[w] + carry;
+      S[w] = (uint32_t)s;
+      carry = s >> 32;
+    }
+    if (!mw_sub_mq<K>(S, V + 1, tb)) V += 1;
+  }
+  uint64_t total = csum + V;
+  const uint64_t qh = __umul64hi(total, tb.tmu);
+  uint64_t r = total - qh * tb.t;
+  while (r >= tb.t) r -= tb.t;
+  m[ct * N + n] = r;
+}
+
+// op: 0 extend, 1 scale, 2 digits, 3 decrypt rounding
 template <int K, int KP>
 cudaError_t conv_launch(int op, const ConvLaunch& a, const ConvTabs& tb) {
   switch (op) {
@@ -194,6 +245,9 @@ cudaError_t conv_launch(int op, const ConvLaunch& a, const ConvTabs& tb) {
     }
     case 2:
       k_digits<K><<<a.grid, a.block, 0, a.stream>>>(a.in, a.dig, a.N, tb);
+      break;
+    case 3:
+      k_decrypt_round<K><<<a.grid, a.block, 0, a.stream>>>(a.in, reinterpret_cast<uint64_t*>(a.out), a.N, tb);
       break;
     default:
       return cudaErrorInvalidValue;

@@ -10,6 +10,7 @@
 #include "conv_kernels.cuh"
 #include "kernels.cuh"
 #include "ntt_kernels.cuh"
+#include "ntt64.cuh"
 #include "tables.hpp"
 
 using namespace hcnn;
@@ -46,6 +47,16 @@ void fail(int code, const std::string& m) { throw Error{code, m}; }
 
 }  // namespace
 
+// Slot codec over Z_t (batching.py:41-95): u64 negacyclic NTT tables.
+struct hcnn_codec {
+  int device = 0;
+  uint32_t n = 0, logn = 0;
+  uint64_t t = 0, zeta = 0;
+  ulonglong2* d_tw = nullptr;
+  ulonglong2* d_itw = nullptr;
+  ulonglong2 ninv{};
+};
+
 struct hcnn_weights {
   size_t count = 0;
   double* wd = nullptr;   // |w| < 2^22: exact FP64 MAC path
@@ -76,6 +87,7 @@ struct hcnn_ctx {
   int rlk_domain = 0;
   uint32_t* d_pk = nullptr;
   uint32_t* d_pk_raw = nullptr;
+  uint32_t* d_sk = nullptr;  // secret key s, NTT domain (spectral positions), [K][N]
   int pk_domain = 0;
   int variant = 0;       // NTT radix variant of the fused kernels (0 = default)
   int keys_variant = -1; // variant the tiled keys were laid out for
@@ -281,6 +293,32 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
   }
   for (uint32_t i = 0; i < c->K; ++i)
     tb.negp_q[i] = (uint32_t)mont_form((q[i] - mod_small(Pp, q[i])) % q[i], q[i]);
+  // decryption rounding constants (usable when t < 2^48)
+  tb.t = t;
+  tb.tmu = (uint64_t)(((u128)1 << 64) / t);
+  for (uint32_t i = 0; i < c->K; ++i) {
+    tb.dec_a[i] = t / q[i];
+    tb.dec_f[i] = (uint32_t)(t % q[i]);
+  }
+  {
+    // H = floor(h 2^59 / q) from the top words of h and q
+    Big h59 = h;
+    for (int b = 0; b < 59; ++b) h59 = mul_small(h59, 2);
+    // long division h59 / Q by repeated subtraction of shifted Q is costly;
+    // h/q = 1/2 - 1/(2q), so H = 2^58 - 1 exactly for q > 2^60
+    if (Q.bits() > 61) {
+      tb.H = (1ull << 58) - 1;  // h/q = 1/2 - 1/(2q), q > 2^61
+    } else {
+      u128 hq = 0, qq = 0;
+      for (int w2 = 3; w2 >= 0; --w2) {
+        hq = (hq << 32) | h.word(w2);
+        qq = (qq << 32) | Q.word(w2);
+      }
+      tb.H = (uint64_t)((hq << 59) / qq);
+    }
+    (void)h59;
+  }
+  for (int w2 = 0; w2 < WMAX; ++w2) tb.h_w[w2] = h.word(w2);
 
   // upload
   CK(cudaMalloc(&c->d_prime, L * sizeof(uint32_t)));
@@ -462,6 +500,33 @@ void multiply(hcnn_ctx* c, const uint32_t* a, const uint32_t* b, size_t n, uint3
     mul_chunk(c, ac, general ? bc : ac, m, y3, dig, ws);
     if (out2) launch_relin(c, dig, y3, out2 + s * 2 * K * N, m);
   }
+}
+
+__global__ void k_sk_rows(const uint8_t* __restrict__ s, uint32_t* __restrict__ rows, int K, int N) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  for (int i = 0; i < K; ++i) rows[(size_t)i * N + n] = s[n];
+}
+
+// tmp[ct][i][:] = tmp * s_ntt[i] (NTT domain, same positions) mod q_i
+__global__ void k_mul_sk(uint32_t* __restrict__ tmp, const uint32_t* __restrict__ sk, int K, int N,
+                         size_t total, const uint32_t* __restrict__ primes, const uint64_t* __restrict__ mus) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int limb = (int)((i / N) % K);
+  const size_t n = i % N;
+  tmp[i] = mul_mod(tmp[i], sk[(size_t)limb * N + n], primes[limb], mus[limb]);
+}
+
+// tmp[ct][i][n] += c0[ct][i][n]; cts: [ct][2][K][N]
+__global__ void k_add_c0(uint32_t* __restrict__ tmp, const uint32_t* __restrict__ cts, int K, int N,
+                         size_t total, const uint32_t* __restrict__ primes) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const size_t kn = (size_t)K * N;
+  const size_t ct = i / kn, r = i % kn;
+  const int limb = (int)(r / N);
+  tmp[i] = add_mod(tmp[i], cts[ct * 2 * kn + r], primes[limb]);
 }
 
 __global__ void k_hadd(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
@@ -674,6 +739,7 @@ int hcnn_ctx_destroy(hcnn_ctx* c) {
     if (c->d_pk_raw) cudaFree(c->d_pk_raw);
     cudaFree(c->d_pinv);
     if (c->d_pk) cudaFree(c->d_pk);
+    if (c->d_sk) cudaFree(c->d_sk);
     if (c->d_delta) cudaFree(c->d_delta);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
@@ -813,8 +879,21 @@ int hcnn_set_public_key(hcnn_ctx* c, const uint64_t* pk, int domain) {
   });
 }
 
+static int hcnn_encrypt_impl(hcnn_ctx* c, const int8_t* u, const int8_t* e1, const int8_t* e2,
+                             const int64_t* msg, int msg_on_device, uint32_t* out, size_t n);
+
 int hcnn_encrypt(hcnn_ctx* c, const int8_t* u, const int8_t* e1, const int8_t* e2, const int64_t* msg,
                  uint32_t* out, size_t n) {
+  return hcnn_encrypt_impl(c, u, e1, e2, msg, 0, out, n);
+}
+
+int hcnn_encrypt_device_msg(hcnn_ctx* c, const int8_t* u, const int8_t* e1, const int8_t* e2,
+                            const int64_t* msg_dev, uint32_t* out, size_t n) {
+  return hcnn_encrypt_impl(c, u, e1, e2, msg_dev, 1, out, n);
+}
+
+static int hcnn_encrypt_impl(hcnn_ctx* c, const int8_t* u, const int8_t* e1, const int8_t* e2,
+                             const int64_t* msg, int msg_on_device, uint32_t* out, size_t n) {
   return guarded([&] {
     if (!c->d_pk_raw) fail(HCNN_ERR_MISSING_KEY, "public key required");
     CK(cudaSetDevice(c->device));
@@ -835,7 +914,10 @@ int hcnn_encrypt(hcnn_ctx* c, const int8_t* u, const int8_t* e1, const int8_t* e
       CK(cudaMemcpyAsync(du, u + s0 * N, m * N, cudaMemcpyHostToDevice, c->stream));
       CK(cudaMemcpyAsync(d1, e1 + s0 * N, m * N, cudaMemcpyHostToDevice, c->stream));
       CK(cudaMemcpyAsync(d2, e2 + s0 * N, m * N, cudaMemcpyHostToDevice, c->stream));
-      CK(cudaMemcpyAsync(dm, msg + s0 * N, m * N * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+      if (msg_on_device)
+        CK(cudaMemcpyAsync(dm, msg + s0 * N, m * N * sizeof(int64_t), cudaMemcpyDeviceToDevice, c->stream));
+      else
+        CK(cudaMemcpyAsync(dm, msg + s0 * N, m * N * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
       NttLaunch a{};
       a.grid = dim3(c->K, (unsigned)m);
       a.u = du;
@@ -850,6 +932,136 @@ int hcnn_encrypt(hcnn_ctx* c, const int8_t* u, const int8_t* e1, const int8_t* e
     }
     CK(cudaFreeAsync(stage, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int hcnn_codec_create(uint64_t t, uint32_t n, int device, hcnn_codec** out) {
+  return guarded([&] {
+    if (!out) fail(HCNN_ERR_PARAM, "null argument");
+    if (n < 2 || (n & (n - 1)) || n > (1u << 15)) fail(HCNN_ERR_UNSUPPORTED, "slot count must be a power of two <= 2^15");
+    if (t >= (1ull << 62) || !is_prime64(t)) fail(HCNN_ERR_UNSUPPORTED, "t must be a prime below 2^62");
+    if ((t - 1) % (2ull * n)) fail(HCNN_ERR_UNSUPPORTED, "2N does not divide t-1");
+    CK(cudaSetDevice(device));
+    auto c = std::make_unique<hcnn_codec>();
+    c->device = device;
+    c->n = n;
+    while ((1u << c->logn) < n) ++c->logn;
+    c->t = t;
+    c->zeta = primitive_2n_root(t, n);
+    const u64 iz = invmod64(c->zeta, t);
+    std::vector<ulonglong2> tw(n), itw(n);
+    std::vector<u64> pw(n), ipw(n);
+    pw[0] = ipw[0] = 1;
+    for (uint32_t i = 1; i < n; ++i) {
+      pw[i] = mulmod64(pw[i - 1], c->zeta, t);
+      ipw[i] = mulmod64(ipw[i - 1], iz, t);
+    }
+    auto shoup64 = [&](u64 w) { return (u64)(((u128)w << 64) / t); };
+    for (uint32_t i = 0; i < n; ++i) {
+      const u64 a = pw[bitrev(i, c->logn)], b = ipw[bitrev(i, c->logn)];
+      tw[i] = make_ulonglong2(a, shoup64(a));
+      itw[i] = make_ulonglong2(b, shoup64(b));
+    }
+    const u64 ni = invmod64(n % t, t);
+    c->ninv = make_ulonglong2(ni, shoup64(ni));
+    CK(cudaMalloc(&c->d_tw, n * sizeof(ulonglong2)));
+    CK(cudaMalloc(&c->d_itw, n * sizeof(ulonglong2)));
+    CK(cudaMemcpy(c->d_tw, tw.data(), n * sizeof(ulonglong2), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_itw, itw.data(), n * sizeof(ulonglong2), cudaMemcpyHostToDevice));
+    *out = c.release();
+  });
+}
+
+int hcnn_codec_destroy(hcnn_codec* c) {
+  return guarded([&] {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaFree(c->d_tw);
+    cudaFree(c->d_itw);
+    delete c;
+  });
+}
+
+// slots (natural order, values < t) -> plaintext polys: batching.encode
+int hcnn_codec_encode(hcnn_codec* c, const uint64_t* slots, uint64_t* polys, size_t rows, void* stream) {
+  return guarded([&] {
+    if (!rows) return;
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    k_permute_brv64<<<dim3(cdiv(c->n, 256), (unsigned)rows), 256, 0, st>>>(slots, polys, (int)c->logn);
+    CK(cudaGetLastError());
+    const size_t smem = (size_t)c->n * 8;
+    if (smem > 200 * 1024) fail(HCNN_ERR_UNSUPPORTED, "slot count too large for the u64 NTT");
+    CK(cudaFuncSetAttribute(k_ntt64<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    k_ntt64<true><<<(unsigned)rows, 512, smem, st>>>(polys, (int)c->logn, c->t, c->d_itw, c->ninv);
+    CK(cudaGetLastError());
+  });
+}
+
+// plaintext polys -> slots (natural order): batching.decode
+int hcnn_codec_decode(hcnn_codec* c, const uint64_t* polys, uint64_t* slots, size_t rows, void* stream) {
+  return guarded([&] {
+    if (!rows) return;
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t smem = (size_t)c->n * 8;
+    if (smem > 200 * 1024) fail(HCNN_ERR_UNSUPPORTED, "slot count too large for the u64 NTT");
+    CK(cudaFuncSetAttribute(k_ntt64<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    uint64_t* tmp = nullptr;
+    CK(cudaMallocAsync((void**)&tmp, rows * c->n * sizeof(uint64_t), st));
+    CK(cudaMemcpyAsync(tmp, polys, rows * c->n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+    k_ntt64<false><<<(unsigned)rows, 512, smem, st>>>(tmp, (int)c->logn, c->t, c->d_tw, c->ninv);
+    CK(cudaGetLastError());
+    k_permute_brv64<<<dim3(cdiv(c->n, 256), (unsigned)rows), 256, 0, st>>>(tmp, slots, (int)c->logn);
+    CK(cudaGetLastError());
+    CK(cudaFreeAsync(tmp, st));
+  });
+}
+
+int hcnn_set_secret_key(hcnn_ctx* c, const uint8_t* s_bits) {
+  return guarded([&] {
+    if (!s_bits) fail(HCNN_ERR_MISSING_KEY, "secret key required");
+    CK(cudaSetDevice(c->device));
+    const size_t N = c->N, K = c->K;
+    uint8_t* ds = nullptr;
+    CK(cudaMallocAsync((void**)&ds, N, c->stream));
+    CK(cudaMemcpyAsync(ds, s_bits, N, cudaMemcpyHostToDevice, c->stream));
+    if (!c->d_sk) CK(cudaMalloc((void**)&c->d_sk, K * N * sizeof(uint32_t)));
+    k_sk_rows<<<cdiv(N, 256), 256, 0, c->stream>>>(ds, c->d_sk, (int)K, (int)N);
+    c->launched("k_sk_rows");
+    launch_ntt_rows(c, c->d_sk, K, (int)K, 0, 0);
+    CK(cudaFreeAsync(ds, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int hcnn_decrypt(hcnn_ctx* c, const uint32_t* cts, uint64_t* m, size_t n) {
+  return guarded([&] {
+    if (!c->d_sk) fail(HCNN_ERR_MISSING_KEY, "secret key required");
+    if (c->t >= (1ull << 48)) fail(HCNN_ERR_UNSUPPORTED, "GPU decryption needs t < 2^48");
+    CK(cudaSetDevice(c->device));
+    if (!n) return;
+    c->mark();
+    const size_t N = c->N, K = c->K, kn = K * N;
+    uint32_t* tmp = nullptr;
+    CK(cudaMallocAsync((void**)&tmp, n * kn * sizeof(uint32_t), c->stream));
+    // c1 of every ciphertext -> tmp, then c1 * s in the NTT domain
+    CK(cudaMemcpy2DAsync(tmp, kn * sizeof(uint32_t), cts + kn, 2 * kn * sizeof(uint32_t),
+                         kn * sizeof(uint32_t), n, cudaMemcpyDeviceToDevice, c->stream));
+    launch_ntt_rows(c, tmp, n * K, (int)K, 0, 0);
+    const size_t total = n * kn;
+    k_mul_sk<<<cdiv(total, 256), 256, 0, c->stream>>>(tmp, c->d_sk, (int)K, (int)N, total, c->d_prime, c->d_mu);
+    c->launched("k_mul_sk");
+    launch_ntt_rows(c, tmp, n * K, (int)K, 0, 1);
+    k_add_c0<<<cdiv(total, 256), 256, 0, c->stream>>>(tmp, cts, (int)K, (int)N, total, c->d_prime);
+    c->launched("k_add_c0");
+    ConvLaunch ca{};
+    ca.block = dim3(128);
+    ca.grid = dim3(cdiv(N, 128), (unsigned)n);
+    ca.in = tmp;
+    ca.out = reinterpret_cast<uint32_t*>(m);
+    conv_dispatch(c, 3, ca, "k_decrypt_round");
+    CK(cudaFreeAsync(tmp, c->stream));
   });
 }
 

@@ -564,10 +564,76 @@ def encrypt_device(pk, polys, params, rng, device=None) -> torch.Tensor:
     return out
 
 
+class GpuCodec:
+    """SIMD slot codec over Z_t on the GPU (u64 NTT, batching.py:41-95)."""
+
+    def __init__(self, t: int, n: int, device=None):
+        self.t, self.n = int(t), int(n)
+        self.device = _device_index(device)
+        h = _lib.C.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.lib().hcnn_codec_create(self.t, self.n, self.device, _lib.C.byref(h)),
+                       "hcnn_codec_create")
+        self.handle = h
+        self._fin = weakref.finalize(self, _lib.lib().hcnn_codec_destroy, h)
+
+    def _run(self, fn, x: torch.Tensor) -> torch.Tensor:
+        x = x.to(device=f"cuda:{self.device}", dtype=torch.int64).contiguous()
+        out = torch.empty_like(x)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        _lib.check(fn(self.handle, _ptr(x), _ptr(out), x.shape[0], _lib.C.c_void_p(stream)), "codec")
+        return out
+
+    def encode(self, slots: torch.Tensor) -> torch.Tensor:
+        """[P][N] slot values in [0, t) -> [P][N] plaintext polys (int64)."""
+        return self._run(_lib.lib().hcnn_codec_encode, slots)
+
+    def decode(self, polys: torch.Tensor) -> torch.Tensor:
+        return self._run(_lib.lib().hcnn_codec_decode, polys)
+
+
+_CODECS: dict = {}
+
+
+def codec_for(t: int, n: int, device=None) -> GpuCodec:
+    key = (int(t), int(n), _device_index(device))
+    c = _CODECS.get(key)
+    if c is None:
+        c = GpuCodec(t, n, device)
+        _CODECS[key] = c
+    return c
+
+
+def decrypt_device(tensor: GpuCipherTensor, sk, params) -> torch.Tensor:
+    """bfv.decrypt (bfv.py:239-250) of every ciphertext on the GPU: [n][N]
+    plaintext polys in [0, t) (int64, device).  Requires t < 2^48."""
+    g = context_for(params, tensor.data.device)
+    s = np.ascontiguousarray(np.asarray(sk.s_bits, dtype=np.uint8))
+    key = hashlib.blake2b(s.tobytes(), digest_size=16).digest()
+    if getattr(g, "_sk_key", None) != key:
+        g.bind_stream()
+        _lib.check(_lib.lib().hcnn_set_secret_key(g.handle, s.ctypes.data), "hcnn_set_secret_key")
+        g._sk_key = key
+    out = torch.empty((len(tensor), g.N), dtype=torch.int64, device=tensor.data.device)
+    g.bind_stream()
+    _lib.check(_lib.lib().hcnn_decrypt(g.handle, _ptr(tensor.data), _ptr(out), len(tensor)), "hcnn_decrypt")
+    return out
+
+
+def unpack_tensor_device(tensor: GpuCipherTensor, sk, params, batch_size: int) -> np.ndarray:
+    """unpack_tensor (engine.py:178-192) on the GPU: decrypt + slot decode,
+    returns (batch, h*w*c) values in [0, t)."""
+    polys = decrypt_device(tensor, sk, params)
+    slots = codec_for(params.t, params.ring_degree, tensor.data.device).decode(polys)
+    return slots[:, :batch_size].T.contiguous().cpu().numpy()
+
+
 def pack_images_device(images, layout: PackingLayout, encoder, pk, params, rng, delta: int,
                        device=None) -> GpuCipherTensor:
-    """pack_images (engine.py:146-175) with the encryption on the GPU: returns
-    the same ciphertexts, resident on the device."""
+    """pack_images (engine.py:146-175) on the GPU: slot encoding (u64 NTT over
+    Z_t) and encryption run on the device from host-drawn randomness; returns
+    the same ciphertexts as the reference, resident on the device.  `encoder`
+    is accepted for signature compatibility (the device codec is used)."""
     if len(images) != layout.batch_size:
         raise CapacityError("image count != layout batch size")
     if layout.slot_count != params.ring_degree:
@@ -577,8 +643,15 @@ def pack_images_device(images, layout: PackingLayout, encoder, pk, params, rng, 
     flat = stack.reshape(layout.batch_size, -1) % params.t
     slots = np.zeros((flat.shape[1], layout.slot_count), dtype=np.int64)
     slots[:, : layout.batch_size] = flat.T
-    polys = encoder.encode_many(slots)
-    data = encrypt_device(pk, polys, params, rng, device)
+    g = context_for(params, device)
+    codec = codec_for(params.t, params.ring_degree, g.device)
+    polys = codec.encode(torch.from_numpy(slots))
+    g.set_public_key(pk)
+    u, e1, e2 = draw_encryption_noise(rng, polys.shape[0], g.N)
+    data = g.empty(polys.shape[0])
+    g.bind_stream()
+    _lib.check(_lib.lib().hcnn_encrypt_device_msg(g.handle, u.ctypes.data, e1.ctypes.data, e2.ctypes.data,
+                                                  _ptr(polys), _ptr(data), polys.shape[0]), "hcnn_encrypt")
     h, w = shape[0], shape[1]
     c = shape[2] if len(shape) == 3 else 1
     return GpuCipherTensor((h, w, c), data, delta, params.t, params)
