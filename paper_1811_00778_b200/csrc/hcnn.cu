@@ -793,10 +793,14 @@ int hcnn_ctx_set_stream(hcnn_ctx* c, void* stream) {
 int hcnn_ctx_set_option(hcnn_ctx* c, int key, int64_t value) {
   return guarded([&] {
     if (key == HCNN_OPT_NTT_VARIANT) {
-      if (value != 0 && value != 3 && value != 4 && value != 5) fail(HCNN_ERR_PARAM, "NTT variant must be 0, 3, 4 or 5");
-      if (value && c->logN < 10) fail(HCNN_ERR_UNSUPPORTED, "NTT variants need N >= 1024");
-      if (value == 3 && c->logN > 13) fail(HCNN_ERR_UNSUPPORTED, "NTT variant 3 needs N <= 8192");
-      if (value && c->logN > (uint32_t)value + 10) fail(HCNN_ERR_UNSUPPORTED, "NTT variant needs more than 1024 threads");
+      // low 4 bits: log2 E of the fused kernels (0 = default); +16: one-row
+      // relinearisation transforms (ntt_kernels.cuh RELIN_SINGLE)
+      const int64_t loge = value & 15;
+      if ((value & ~(int64_t)31) || (loge != 0 && loge != 3 && loge != 4 && loge != 5))
+        fail(HCNN_ERR_PARAM, "NTT variant must be 0, 3, 4 or 5 (+16 for one-row relinearisation)");
+      if (loge && c->logN < 10) fail(HCNN_ERR_UNSUPPORTED, "NTT variants need N >= 1024");
+      if (loge == 3 && c->logN > 13) fail(HCNN_ERR_UNSUPPORTED, "NTT variant 3 needs N <= 8192");
+      if (loge && c->logN > (uint32_t)loge + 10) fail(HCNN_ERR_UNSUPPORTED, "NTT variant needs more than 1024 threads");
       c->variant = (int)value;
     } else {
       fail(HCNN_ERR_PARAM, "unknown option");

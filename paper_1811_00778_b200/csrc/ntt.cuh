@@ -1,4 +1,4 @@
-// CTA-level negacyclic NTT over one RNS limb (u32 residues, p < 2^30).
+// CTA-level negacyclic NTT over RNS limbs (u32 residues, p < 2^30).
 //
 // What it computes.  The reference transforms with a psi-twist followed by a
 // bit-reverse + radix-2 Cooley-Tukey pass and keeps natural order
@@ -12,16 +12,18 @@
 // coefficient domain are bit-identical to the reference's; reference-order
 // NTT-domain keys are permuted once at upload.
 //
-// How.  One CTA owns one row of N residues: T = N/E threads each keep E = 2^LOGE
-// residues in registers.  The top LOGN - REM butterfly bits are done in
-// radix-E passes (LOGE stages in registers, then an exchange through padded
-// shared memory); the REM = LOGN mod LOGE lowest bits are done with warp
-// shuffles (the partner element lives in lane ^ 2^b), so there is no radix-2
-// shared-memory tail.  Butterflies are Harvey's lazy ones: forward values in
-// [0, 4p), inverse values in [0, 2p).  Twiddles are Shoup pairs
-// (w, floor(w 2^32/p)) indexed like SEAL's psi^brv table; each thread loads
-// the 2^ss twiddles of stage ss as one contiguous vector (15 per radix-16 pass
-// in 8 loads instead of 32).
+// How.  One CTA transforms NR rows of N residues of the same prime in lockstep
+// (NR = 1 or 2: the rows share every twiddle load, barrier and exchange).  T =
+// N/E threads each keep E = 2^LOGE residues of every row in registers.  The
+// top LOGN - REM butterfly bits are done in radix-E passes (LOGE stages in
+// registers, then an exchange through padded shared memory, alternating
+// between two buffers so that each exchange needs one barrier); the REM =
+// LOGN mod LOGE lowest bits are done with warp shuffles (radix-16 geometry) or
+// in registers after one more exchange (radix-32 geometry).  Butterflies are
+// Harvey's lazy ones: forward values in [0, 4p), inverse values in [0, 2p).
+// Twiddles are Shoup pairs (w, floor(w 2^32/p)) indexed like SEAL's psi^brv
+// table; each thread loads the 2^ss twiddles of stage ss as one contiguous
+// vector (15 per radix-16 pass in 8 loads).
 #pragma once
 #include "modarith.cuh"
 
@@ -31,9 +33,6 @@ __host__ __device__ constexpr int pick_loge(int logn) {
   return logn >= 15 ? 5 : logn >= 9 ? 4 : logn >= 6 ? logn - 5 : 1;
 }
 
-// SHFL_TAIL: the REM = LOGN mod LOGE lowest butterfly bits are done with warp
-// shuffles (radix-16 geometry) or in registers after one more exchange
-// (E/2^REM independent groups per thread; radix-32 geometry).
 template <int LOGN_, int LOGE_ = pick_loge(LOGN_), bool SHFL_TAIL_ = (LOGE_ <= 4)>
 struct NttGeom {
   static constexpr int LOGN = LOGN_;
@@ -47,11 +46,16 @@ struct NttGeom {
   static constexpr bool SHFL_TAIL = SHFL_TAIL_ && REM > 0;
   static constexpr bool REG_TAIL = !SHFL_TAIL_ && REM > 0;
   static_assert(!SHFL_TAIL || T >= 32, "shuffle stages need full warps");
-  // shared-memory words for one padded row; the NTT alternates between two
-  // such buffers (one barrier per exchange)
+  // shared-memory words for one padded row; an NR-row NTT uses
+  // ntt_smem_words(NR) (two alternating buffers of NR rows)
   static constexpr int SMEM_WORDS = N + 2 * (N >> 5) + 2;
   static constexpr int XW = (SMEM_WORDS + 3) & ~3;
-  static constexpr int NTT_SMEM_WORDS = 2 * XW;
+  // two alternating exchange buffers (one barrier per exchange) when they fit
+  // in LIMIT_WORDS, else one buffer and two barriers per exchange
+  static constexpr int LIMIT_WORDS = 200 * 1024 / 4;
+  __host__ __device__ static constexpr bool dbl(int nr) { return 2 * nr * XW <= LIMIT_WORDS; }
+  __host__ __device__ static constexpr int ntt_smem_words(int nr) { return (dbl(nr) ? 2 : 1) * nr * XW; }
+  __host__ __device__ static constexpr bool fits(int nr) { return ntt_smem_words(nr) <= 227 * 1024 / 4; }
   static constexpr int FWD_EXCHANGES = NFULL - 1 + (REG_TAIL ? 1 : 0);
   // pass P covers butterfly bits [lo(P), lo(P) + LOGE), from the top
   __host__ __device__ static constexpr int lo(int P) { return LOGN - (P + 1) * LOGE; }
@@ -92,8 +96,22 @@ DI void load_tw(uint2* w, const uint2* __restrict__ tw, int base) {
   }
 }
 
+DI void bfly_fwd(uint32_t& a, uint32_t& b, uint2 w, uint32_t p, uint32_t p2) {
+  uint32_t X = umin32(a, a - p2);
+  const uint32_t Tt = mul_shoup_lazy(b, w.x, w.y, p);
+  a = X + Tt;
+  b = X - Tt + p2;
+}
+
+DI void bfly_inv(uint32_t& a, uint32_t& b, uint2 w, uint32_t p, uint32_t p2) {
+  const uint32_t X = a, Y = b;
+  const uint32_t U = X + Y;
+  a = umin32(U, U - p2);
+  b = mul_shoup_lazy(X - Y + p2, w.x, w.y, p);
+}
+
 // forward (CT) stage SS of a radix-E pass at bits [LO, LO+LOGE); values in [0, 4p)
-template <class G, int LO, int SS>
+template <class G, int LO, int SS, int NR>
 DI void fwd_stage(uint32_t* x, const uint2* __restrict__ tw, uint32_t p, int tid) {
   constexpr int KB = G::LOGE;
   if constexpr (SS < KB) {
@@ -107,25 +125,16 @@ DI void fwd_stage(uint32_t* x, const uint2* __restrict__ tw, uint32_t p, int tid
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       if (e & half) continue;
-      const uint2 ww = w[e >> (KB - SS)];
-      uint32_t X = x[e];
-      X = umin32(X, X - p2);
-      const uint32_t Tt = mul_shoup_lazy(x[e | half], ww.x, ww.y, p);
-      x[e] = X + Tt;
-      x[e | half] = X - Tt + p2;
+#pragma unroll
+      for (int r = 0; r < NR; ++r) bfly_fwd(x[r * E + e], x[r * E + (e | half)], w[e >> (KB - SS)], p, p2);
     }
-    fwd_stage<G, LO, SS + 1>(x, tw, p, tid);
+    fwd_stage<G, LO, SS + 1, NR>(x, tw, p, tid);
   }
-}
-
-template <class G, int LO>
-DI void fwd_pass(uint32_t* x, const uint2* __restrict__ tw, uint32_t p, int tid) {
-  fwd_stage<G, LO, 0>(x, tw, p, tid);
 }
 
 // inverse (GS) stage SS of a radix-E pass (SS descending = bits ascending);
 // values in [0, 2p)
-template <class G, int LO, int SS>
+template <class G, int LO, int SS, int NR>
 DI void inv_stage(uint32_t* x, const uint2* __restrict__ itw, uint32_t p, int tid) {
   constexpr int KB = G::LOGE;
   if constexpr (SS >= 0) {
@@ -139,23 +148,15 @@ DI void inv_stage(uint32_t* x, const uint2* __restrict__ itw, uint32_t p, int ti
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       if (e & half) continue;
-      const uint2 ww = w[e >> (KB - SS)];
-      const uint32_t X = x[e], Y = x[e | half];
-      const uint32_t U = X + Y;
-      x[e] = umin32(U, U - p2);
-      x[e | half] = mul_shoup_lazy(X - Y + p2, ww.x, ww.y, p);
+#pragma unroll
+      for (int r = 0; r < NR; ++r) bfly_inv(x[r * E + e], x[r * E + (e | half)], w[e >> (KB - SS)], p, p2);
     }
-    inv_stage<G, LO, SS - 1>(x, itw, p, tid);
+    inv_stage<G, LO, SS - 1, NR>(x, itw, p, tid);
   }
 }
 
-template <class G, int LO>
-DI void inv_pass(uint32_t* x, const uint2* __restrict__ itw, uint32_t p, int tid) {
-  inv_stage<G, LO, G::LOGE - 1>(x, itw, p, tid);
-}
-
 // register tail, forward stage SS (bits REM-1-SS), all E/2^REM groups
-template <class G, int SS>
+template <class G, int SS, int NR>
 DI void fwd_tail(uint32_t* x, const uint2* __restrict__ tw, uint32_t p, int tid) {
   if constexpr (SS < G::REM) {
     constexpr int R = G::REM;
@@ -171,19 +172,15 @@ DI void fwd_tail(uint32_t* x, const uint2* __restrict__ tw, uint32_t p, int tid)
       for (int el = 0; el < (1 << R); ++el) {
         if (el & half) continue;
         const int e = (grp << R) | el;
-        const uint2 ww = w[el >> (R - SS)];
-        uint32_t X = x[e];
-        X = umin32(X, X - p2);
-        const uint32_t Tt = mul_shoup_lazy(x[e | half], ww.x, ww.y, p);
-        x[e] = X + Tt;
-        x[e | half] = X - Tt + p2;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) bfly_fwd(x[r * G::E + e], x[r * G::E + (e | half)], w[el >> (R - SS)], p, p2);
       }
     }
-    fwd_tail<G, SS + 1>(x, tw, p, tid);
+    fwd_tail<G, SS + 1, NR>(x, tw, p, tid);
   }
 }
 
-template <class G, int SS>
+template <class G, int SS, int NR>
 DI void inv_tail(uint32_t* x, const uint2* __restrict__ itw, uint32_t p, int tid) {
   if constexpr (SS >= 0) {
     constexpr int R = G::REM;
@@ -199,14 +196,11 @@ DI void inv_tail(uint32_t* x, const uint2* __restrict__ itw, uint32_t p, int tid
       for (int el = 0; el < (1 << R); ++el) {
         if (el & half) continue;
         const int e = (grp << R) | el;
-        const uint2 ww = w[el >> (R - SS)];
-        const uint32_t X = x[e], Y = x[e | half];
-        const uint32_t U = X + Y;
-        x[e] = umin32(U, U - p2);
-        x[e | half] = mul_shoup_lazy(X - Y + p2, ww.x, ww.y, p);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) bfly_inv(x[r * G::E + e], x[r * G::E + (e | half)], w[el >> (R - SS)], p, p2);
       }
     }
-    inv_tail<G, SS - 1>(x, itw, p, tid);
+    inv_tail<G, SS - 1, NR>(x, itw, p, tid);
   }
 }
 
@@ -230,7 +224,7 @@ DI void load_shfl_tw(uint2* w, const uint2* __restrict__ tw, int tid) {
 }
 
 // forward butterflies on the REM lowest bits through warp shuffles
-template <class G, int B>
+template <class G, int B, int NR>
 DI void fwd_shfl(uint32_t* x, const uint2* __restrict__ tw, uint32_t p, int tid) {
   if constexpr (B >= 0) {
     const uint32_t p2 = 2 * p;
@@ -239,19 +233,22 @@ DI void fwd_shfl(uint32_t* x, const uint2* __restrict__ tw, uint32_t p, int tid)
     load_shfl_tw<G, B>(w, tw, tid);
 #pragma unroll
     for (int e = 0; e < G::E; ++e) {
-      const uint32_t v = x[e];
-      const uint32_t u = __shfl_xor_sync(0xffffffffu, v, 1 << B);
-      uint32_t X = upper ? u : v;
-      const uint32_t Y = upper ? v : u;
-      X = umin32(X, X - p2);
-      const uint32_t Tt = mul_shoup_lazy(Y, w[e].x, w[e].y, p);
-      x[e] = upper ? X - Tt + p2 : X + Tt;
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const uint32_t v = x[r * G::E + e];
+        const uint32_t u = __shfl_xor_sync(0xffffffffu, v, 1 << B);
+        uint32_t X = upper ? u : v;
+        const uint32_t Y = upper ? v : u;
+        X = umin32(X, X - p2);
+        const uint32_t Tt = mul_shoup_lazy(Y, w[e].x, w[e].y, p);
+        x[r * G::E + e] = upper ? X - Tt + p2 : X + Tt;
+      }
     }
-    fwd_shfl<G, B - 1>(x, tw, p, tid);
+    fwd_shfl<G, B - 1, NR>(x, tw, p, tid);
   }
 }
 
-template <class G, int B>
+template <class G, int B, int NR>
 DI void inv_shfl(uint32_t* x, const uint2* __restrict__ itw, uint32_t p, int tid) {
   if constexpr (B < G::REM) {
     const uint32_t p2 = 2 * p;
@@ -260,64 +257,93 @@ DI void inv_shfl(uint32_t* x, const uint2* __restrict__ itw, uint32_t p, int tid
     load_shfl_tw<G, B>(w, itw, tid);
 #pragma unroll
     for (int e = 0; e < G::E; ++e) {
-      const uint32_t v = x[e];
-      const uint32_t u = __shfl_xor_sync(0xffffffffu, v, 1 << B);
-      const uint32_t X = upper ? u : v;
-      const uint32_t Y = upper ? v : u;
-      const uint32_t U = X + Y;
-      x[e] = upper ? mul_shoup_lazy(X - Y + p2, w[e].x, w[e].y, p) : umin32(U, U - p2);
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const uint32_t v = x[r * G::E + e];
+        const uint32_t u = __shfl_xor_sync(0xffffffffu, v, 1 << B);
+        const uint32_t X = upper ? u : v;
+        const uint32_t Y = upper ? v : u;
+        const uint32_t U = X + Y;
+        x[r * G::E + e] = upper ? mul_shoup_lazy(X - Y + p2, w[e].x, w[e].y, p) : umin32(U, U - p2);
+      }
     }
-    inv_shfl<G, B + 1>(x, itw, p, tid);
+    inv_shfl<G, B + 1, NR>(x, itw, p, tid);
   }
 }
 
-template <class G, int LO>
-DI void regs_to_smem(const uint32_t* x, uint32_t* s, int tid) {
-#pragma unroll
-  for (int e = 0; e < G::E; ++e)
-    s[sidx(pass_index<LO, G::LOGE>(tid, e))] = x[e];
+// exchange buffer XI of an NR-row transform
+template <class G, int NR>
+DI uint32_t* xbuf(uint32_t* s, int xi) {
+  if constexpr (G::dbl(NR)) return s + (xi & 1) * NR * G::XW;
+  else return s;
 }
 
-template <class G, int LO>
-DI void smem_to_regs(uint32_t* x, const uint32_t* s, int tid) {
-#pragma unroll
-  for (int e = 0; e < G::E; ++e)
-    x[e] = s[sidx(pass_index<LO, G::LOGE>(tid, e))];
+// before writing an exchange buffer: with a single buffer, wait until every
+// thread has read the previous exchange
+template <class G, int NR>
+DI void pre_exchange() {
+  if constexpr (!G::dbl(NR)) __syncthreads();
 }
 
-template <class G, int P>
+// after a transform: with two buffers the next transform's first exchange
+// writes buffer 0, which was read by this one's last exchange when the count
+// is odd; with one buffer it is always the same buffer
+template <class G, int NR>
+DI void post_transform() {
+  if constexpr (G::FWD_EXCHANGES > 0 && (!G::dbl(NR) || (G::FWD_EXCHANGES & 1))) __syncthreads();
+}
+
+template <class G, int LO, int NR>
+DI void regs_to_smem(const uint32_t* x, uint32_t* b, int tid) {
+#pragma unroll
+  for (int r = 0; r < NR; ++r)
+#pragma unroll
+    for (int e = 0; e < G::E; ++e) b[r * G::XW + sidx(pass_index<LO, G::LOGE>(tid, e))] = x[r * G::E + e];
+}
+
+template <class G, int LO, int NR>
+DI void smem_to_regs(uint32_t* x, const uint32_t* b, int tid) {
+#pragma unroll
+  for (int r = 0; r < NR; ++r)
+#pragma unroll
+    for (int e = 0; e < G::E; ++e) x[r * G::E + e] = b[r * G::XW + sidx(pass_index<LO, G::LOGE>(tid, e))];
+}
+
+template <class G, int P, int NR>
 DI void fwd_from(uint32_t* x, uint32_t* s, const uint2* __restrict__ tw, uint32_t p, int tid) {
   if constexpr (P < G::NFULL) {
     if constexpr (P > 0) {
-      uint32_t* b = s + ((P - 1) & 1) * G::XW;  // exchange P-1
-      regs_to_smem<G, G::lo(P - 1)>(x, b, tid);
+      uint32_t* b = xbuf<G, NR>(s, P - 1);  // exchange P-1
+      pre_exchange<G, NR>();
+      regs_to_smem<G, G::lo(P - 1), NR>(x, b, tid);
       __syncthreads();
-      smem_to_regs<G, G::lo(P)>(x, b, tid);
+      smem_to_regs<G, G::lo(P), NR>(x, b, tid);
     }
-    fwd_pass<G, G::lo(P)>(x, tw, p, tid);
-    fwd_from<G, P + 1>(x, s, tw, p, tid);
+    fwd_stage<G, G::lo(P), 0, NR>(x, tw, p, tid);
+    fwd_from<G, P + 1, NR>(x, s, tw, p, tid);
   }
 }
 
-template <class G, int P>
+template <class G, int P, int NR>
 DI void inv_from(uint32_t* x, uint32_t* s, const uint2* __restrict__ itw, uint32_t p, int tid) {
   if constexpr (P >= 0) {
     if constexpr (P < G::NFULL - 1) {
       // exchange index continues after the register-tail exchange (if any)
       constexpr int XI = (G::REG_TAIL ? 1 : 0) + (G::NFULL - 2 - P);
-      uint32_t* b = s + (XI & 1) * G::XW;
-      regs_to_smem<G, G::lo(P + 1)>(x, b, tid);
+      uint32_t* b = xbuf<G, NR>(s, XI);
+      pre_exchange<G, NR>();
+      regs_to_smem<G, G::lo(P + 1), NR>(x, b, tid);
       __syncthreads();
-      smem_to_regs<G, G::lo(P)>(x, b, tid);
+      smem_to_regs<G, G::lo(P), NR>(x, b, tid);
     }
-    inv_pass<G, G::lo(P)>(x, itw, p, tid);
-    inv_from<G, P - 1>(x, s, itw, p, tid);
+    inv_stage<G, G::lo(P), G::LOGE - 1, NR>(x, itw, p, tid);
+    inv_from<G, P - 1, NR>(x, s, itw, p, tid);
   }
 }
 
 // Register layouts at the boundaries:
 //   natural  : x[e] = a[e * T + tid]                     (coalesced global access)
-//   spectral : x[e] = A[pass_index<REM, LOGE>(tid, e)]   (what the forward leaves)
+//   spectral : x[e] = A[spectral_index(tid, e)]          (what the forward leaves)
 //   tiled    : spectral values in 16-byte groups (device key layout, below)
 template <class G>
 DI int natural_index(int tid, int e) { return e * G::T + tid; }
@@ -356,25 +382,6 @@ DI void load_tiled(uint32_t* x, const uint32_t* __restrict__ row, int tid) {
   }
 }
 
-// same, from shared memory
-template <class G>
-DI void load_tiled_smem(uint32_t* x, const uint32_t* row, int tid) {
-  if constexpr (G::E >= 4) {
-    const uint4* v = reinterpret_cast<const uint4*>(row) + tid;
-#pragma unroll
-    for (int k = 0; k < G::E / 4; ++k) {
-      const uint4 q = v[k * G::T];
-      x[4 * k] = q.x;
-      x[4 * k + 1] = q.y;
-      x[4 * k + 2] = q.z;
-      x[4 * k + 3] = q.w;
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < G::E; ++e) x[e] = row[tiled_index<G>(tid, e)];
-  }
-}
-
 template <class G>
 DI void store_tiled(const uint32_t* x, uint32_t* __restrict__ row, int tid) {
   if constexpr (G::E >= 4) {
@@ -388,51 +395,62 @@ DI void store_tiled(const uint32_t* x, uint32_t* __restrict__ row, int tid) {
   }
 }
 
-// Forward negacyclic NTT: natural layout in (any values < 4p), spectral layout
-// out, fully reduced to [0, p).  `s`: G::NTT_SMEM_WORDS of shared memory (two
-// padded buffers used alternately, one barrier per exchange).
-template <class G>
+// Forward negacyclic NTT of NR rows of one prime: natural layout in (values
+// < 4p), spectral layout out, fully reduced to [0, p).  `s`:
+// G::ntt_smem_words(NR) words of shared memory.
+template <class G, int NR = 1>
 DI void ntt_fwd(uint32_t* x, uint32_t* s, const uint2* __restrict__ tw, uint32_t p, int tid) {
-  fwd_from<G, 0>(x, s, tw, p, tid);
+  fwd_from<G, 0, NR>(x, s, tw, p, tid);
   if constexpr (G::SHFL_TAIL) {
-    fwd_shfl<G, G::REM - 1>(x, tw, p, tid);
+    fwd_shfl<G, G::REM - 1, NR>(x, tw, p, tid);
   } else if constexpr (G::REG_TAIL) {
-    uint32_t* b = s + ((G::NFULL - 1) & 1) * G::XW;
+    uint32_t* b = xbuf<G, NR>(s, G::NFULL - 1);
+    pre_exchange<G, NR>();
 #pragma unroll
-    for (int e = 0; e < G::E; ++e) b[sidx(pass_index<G::REM, G::LOGE>(tid, e))] = x[e];
+    for (int r = 0; r < NR; ++r)
+#pragma unroll
+      for (int e = 0; e < G::E; ++e) b[r * G::XW + sidx(pass_index<G::REM, G::LOGE>(tid, e))] = x[r * G::E + e];
     __syncthreads();
 #pragma unroll
-    for (int e = 0; e < G::E; ++e) x[e] = b[sidx(tail_index<G>(tid, e))];
-    fwd_tail<G, 0>(x, tw, p, tid);
+    for (int r = 0; r < NR; ++r)
+#pragma unroll
+      for (int e = 0; e < G::E; ++e) x[r * G::E + e] = b[r * G::XW + sidx(tail_index<G>(tid, e))];
+    fwd_tail<G, 0, NR>(x, tw, p, tid);
   }
-  if constexpr (G::FWD_EXCHANGES & 1) __syncthreads();
+  post_transform<G, NR>();
   const uint32_t p2 = 2 * p;
 #pragma unroll
-  for (int e = 0; e < G::E; ++e) {
+  for (int e = 0; e < NR * G::E; ++e) {
     const uint32_t v = umin32(x[e], x[e] - p2);
     x[e] = umin32(v, v - p);
   }
 }
 
-// Inverse negacyclic NTT: spectral layout in (values < 2p), natural layout out,
-// times N^-1, reduced to [0, p).
-template <class G>
+// Inverse negacyclic NTT of NR rows: spectral layout in (values < 2p),
+// natural layout out, times N^-1, reduced to [0, p).
+template <class G, int NR = 1>
 DI void ntt_inv(uint32_t* x, uint32_t* s, const uint2* __restrict__ itw, uint32_t p, uint2 ninv,
                 int tid) {
   if constexpr (G::SHFL_TAIL) {
-    inv_shfl<G, 0>(x, itw, p, tid);
+    inv_shfl<G, 0, NR>(x, itw, p, tid);
   } else if constexpr (G::REG_TAIL) {
-    inv_tail<G, G::REM - 1>(x, itw, p, tid);
+    inv_tail<G, G::REM - 1, NR>(x, itw, p, tid);
+    uint32_t* b = xbuf<G, NR>(s, 0);
+    pre_exchange<G, NR>();
 #pragma unroll
-    for (int e = 0; e < G::E; ++e) s[sidx(tail_index<G>(tid, e))] = x[e];
+    for (int r = 0; r < NR; ++r)
+#pragma unroll
+      for (int e = 0; e < G::E; ++e) b[r * G::XW + sidx(tail_index<G>(tid, e))] = x[r * G::E + e];
     __syncthreads();
 #pragma unroll
-    for (int e = 0; e < G::E; ++e) x[e] = s[sidx(pass_index<G::REM, G::LOGE>(tid, e))];
-  }
-  inv_from<G, G::NFULL - 1>(x, s, itw, p, tid);
-  if constexpr (G::FWD_EXCHANGES & 1) __syncthreads();
+    for (int r = 0; r < NR; ++r)
 #pragma unroll
-  for (int e = 0; e < G::E; ++e) x[e] = mul_shoup(x[e], ninv.x, ninv.y, p);
+      for (int e = 0; e < G::E; ++e) x[r * G::E + e] = b[r * G::XW + sidx(pass_index<G::REM, G::LOGE>(tid, e))];
+  }
+  inv_from<G, G::NFULL - 1, NR>(x, s, itw, p, tid);
+  post_transform<G, NR>();
+#pragma unroll
+  for (int e = 0; e < NR * G::E; ++e) x[e] = mul_shoup(x[e], ninv.x, ninv.y, p);
 }
 
 }  // namespace hcnn

@@ -92,14 +92,42 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
   }
 }
 
+// Transforms of two rows x[0, E) and x[E, 2E): in lockstep when the
+// geometry's shared memory allows, else one after the other.
+template <class G>
+__host__ __device__ constexpr int pair_nr() { return G::fits(2) ? 2 : 1; }
+
+template <class G>
+DI void ntt_fwd_pair(uint32_t* x, uint32_t* s, const uint2* tw, uint32_t p, int tid) {
+  if constexpr (pair_nr<G>() == 2) {
+    ntt_fwd<G, 2>(x, s, tw, p, tid);
+  } else {
+    ntt_fwd<G>(x, s, tw, p, tid);
+    ntt_fwd<G>(x + G::E, s, tw, p, tid);
+  }
+}
+
+template <class G>
+DI void ntt_inv_pair(uint32_t* x, uint32_t* s, const uint2* itw, uint32_t p, uint2 ninv, int tid) {
+  if constexpr (pair_nr<G>() == 2) {
+    ntt_inv<G, 2>(x, s, itw, p, ninv, tid);
+  } else {
+    ntt_inv<G>(x, s, itw, p, ninv, tid);
+    ntt_inv<G>(x + G::E, s, itw, p, ninv, tid);
+  }
+}
+
 // One CTA per (ct, prime of Q u P).  a/b: [B][2][K][N]; ae/be: [B][2][KP][N]
 // (exact extensions); d: [B][3][K+KP][N] exact tensor parts, coefficient domain.
+// The four (two for a square) forward transforms run as row pairs and the
+// inverse of d0, d1 as a pair, sharing twiddle loads and barriers.
 template <class G>
 __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
     k_tensor(const uint32_t* __restrict__ a, const uint32_t* __restrict__ a_ext,
              const uint32_t* __restrict__ b, const uint32_t* __restrict__ b_ext,
              uint32_t* __restrict__ d, int K, int KP, int square, NttTabs nt) {
   extern __shared__ uint32_t s[];
+  constexpr int E = G::E;
   const int tid = threadIdx.x;
   const int j = blockIdx.x;
   const size_t ct = blockIdx.y;
@@ -116,74 +144,81 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
   uint32_t* o0 = d + ((ct * 3 + 0) * L + j) * G::N;
   uint32_t* o1 = d + ((ct * 3 + 1) * L + j) * G::N;
   uint32_t* o2 = d + ((ct * 3 + 2) * L + j) * G::N;
-  uint32_t x0[G::E], x1[G::E], t[G::E];
-  load_natural<G>(x0, row_of(a, a_ext, 0), tid);
-  ntt_fwd<G>(x0, s, tw, p, tid);
+  uint32_t x[2 * E], y[2 * E];
   if (square) {
-    load_natural<G>(x1, row_of(a, a_ext, 1), tid);
-    ntt_fwd<G>(x1, s, tw, p, tid);
+    // x = (A0 | A1)
+    load_natural<G>(x, row_of(a, a_ext, 0), tid);
+    load_natural<G>(x + E, row_of(a, a_ext, 1), tid);
+    ntt_fwd_pair<G>(x, s, tw, p, tid);
 #pragma unroll
-    for (int e = 0; e < G::E; ++e) t[e] = mul_mod(x0[e], x0[e], p, mu);
-    inv_store<G>(t, s, itw, p, ninv, tid, o0);
-#pragma unroll
-    for (int e = 0; e < G::E; ++e) {
-      const uint32_t c = mul_mod(x0[e], x1[e], p, mu);
-      t[e] = add_mod(c, c, p);
+    for (int e = 0; e < E; ++e) {
+      const uint32_t a0 = x[e], a1 = x[E + e];
+      const uint32_t c = mul_mod(a0, a1, p, mu);
+      x[e] = mul_mod(a0, a0, p, mu);
+      x[E + e] = add_mod(c, c, p);
+      y[e] = mul_mod(a1, a1, p, mu);
     }
-    inv_store<G>(t, s, itw, p, ninv, tid, o1);
-#pragma unroll
-    for (int e = 0; e < G::E; ++e) t[e] = mul_mod(x1[e], x1[e], p, mu);
-    inv_store<G>(t, s, itw, p, ninv, tid, o2);
   } else {
-    // x0 = A0, x1 = B0 -> d0; then A1 into t; x1 := A1 B0 (part of d1)
-    load_natural<G>(x1, row_of(b, b_ext, 0), tid);
-    ntt_fwd<G>(x1, s, tw, p, tid);
+    // x = (A0 | B0), y = (A1 | B1)
+    load_natural<G>(x, row_of(a, a_ext, 0), tid);
+    load_natural<G>(x + E, row_of(b, b_ext, 0), tid);
+    ntt_fwd_pair<G>(x, s, tw, p, tid);
+    load_natural<G>(y, row_of(a, a_ext, 1), tid);
+    load_natural<G>(y + E, row_of(b, b_ext, 1), tid);
+    ntt_fwd_pair<G>(y, s, tw, p, tid);
 #pragma unroll
-    for (int e = 0; e < G::E; ++e) t[e] = mul_mod(x0[e], x1[e], p, mu);
-    inv_store<G>(t, s, itw, p, ninv, tid, o0);
-    load_natural<G>(t, row_of(a, a_ext, 1), tid);
-    ntt_fwd<G>(t, s, tw, p, tid);
-#pragma unroll
-    for (int e = 0; e < G::E; ++e) x1[e] = mul_mod(t[e], x1[e], p, mu);
-    uint32_t y1[G::E];
-    load_natural<G>(y1, row_of(b, b_ext, 1), tid);
-    ntt_fwd<G>(y1, s, tw, p, tid);
-#pragma unroll
-    for (int e = 0; e < G::E; ++e) {
-      x1[e] = add_mod(x1[e], mul_mod(x0[e], y1[e], p, mu), p);  // d1
-      t[e] = mul_mod(t[e], y1[e], p, mu);                       // d2
+    for (int e = 0; e < E; ++e) {
+      const uint32_t a0 = x[e], b0 = x[E + e], a1 = y[e], b1 = y[E + e];
+      x[e] = mul_mod(a0, b0, p, mu);
+      x[E + e] = add_mod(mul_mod(a0, b1, p, mu), mul_mod(a1, b0, p, mu), p);
+      y[e] = mul_mod(a1, b1, p, mu);
     }
-    inv_store<G>(x1, s, itw, p, ninv, tid, o1);
-    inv_store<G>(t, s, itw, p, ninv, tid, o2);
   }
+  ntt_inv_pair<G>(x, s, itw, p, ninv, tid);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    o0[natural_index<G>(tid, e)] = x[e];
+    o1[natural_index<G>(tid, e)] = x[E + e];
+  }
+  inv_store<G>(y, s, itw, p, ninv, tid, o2);
 }
 
-// Shared-memory plan of k_relin: STAGES buffers, each holding one digit row
-// (padded, doubling as the NTT exchange buffer once its residues are in
-// registers) and the two rlk rows of that digit, streamed in by TMA bulk
-// copies one digit ahead of the compute.
+// Relinearisation configuration of a geometry: NR digit rows transformed in
+// lockstep, and the accumulator form: lazy u64 (plain keys) while the
+// registers allow, else u32 fed by Montgomery products (keys uploaded in
+// Montgomery form).  single selects the one-row kernel (variant flag).
 template <class G>
+__host__ __device__ constexpr int relin_nr(bool single) { return single ? 1 : pair_nr<G>(); }
+
+template <class G>
+__host__ __device__ constexpr bool relin_acc64(bool single) { return relin_nr<G>(single) * G::E <= 16 && G::T <= 512; }
+
+// Shared-memory plan of k_relin: [NTT exchange buffers][STAGES groups of NR
+// digit rows streamed in by TMA bulk copies one group ahead][mbarriers]
+template <class G, int NR>
 struct RelinSmem {
-  // [two NTT exchange buffers][STAGES digit rows streamed by TMA][mbarriers]
-  static constexpr int STAGE_WORDS = G::N;
   static constexpr int LIMIT = 220 * 1024;
-  static constexpr int BASE = G::NTT_SMEM_WORDS;
-  static constexpr int STAGES = (BASE + 2 * G::N) * 4 <= LIMIT ? 2 : ((BASE + G::N) * 4 <= LIMIT ? 1 : 0);
-  static constexpr int BYTES = (BASE + STAGES * G::N) * 4 + 16 * 2;
+  static constexpr int BASE = G::ntt_smem_words(NR);
+  static constexpr int STAGE_WORDS = NR * G::N;
+  static constexpr int STAGES = (BASE + 2 * STAGE_WORDS) * 4 <= LIMIT ? 2
+                                : ((BASE + STAGE_WORDS) * 4 <= LIMIT ? 1 : 0);
+  static constexpr int BYTES = (BASE + STAGES * STAGE_WORDS) * 4 + 16 * 2;
 };
 
 // One CTA per (ct, prime of q).  dig: [B][D][N] base-w digits of c2;
 // y3: [B][3][K][N] scaled parts (0 and 1 used); rlk: [D][2][K][N] NTT domain,
 // tiled layout (ntt.cuh), Montgomery form unless ACC64;
 // out: [B][2][K][N] = (y0 + sum_i D_i k0_i, y1 + sum_i D_i k1_i).
-// ACC64: lazy 64-bit accumulators (one reduction per 15 digits); otherwise
-// u32 accumulators in [0, 2p) fed by Montgomery products (half the registers).
-template <class G, bool ACC64>
+// Digits go through the forward NTT NR at a time (a single one first when the
+// count is odd); ACC64: lazy 64-bit accumulators (reduced before 16 products
+// pile up); otherwise u32 accumulators in [0, 2p) fed by Montgomery products.
+template <class G, bool ACC64, int NR>
 __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
     k_relin(const uint32_t* __restrict__ dig, const uint32_t* __restrict__ y3,
             const uint32_t* __restrict__ rlk, uint32_t* __restrict__ out, int K, int D,
             int reduce_digits, NttTabs nt) {
-  using SM = RelinSmem<G>;
+  using SM = RelinSmem<G, NR>;
+  constexpr int E = G::E;
   extern __shared__ __align__(16) uint32_t s[];
   const int tid = threadIdx.x;
   const int j = blockIdx.x;
@@ -194,96 +229,132 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
   const uint32_t p2 = 2 * p;
   const uint2* tw = nt.tw + (size_t)j * G::N;
   using Acc = typename std::conditional<ACC64, uint64_t, uint32_t>::type;
-  Acc acc0[G::E], acc1[G::E];
+  Acc acc0[E], acc1[E];
 #pragma unroll
-  for (int e = 0; e < G::E; ++e) acc0[e] = acc1[e] = 0;
+  for (int e = 0; e < E; ++e) acc0[e] = acc1[e] = 0;
 
   const uint32_t* dig_ct = dig + ct * D * G::N;
   auto krow = [&](int i, int part) { return rlk + ((size_t)(i * 2 + part) * K + j) * G::N; };
+  // rows in the group starting at digit i
+  auto group_rows = [&](int i) { return (NR == 2 && ((D - i) & 1)) ? 1 : NR; };
   uint32_t* stage0 = s + SM::BASE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stage0 + SM::STAGES * G::N);
-  auto issue = [&](int i) {  // elected thread: digit row i into its stage
-    uint64_t* bar = &bars[i % SM::STAGES];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage0 + SM::STAGES * SM::STAGE_WORDS);
+  auto issue = [&](int i, int g) {  // elected thread: group g (from digit i) into its stage
+    constexpr int NS = SM::STAGES > 0 ? SM::STAGES : 1;
+    uint64_t* bar = &bars[g % NS];
+    const uint32_t bytes = (uint32_t)group_rows(i) * G::N * 4;
     fence_proxy_async();
-    mbar_expect_tx(bar, G::N * 4);
-    bulk_g2s(stage0 + (i % SM::STAGES) * G::N, dig_ct + (size_t)i * G::N, G::N * 4, bar);
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(stage0 + (g % NS) * SM::STAGE_WORDS, dig_ct + (size_t)i * G::N, bytes, bar);
   };
   if constexpr (SM::STAGES > 0) {
     if (tid == 0) {
       for (int st = 0; st < SM::STAGES; ++st) mbar_init(&bars[st], 1);
       fence_mbar_init();
-      issue(0);
+      issue(0, 0);
     }
     __syncthreads();
   }
 
-  for (int i = 0; i < D; ++i) {
-    uint32_t x[G::E];
+  int pending = 0;  // ACC64: products accumulated since the last reduction
+  auto step = [&](auto rows_c, int i, int g) {
+    constexpr int R = decltype(rows_c)::value;
+    uint32_t x[R * E];
     if constexpr (SM::STAGES > 0) {
-      // with two stages, digit i+1 streams in while digit i is transformed;
-      // its buffer was last read before this thread's previous-digit barriers
+      // with two stages, group g+1 streams in while group g is transformed;
+      // its buffer was last read before this thread's previous-group barriers
       if constexpr (SM::STAGES == 2) {
-        if (tid == 0 && i + 1 < D) issue(i + 1);
+        if (tid == 0 && i + R < D) issue(i + R, g + 1);
       }
-      const uint32_t* row = stage0 + (i % SM::STAGES) * G::N;
-      mbar_wait(&bars[i % SM::STAGES], (uint32_t)(i / SM::STAGES) & 1);
+      const uint32_t* row = stage0 + (g % SM::STAGES) * SM::STAGE_WORDS;
+      mbar_wait(&bars[g % SM::STAGES], (uint32_t)(g / SM::STAGES) & 1);
 #pragma unroll
-      for (int e = 0; e < G::E; ++e) x[e] = row[natural_index<G>(tid, e)];
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int e = 0; e < E; ++e) x[r * E + e] = row[r * G::N + natural_index<G>(tid, e)];
       if constexpr (SM::STAGES == 1) {
         __syncthreads();
-        if (tid == 0 && i + 1 < D) issue(i + 1);
+        if (tid == 0 && i + R < D) issue(i + R, g + 1);
       }
     } else {
-      load_natural<G>(x, dig_ct + (size_t)i * G::N, tid);
+#pragma unroll
+      for (int r = 0; r < R; ++r) load_natural<G>(x + r * E, dig_ct + (size_t)(i + r) * G::N, tid);
     }
     if (reduce_digits) {
 #pragma unroll
-      for (int e = 0; e < G::E; ++e) x[e] = reduce64(x[e], p, mu);
+      for (int e = 0; e < R * E; ++e) x[e] = reduce64(x[e], p, mu);
     }
-    ntt_fwd<G>(x, s, tw, p, tid);
+    ntt_fwd<G, R>(x, s, tw, p, tid);
 #pragma unroll
-    for (int part = 0; part < 2; ++part) {
-      Acc* acc = part ? acc1 : acc0;
-      uint32_t k[G::E];
-      load_tiled<G>(k, krow(i, part), tid);
+    for (int r = 0; r < R; ++r) {
 #pragma unroll
-      for (int e = 0; e < G::E; ++e) {
-        if constexpr (ACC64) {
-          acc[e] += (uint64_t)x[e] * k[e];
-        } else {
-          const uint32_t v = acc[e] + mont_mul(x[e], k[e], p, pinv);
-          acc[e] = umin32(v, v - p2);
+      for (int part = 0; part < 2; ++part) {
+        Acc* acc = part ? acc1 : acc0;
+        uint32_t k[E];
+        load_tiled<G>(k, krow(i + r, part), tid);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          if constexpr (ACC64) {
+            acc[e] += (uint64_t)x[r * E + e] * k[e];
+          } else {
+            const uint32_t v = acc[e] + mont_mul(x[r * E + e], k[e], p, pinv);
+            acc[e] = umin32(v, v - p2);
+          }
         }
       }
     }
     if constexpr (ACC64) {
-      // at most 16 products of (p-1)^2 on top of a reduced value stay < 2^64
-      if ((i & 15) == 14) {
+      // a reduced value plus 16 products of (p-1)^2 stays below 2^64
+      pending += R;
+      if (pending + NR > 16) {
 #pragma unroll
-        for (int e = 0; e < G::E; ++e) {
+        for (int e = 0; e < E; ++e) {
           acc0[e] = reduce64(acc0[e], p, mu);
           acc1[e] = reduce64(acc1[e], p, mu);
         }
+        pending = 0;
       }
     }
+  };
+  for (int i = 0, g = 0; i < D; ++g) {
+    const int R = group_rows(i);
+    if (NR == 2 && R == 2) {
+      step(std::integral_constant<int, NR>(), i, g);
+    } else {
+      step(std::integral_constant<int, 1>(), i, g);
+      // a one-row transform's last exchange buffer overlaps the two-row one's first
+      if constexpr (NR == 2) __syncthreads();
+    }
+    i += R;
   }
   const uint2* itw = nt.itw + (size_t)j * G::N;
   const uint2 ninv = nt.ninv[j];
+  // both parts through the inverse (in lockstep when NR = 2)
+  uint32_t x[2 * E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    if constexpr (ACC64) {
+      x[e] = reduce64(acc0[e], p, mu);
+      x[E + e] = reduce64(acc1[e], p, mu);
+    } else {  // in [0, 2p): valid inverse input
+      x[e] = acc0[e];
+      x[E + e] = acc1[e];
+    }
+  }
+  if constexpr (NR == 2) {
+    ntt_inv<G, 2>(x, s, itw, p, ninv, tid);
+  } else {
+    ntt_inv<G>(x, s, itw, p, ninv, tid);
+    ntt_inv<G>(x + E, s, itw, p, ninv, tid);
+  }
 #pragma unroll
   for (int part = 0; part < 2; ++part) {
-    uint32_t x[G::E];
-#pragma unroll
-    for (int e = 0; e < G::E; ++e) {
-      if constexpr (ACC64) x[e] = reduce64(part ? acc1[e] : acc0[e], p, mu);
-      else x[e] = part ? acc1[e] : acc0[e];  // in [0, 2p): valid inverse input
-    }
-    ntt_inv<G>(x, s, itw, p, ninv, tid);
     const uint32_t* yr = y3 + ((ct * 3 + part) * K + j) * G::N;
     uint32_t* o = out + ((ct * 2 + part) * K + j) * G::N;
 #pragma unroll
-    for (int e = 0; e < G::E; ++e) {
+    for (int e = 0; e < E; ++e) {
       const int idx = natural_index<G>(tid, e);
-      o[idx] = add_mod(x[e], yr[idx], p);
+      o[idx] = add_mod(x[part * E + e], yr[idx], p);
     }
   }
 }
@@ -371,18 +442,30 @@ __global__ void k_to_mont(uint32_t* __restrict__ rows, int limbs, NttTabs nt) {
 
 template <class G>
 void configure_smem() {
-  const int smem = G::NTT_SMEM_WORDS * sizeof(uint32_t);
+  const int smem = G::ntt_smem_words(1) * sizeof(uint32_t);
   cudaFuncSetAttribute(k_ntt_rows<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_tensor<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_relin<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, RelinSmem<G>::BYTES);
-  cudaFuncSetAttribute(k_relin<G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, RelinSmem<G>::BYTES);
+  cudaFuncSetAttribute(k_tensor<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       G::ntt_smem_words(pair_nr<G>()) * sizeof(uint32_t));
+  cudaFuncSetAttribute(k_relin<G, relin_acc64<G>(false), relin_nr<G>(false)>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, RelinSmem<G, relin_nr<G>(false)>::BYTES);
+  cudaFuncSetAttribute(k_relin<G, relin_acc64<G>(true), 1>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, RelinSmem<G, 1>::BYTES);
   cudaFuncSetAttribute(k_encrypt<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
-// relin accumulators: u64 when the registers allow (<= 16 per thread and at
-// most 512 threads), Montgomery u32 otherwise (rlk uploaded in that form)
-template <class G>
-constexpr bool relin_acc64() { return G::E <= 16 && G::T <= 512; }
+// variant: bits 0-3 = log2 E of the fused kernels (0 = default geometry);
+// RELIN_SINGLE = one-row relinearisation transforms
+constexpr int RELIN_SINGLE = 16;
+
+template <class G, bool SINGLE>
+cudaError_t launch_relin(const NttLaunch& a) {
+  constexpr int NR = relin_nr<G>(SINGLE);
+  constexpr bool ACC64 = relin_acc64<G>(SINGLE);
+  if (a.rlk_mont != (ACC64 ? 0 : 1)) return cudaErrorInvalidValue;
+  k_relin<G, ACC64, NR><<<a.grid, G::T, RelinSmem<G, NR>::BYTES, a.stream>>>(
+      a.dig, a.y3, a.rlk, a.out, a.K, a.D, a.reduce_digits, a.nt);
+  return cudaSuccess;
+}
 
 template <class G>
 cudaError_t launch_with(int op, const NttLaunch& a) {
@@ -391,21 +474,20 @@ cudaError_t launch_with(int op, const NttLaunch& a) {
     configure_smem<G>();
     configured = true;
   }
-  const size_t smem = G::NTT_SMEM_WORDS * sizeof(uint32_t);
+  const size_t smem = G::ntt_smem_words(1) * sizeof(uint32_t);
   switch (op) {
     case 0:
       k_ntt_rows<G><<<a.grid, G::T, smem, a.stream>>>(a.rows, a.limbs, a.prime_off, a.inverse, a.nt);
       break;
     case 1:
-      k_tensor<G><<<a.grid, G::T, smem, a.stream>>>(a.a, a.ae, a.b, a.be, a.d, a.K, a.KP, a.square, a.nt);
+      k_tensor<G><<<a.grid, G::T, G::ntt_smem_words(pair_nr<G>()) * sizeof(uint32_t), a.stream>>>(
+          a.a, a.ae, a.b, a.be, a.d, a.K, a.KP, a.square, a.nt);
       break;
-    case 2:
-      if (a.rlk_mont != (relin_acc64<G>() ? 0 : 1)) return cudaErrorInvalidValue;
-      if constexpr (relin_acc64<G>())
-        k_relin<G, true><<<a.grid, G::T, RelinSmem<G>::BYTES, a.stream>>>(a.dig, a.y3, a.rlk, a.out, a.K, a.D, a.reduce_digits, a.nt);
-      else
-        k_relin<G, false><<<a.grid, G::T, RelinSmem<G>::BYTES, a.stream>>>(a.dig, a.y3, a.rlk, a.out, a.K, a.D, a.reduce_digits, a.nt);
+    case 2: {
+      const cudaError_t e = (a.variant & RELIN_SINGLE) ? launch_relin<G, true>(a) : launch_relin<G, false>(a);
+      if (e != cudaSuccess) return e;
       break;
+    }
     case 3:
       k_encrypt<G><<<a.grid, G::T, smem, a.stream>>>(a.u, a.e1, a.e2, a.msg, a.pk, a.delta, a.out, a.K, a.nt);
       break;
@@ -421,33 +503,38 @@ cudaError_t launch_with(int op, const NttLaunch& a) {
   return cudaGetLastError();
 }
 
-// variant: log2 E of the fused kernels (0 = default geometry); the key layout
-// (tiled, Montgomery) follows the geometry, so keys are uploaded per variant.
+// The key layout (tiled, Montgomery or not) follows the geometry and the
+// relinearisation kernel, so keys are laid out per variant.
 template <int LOGN>
 cudaError_t ntt_launch(int op, const NttLaunch& a) {
+  const int loge = a.variant & 15;
   if constexpr (LOGN >= 10 && LOGN <= 13 && pick_loge(LOGN) != 3) {
-    if (a.variant == 3) return launch_with<NttGeom<LOGN, 3>>(op, a);
+    if (loge == 3) return launch_with<NttGeom<LOGN, 3>>(op, a);
   }
   if constexpr (LOGN >= 10 && pick_loge(LOGN) != 5) {
-    if (a.variant == 5) return launch_with<NttGeom<LOGN, 5>>(op, a);
+    if (loge == 5) return launch_with<NttGeom<LOGN, 5>>(op, a);
   }
   if constexpr (LOGN >= 10 && pick_loge(LOGN) != 4) {
-    if (a.variant == 4) return launch_with<NttGeom<LOGN, 4>>(op, a);
+    if (loge == 4) return launch_with<NttGeom<LOGN, 4>>(op, a);
   }
   return launch_with<NttGeom<LOGN>>(op, a);
 }
 
+template <class G>
+int mont_of(int v) { return relin_acc64<G>((v & RELIN_SINGLE) != 0) ? 0 : 1; }
+
 // does variant v use Montgomery-form rlk?
 template <int LOGN>
 int ntt_variant_mont(int v) {
+  const int loge = v & 15;
   if constexpr (LOGN >= 10 && LOGN <= 13) {
-    if (v == 3) return relin_acc64<NttGeom<LOGN, 3>>() ? 0 : 1;
+    if (loge == 3) return mont_of<NttGeom<LOGN, 3>>(v);
   }
   if constexpr (LOGN >= 10) {
-    if (v == 5) return relin_acc64<NttGeom<LOGN, 5>>() ? 0 : 1;
-    if (v == 4) return relin_acc64<NttGeom<LOGN, 4>>() ? 0 : 1;
+    if (loge == 5) return mont_of<NttGeom<LOGN, 5>>(v);
+    if (loge == 4) return mont_of<NttGeom<LOGN, 4>>(v);
   }
-  return relin_acc64<NttGeom<LOGN>>() ? 0 : 1;
+  return mont_of<NttGeom<LOGN>>(v);
 }
 
 }  // namespace hcnn
