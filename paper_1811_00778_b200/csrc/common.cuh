@@ -66,6 +66,8 @@ struct NttTabs {
   const uint2* itw;       // [(K+KP) * N]  psi^-brv(i), Shoup
   const uint2* ninv;      // [K+KP]        N^-1, Shoup
   const uint32_t* pinv;   // [K+KP]        -p^-1 mod 2^32 (Montgomery)
+  const uint2* ninv_m;    // [K+KP]        N^-1 2^32 mod p, Shoup: undoes the 2^-32
+                          //               of Montgomery pointwise products
 };
 
 // fixed point of the CRT overflow estimates: 59 fractional bits

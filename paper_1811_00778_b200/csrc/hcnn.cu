@@ -212,7 +212,7 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
   // NTT tables
   std::vector<uint32_t> hp(L);
   std::vector<uint64_t> hmu(L);
-  std::vector<uint2> htw((size_t)L * N), hitw((size_t)L * N), hninv(L);
+  std::vector<uint2> htw((size_t)L * N), hitw((size_t)L * N), hninv(2 * L);
   std::vector<uint32_t> hpinv(L);
   c->psi.resize(L);
   for (uint32_t j = 0; j < L; ++j) {
@@ -240,6 +240,8 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
     }
     const uint32_t ninv = (uint32_t)invmod64(N % p, p);
     hninv[j] = make_uint2(ninv, shoup_of(ninv, (uint32_t)p));
+    const uint32_t ninv_m = (uint32_t)mont_form(ninv, p);
+    hninv[L + j] = make_uint2(ninv_m, shoup_of(ninv_m, (uint32_t)p));
   }
 
   // exact base conversion and scaling constants
@@ -325,15 +327,15 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
   CK(cudaMalloc(&c->d_mu, L * sizeof(uint64_t)));
   CK(cudaMalloc(&c->d_tw, (size_t)L * N * sizeof(uint2)));
   CK(cudaMalloc(&c->d_itw, (size_t)L * N * sizeof(uint2)));
-  CK(cudaMalloc(&c->d_ninv, L * sizeof(uint2)));
+  CK(cudaMalloc(&c->d_ninv, 2 * L * sizeof(uint2)));
   CK(cudaMalloc(&c->d_pinv, L * sizeof(uint32_t)));
   CK(cudaMemcpy(c->d_pinv, hpinv.data(), L * sizeof(uint32_t), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_prime, hp.data(), L * sizeof(uint32_t), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_mu, hmu.data(), L * sizeof(uint64_t), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_tw, htw.data(), (size_t)L * N * sizeof(uint2), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_itw, hitw.data(), (size_t)L * N * sizeof(uint2), cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(c->d_ninv, hninv.data(), L * sizeof(uint2), cudaMemcpyHostToDevice));
-  c->nt = NttTabs{c->d_prime, c->d_mu, c->d_tw, c->d_itw, c->d_ninv, c->d_pinv};
+  CK(cudaMemcpy(c->d_ninv, hninv.data(), 2 * L * sizeof(uint2), cudaMemcpyHostToDevice));
+  c->nt = NttTabs{c->d_prime, c->d_mu, c->d_tw, c->d_itw, c->d_ninv, c->d_pinv, c->d_ninv + L};
 }
 
 // ---------------------------------------------------------------- dispatch
@@ -634,11 +636,11 @@ void layout_key(hcnn_ctx* c, const uint32_t* raw, int domain, size_t rows, uint3
 }
 
 void prepare_keys(hcnn_ctx* c) {
-  if (c->keys_variant == c->variant) return;
+  if (c->keys_variant == (c->variant & ~32)) return;
   if (c->d_rlk_raw)
     layout_key(c, c->d_rlk_raw, c->rlk_domain, (size_t)c->D * 2 * c->K, &c->d_rlk, variant_mont(c, c->variant));
   if (c->d_pk_raw) layout_key(c, c->d_pk_raw, c->pk_domain, 2 * (size_t)c->K, &c->d_pk, 0);
-  c->keys_variant = c->variant;
+  c->keys_variant = c->variant & ~32;
 }
 
 }  // namespace
@@ -793,14 +795,11 @@ int hcnn_ctx_set_stream(hcnn_ctx* c, void* stream) {
 int hcnn_ctx_set_option(hcnn_ctx* c, int key, int64_t value) {
   return guarded([&] {
     if (key == HCNN_OPT_NTT_VARIANT) {
-      // low 4 bits: log2 E of the fused kernels (0 = default); +16: one-row
-      // relinearisation transforms (ntt_kernels.cuh RELIN_SINGLE)
-      const int64_t loge = value & 15;
-      if ((value & ~(int64_t)31) || (loge != 0 && loge != 3 && loge != 4 && loge != 5))
-        fail(HCNN_ERR_PARAM, "NTT variant must be 0, 3, 4 or 5 (+16 for one-row relinearisation)");
-      if (loge && c->logN < 10) fail(HCNN_ERR_UNSUPPORTED, "NTT variants need N >= 1024");
-      if (loge == 3 && c->logN > 13) fail(HCNN_ERR_UNSUPPORTED, "NTT variant 3 needs N <= 8192");
-      if (loge && c->logN > (uint32_t)loge + 10) fail(HCNN_ERR_UNSUPPORTED, "NTT variant needs more than 1024 threads");
+      // geometry flags of the fused kernels (ntt_kernels.cuh): +16 one-row
+      // relinearisation transforms, +32 square tensors on the radix-32 mixed
+      // geometry, +64 mixed-width passes instead of a warp-shuffle tail
+      if (value & ~(int64_t)(16 | 32 | 64)) fail(HCNN_ERR_PARAM, "NTT variant flags are 16, 32 and 64");
+      if ((value & (32 | 64)) && c->logN < 10) fail(HCNN_ERR_UNSUPPORTED, "mixed geometries need N >= 1024");
       c->variant = (int)value;
     } else {
       fail(HCNN_ERR_PARAM, "unknown option");

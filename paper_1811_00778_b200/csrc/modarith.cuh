@@ -43,4 +43,17 @@ DI uint32_t mul_mod(uint32_t a, uint32_t b, uint32_t p, uint64_t mu) {
   return reduce64((uint64_t)a * b, p, mu);
 }
 
+// Montgomery reduction z 2^-32 mod p in [0, 2p) for z < 2^32 p;
+// pinv = -p^-1 mod 2^32.
+DI uint32_t redc64(uint64_t z, uint32_t p, uint32_t pinv) {
+  const uint32_t m = (uint32_t)z * pinv;
+  return (uint32_t)((z + (uint64_t)m * p) >> 32);
+}
+
+// Montgomery product x k 2^-32 mod p in [0, 2p) for x, k < p < 2^30.  With
+// k = k' 2^32 mod p (Montgomery form) this is x k' mod p.
+DI uint32_t mont_mul(uint32_t x, uint32_t k, uint32_t p, uint32_t pinv) {
+  return redc64((uint64_t)x * k, p, pinv);
+}
+
 }  // namespace hcnn

@@ -33,7 +33,12 @@ __host__ __device__ constexpr int pick_loge(int logn) {
   return logn >= 15 ? 5 : logn >= 9 ? 4 : logn >= 6 ? logn - 5 : 1;
 }
 
-template <int LOGN_, int LOGE_ = pick_loge(LOGN_), bool SHFL_TAIL_ = (LOGE_ <= 4)>
+// MIXED geometries cover the LOGN butterfly bits with passes of unequal
+// width and no tail: the first pass takes LOGE bits (natural layout in), the
+// remaining bits are split evenly over the other passes; a pass narrower than
+// LOGE works on E / 2^kb independent groups per thread.  They use one
+// exchange buffer at radix 32 (so that two CTAs fit one SM).
+template <int LOGN_, int LOGE_ = pick_loge(LOGN_), bool SHFL_TAIL_ = (LOGE_ <= 4), bool MIXED_ = false>
 struct NttGeom {
   static constexpr int LOGN = LOGN_;
   static constexpr int N = 1 << LOGN;
@@ -41,10 +46,12 @@ struct NttGeom {
   static constexpr int E = 1 << LOGE;
   static constexpr int LOGT = LOGN - LOGE;
   static constexpr int T = 1 << LOGT;
-  static constexpr int NFULL = LOGN / LOGE;  // radix-E passes
-  static constexpr int REM = LOGN % LOGE;    // low bits of the tail
-  static constexpr bool SHFL_TAIL = SHFL_TAIL_ && REM > 0;
-  static constexpr bool REG_TAIL = !SHFL_TAIL_ && REM > 0;
+  static constexpr bool MIXED = MIXED_;
+  static constexpr int REST = LOGN - LOGE;
+  static constexpr int NFULL = MIXED ? 1 + (REST + LOGE - 1) / LOGE : LOGN / LOGE;  // passes
+  static constexpr int REM = MIXED ? 0 : LOGN % LOGE;  // low bits of the tail
+  static constexpr bool SHFL_TAIL = !MIXED && SHFL_TAIL_ && REM > 0;
+  static constexpr bool REG_TAIL = !MIXED && !SHFL_TAIL_ && REM > 0;
   static_assert(!SHFL_TAIL || T >= 32, "shuffle stages need full warps");
   // shared-memory words for one padded row; an NR-row NTT uses
   // ntt_smem_words(NR) (two alternating buffers of NR rows)
@@ -52,13 +59,17 @@ struct NttGeom {
   static constexpr int XW = (SMEM_WORDS + 3) & ~3;
   // two alternating exchange buffers (one barrier per exchange) when they fit
   // in LIMIT_WORDS, else one buffer and two barriers per exchange
-  static constexpr int LIMIT_WORDS = 200 * 1024 / 4;
+  static constexpr int LIMIT_WORDS = (MIXED && LOGE >= 5 ? 40 : 200) * 1024 / 4;
   __host__ __device__ static constexpr bool dbl(int nr) { return 2 * nr * XW <= LIMIT_WORDS; }
   __host__ __device__ static constexpr int ntt_smem_words(int nr) { return (dbl(nr) ? 2 : 1) * nr * XW; }
   __host__ __device__ static constexpr bool fits(int nr) { return ntt_smem_words(nr) <= 227 * 1024 / 4; }
   static constexpr int FWD_EXCHANGES = NFULL - 1 + (REG_TAIL ? 1 : 0);
-  // pass P covers butterfly bits [lo(P), lo(P) + LOGE), from the top
-  __host__ __device__ static constexpr int lo(int P) { return LOGN - (P + 1) * LOGE; }
+  // width of pass P (from the top bits)
+  __host__ __device__ static constexpr int kb(int P) {
+    return !MIXED ? LOGE : P == 0 ? LOGE : REST / (NFULL - 1) + ((P - 1) < REST % (NFULL - 1) ? 1 : 0);
+  }
+  // pass P covers butterfly bits [lo(P), lo(P) + kb(P)), from the top
+  __host__ __device__ static constexpr int lo(int P) { return P < 0 ? LOGN : lo(P - 1) - kb(P); }
 };
 
 // padded shared-memory slot of element idx (2 words every 32)
@@ -71,7 +82,36 @@ DI int pass_index(int tid, int e) {
   return ((tid >> LO) << (LO + KB)) | (e << LO) | (tid & ((1 << LO) - 1));
 }
 
+// Element index of register e in a pass of KB <= LOGE bits at [LO, LO+KB):
+// e = (g, el), el supplies the butterfly bits and o = (g, tid) the others.
+template <class G, int LO, int KB>
+DI int gpass_index(int tid, int e) {
+  if constexpr (KB == G::LOGE) {
+    return pass_index<LO, KB>(tid, e);
+  } else {
+    const int o = ((e >> KB) << G::LOGT) | tid;
+    return ((o >> LO) << (LO + KB)) | ((e & ((1 << KB) - 1)) << LO) | (o & ((1 << LO) - 1));
+  }
+}
+
 DI uint32_t umin32(uint32_t a, uint32_t b) { return a < b ? a : b; }
+
+// Twiddle loads are volatile non-coherent loads: kernels that run several
+// transforms with the same table must not keep one transform's twiddles live
+// into the next (the compiler would CSE __ldg loads and pin registers).
+DI uint4 ldg_tw4(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+DI uint2 ldg_tw2(const uint2* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
 
 // register-tail mapping: bits [0, REM) from e's low bits, group e >> REM and
 // tid fill the rest
@@ -84,12 +124,12 @@ DI int tail_index(int tid, int e) {
 template <int COUNT>
 DI void load_tw(uint2* w, const uint2* __restrict__ tw, int base) {
   if constexpr (COUNT == 1) {
-    w[0] = __ldg(&tw[base]);
+    w[0] = ldg_tw2(&tw[base]);
   } else {
     const uint4* v = reinterpret_cast<const uint4*>(tw + base);
 #pragma unroll
     for (int k = 0; k < COUNT / 2; ++k) {
-      const uint4 q = __ldg(&v[k]);
+      const uint4 q = ldg_tw4(&v[k]);
       w[2 * k] = make_uint2(q.x, q.y);
       w[2 * k + 1] = make_uint2(q.z, q.w);
     }
@@ -110,48 +150,67 @@ DI void bfly_inv(uint32_t& a, uint32_t& b, uint2 w, uint32_t p, uint32_t p2) {
   b = mul_shoup_lazy(X - Y + p2, w.x, w.y, p);
 }
 
-// forward (CT) stage SS of a radix-E pass at bits [LO, LO+LOGE); values in [0, 4p)
-template <class G, int LO, int SS, int NR>
+// twiddle pairs live at once per stage (bounds register pressure at radix 32)
+constexpr int TW_CHUNK = 4;
+
+// forward (CT) stage SS of a pass at bits [LO, LO+KB); values in [0, 4p)
+template <class G, int LO, int KB, int SS, int NR>
 DI void fwd_stage(uint32_t* x, const uint2* __restrict__ tw, uint32_t p, int tid) {
-  constexpr int KB = G::LOGE;
   if constexpr (SS < KB) {
-    constexpr int E = G::E;
     constexpr int bpos = LO + KB - 1 - SS;
     constexpr int s = G::LOGN - 1 - bpos;
     constexpr int half = 1 << (KB - 1 - SS);
     const uint32_t p2 = 2 * p;
-    uint2 w[1 << SS];
-    load_tw<(1 << SS)>(w, tw, (1 << s) + ((tid >> LO) << SS));
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      if (e & half) continue;
+    for (int g = 0; g < (G::E >> KB); ++g) {
+      const int o = (g << G::LOGT) | tid;
+      // twiddles in chunks of TWC pairs, loaded just before their butterflies
+      constexpr int TWC = (1 << SS) < TW_CHUNK ? (1 << SS) : TW_CHUNK;
 #pragma unroll
-      for (int r = 0; r < NR; ++r) bfly_fwd(x[r * E + e], x[r * E + (e | half)], w[e >> (KB - SS)], p, p2);
+      for (int tc = 0; tc < (1 << SS); tc += TWC) {
+        uint2 w[TWC];
+        load_tw<TWC>(w, tw, (1 << s) + ((o >> LO) << SS) + tc);
+#pragma unroll
+        for (int el = tc << (KB - SS); el < (tc + TWC) << (KB - SS); ++el) {
+          if (el & half) continue;
+          const int e = (g << KB) | el;
+#pragma unroll
+          for (int r = 0; r < NR; ++r) bfly_fwd(x[r * G::E + e], x[r * G::E + (e | half)], w[(el >> (KB - SS)) - tc], p, p2);
+        }
+      }
     }
-    fwd_stage<G, LO, SS + 1, NR>(x, tw, p, tid);
+    fwd_stage<G, LO, KB, SS + 1, NR>(x, tw, p, tid);
   }
 }
 
-// inverse (GS) stage SS of a radix-E pass (SS descending = bits ascending);
-// values in [0, 2p)
-template <class G, int LO, int SS, int NR>
+// inverse (GS) stage SS of a pass (SS descending = bits ascending); values
+// in [0, 2p)
+template <class G, int LO, int KB, int SS, int NR>
 DI void inv_stage(uint32_t* x, const uint2* __restrict__ itw, uint32_t p, int tid) {
-  constexpr int KB = G::LOGE;
   if constexpr (SS >= 0) {
-    constexpr int E = G::E;
     constexpr int bpos = LO + KB - 1 - SS;
     constexpr int s = G::LOGN - 1 - bpos;
     constexpr int half = 1 << (KB - 1 - SS);
     const uint32_t p2 = 2 * p;
-    uint2 w[1 << SS];
-    load_tw<(1 << SS)>(w, itw, (1 << s) + ((tid >> LO) << SS));
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      if (e & half) continue;
+    for (int g = 0; g < (G::E >> KB); ++g) {
+      const int o = (g << G::LOGT) | tid;
+      // twiddles in chunks of TWC pairs, loaded just before their butterflies
+      constexpr int TWC = (1 << SS) < TW_CHUNK ? (1 << SS) : TW_CHUNK;
 #pragma unroll
-      for (int r = 0; r < NR; ++r) bfly_inv(x[r * E + e], x[r * E + (e | half)], w[e >> (KB - SS)], p, p2);
+      for (int tc = 0; tc < (1 << SS); tc += TWC) {
+        uint2 w[TWC];
+        load_tw<TWC>(w, itw, (1 << s) + ((o >> LO) << SS) + tc);
+#pragma unroll
+        for (int el = tc << (KB - SS); el < (tc + TWC) << (KB - SS); ++el) {
+          if (el & half) continue;
+          const int e = (g << KB) | el;
+#pragma unroll
+          for (int r = 0; r < NR; ++r) bfly_inv(x[r * G::E + e], x[r * G::E + (e | half)], w[(el >> (KB - SS)) - tc], p, p2);
+        }
+      }
     }
-    inv_stage<G, LO, SS - 1, NR>(x, itw, p, tid);
+    inv_stage<G, LO, KB, SS - 1, NR>(x, itw, p, tid);
   }
 }
 
@@ -212,36 +271,53 @@ DI int shfl_tw_index(int tid, int e, int b) {
   return (1 << (G::LOGN - 1 - b)) + (j >> (b + 1));
 }
 
-template <class G, int B>
-DI void load_shfl_tw(uint2* w, const uint2* __restrict__ tw, int tid) {
+// Twiddles of the shuffle stage at bit B for registers [e0, e0 + CNT) of
+// this lane (every lane loads only the half it multiplies with).
+template <class G, int B, int CNT>
+DI void load_shfl_tw(uint2* w, const uint2* __restrict__ tw, int tid, int e0) {
   if constexpr (B == G::REM - 1) {
-    // consecutive in e: one aligned vector of E pairs
-    load_tw<G::E>(w, tw, shfl_tw_index<G>(tid, 0, B));
+    // consecutive in e: aligned vectors
+    load_tw<CNT>(w, tw, shfl_tw_index<G>(tid, 0, B) + e0);
   } else {
 #pragma unroll
-    for (int e = 0; e < G::E; ++e) w[e] = __ldg(&tw[shfl_tw_index<G>(tid, e, B)]);
+    for (int k = 0; k < CNT; ++k) w[k] = __ldg(&tw[shfl_tw_index<G>(tid, e0 + k, B)]);
   }
 }
 
-// forward butterflies on the REM lowest bits through warp shuffles
+// Butterflies on the REM lowest bits through warp shuffles.  Lanes L and U =
+// L ^ 2^B hold the two operands of every butterfly in the same register e;
+// L computes the butterflies of e < E/2 and U those of e >= E/2 (one shuffle
+// brings the partner operand, one returns the partner result), so every
+// modular product is computed once.
 template <class G, int B, int NR>
 DI void fwd_shfl(uint32_t* x, const uint2* __restrict__ tw, uint32_t p, int tid) {
   if constexpr (B >= 0) {
+    constexpr int H = G::E / 2;
+    constexpr int C = H < TW_CHUNK ? H : TW_CHUNK;
     const uint32_t p2 = 2 * p;
     const bool upper = (tid >> B) & 1;
-    uint2 w[G::E];
-    load_shfl_tw<G, B>(w, tw, tid);
+    const int off = upper ? H : 0;
 #pragma unroll
-    for (int e = 0; e < G::E; ++e) {
+    for (int c0 = 0; c0 < H; c0 += C) {
+      uint2 w[C];
+      load_shfl_tw<G, B, C>(w, tw, tid, c0 + off);
 #pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        const uint32_t v = x[r * G::E + e];
-        const uint32_t u = __shfl_xor_sync(0xffffffffu, v, 1 << B);
-        uint32_t X = upper ? u : v;
-        const uint32_t Y = upper ? v : u;
-        X = umin32(X, X - p2);
-        const uint32_t Tt = mul_shoup_lazy(Y, w[e].x, w[e].y, p);
-        x[r * G::E + e] = upper ? X - Tt + p2 : X + Tt;
+      for (int k = 0; k < C; ++k) {
+        const int e = c0 + k;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          uint32_t& lo = x[r * G::E + e];
+          uint32_t& hi = x[r * G::E + e + H];
+          const uint32_t got = __shfl_xor_sync(0xffffffffu, upper ? lo : hi, 1 << B);
+          uint32_t X = upper ? got : lo;   // L: own e, U: L's e+H
+          const uint32_t Y = upper ? hi : got;
+          X = umin32(X, X - p2);
+          const uint32_t Tt = mul_shoup_lazy(Y, w[k].x, w[k].y, p);
+          const uint32_t A = X + Tt, Bv = X - Tt + p2;  // results for L, U
+          const uint32_t back = __shfl_xor_sync(0xffffffffu, upper ? A : Bv, 1 << B);
+          lo = upper ? back : A;
+          hi = upper ? Bv : back;
+        }
       }
     }
     fwd_shfl<G, B - 1, NR>(x, tw, p, tid);
@@ -251,20 +327,32 @@ DI void fwd_shfl(uint32_t* x, const uint2* __restrict__ tw, uint32_t p, int tid)
 template <class G, int B, int NR>
 DI void inv_shfl(uint32_t* x, const uint2* __restrict__ itw, uint32_t p, int tid) {
   if constexpr (B < G::REM) {
+    constexpr int H = G::E / 2;
+    constexpr int C = H < TW_CHUNK ? H : TW_CHUNK;
     const uint32_t p2 = 2 * p;
     const bool upper = (tid >> B) & 1;
-    uint2 w[G::E];
-    load_shfl_tw<G, B>(w, itw, tid);
+    const int off = upper ? H : 0;
 #pragma unroll
-    for (int e = 0; e < G::E; ++e) {
+    for (int c0 = 0; c0 < H; c0 += C) {
+      uint2 w[C];
+      load_shfl_tw<G, B, C>(w, itw, tid, c0 + off);
 #pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        const uint32_t v = x[r * G::E + e];
-        const uint32_t u = __shfl_xor_sync(0xffffffffu, v, 1 << B);
-        const uint32_t X = upper ? u : v;
-        const uint32_t Y = upper ? v : u;
-        const uint32_t U = X + Y;
-        x[r * G::E + e] = upper ? mul_shoup_lazy(X - Y + p2, w[e].x, w[e].y, p) : umin32(U, U - p2);
+      for (int k = 0; k < C; ++k) {
+        const int e = c0 + k;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          uint32_t& lo = x[r * G::E + e];
+          uint32_t& hi = x[r * G::E + e + H];
+          const uint32_t got = __shfl_xor_sync(0xffffffffu, upper ? lo : hi, 1 << B);
+          const uint32_t X = upper ? got : lo;
+          const uint32_t Y = upper ? hi : got;
+          const uint32_t U = X + Y;
+          const uint32_t A = umin32(U, U - p2);
+          const uint32_t Bv = mul_shoup_lazy(X - Y + p2, w[k].x, w[k].y, p);
+          const uint32_t back = __shfl_xor_sync(0xffffffffu, upper ? A : Bv, 1 << B);
+          lo = upper ? back : A;
+          hi = upper ? Bv : back;
+        }
       }
     }
     inv_shfl<G, B + 1, NR>(x, itw, p, tid);
@@ -293,20 +381,25 @@ DI void post_transform() {
   if constexpr (G::FWD_EXCHANGES > 0 && (!G::dbl(NR) || (G::FWD_EXCHANGES & 1))) __syncthreads();
 }
 
-template <class G, int LO, int NR>
+// The pass maps are bit permutations of (e, tid), so an element's padded slot
+// splits into a per-thread base plus a compile-time offset per register:
+// sidx(A | C) = sidx(A) + sidx(C) for disjoint bit sets A, C.
+template <class G, int P, int NR>
 DI void regs_to_smem(const uint32_t* x, uint32_t* b, int tid) {
+  uint32_t* bt = b + sidx(gpass_index<G, G::lo(P), G::kb(P)>(tid, 0));
 #pragma unroll
   for (int r = 0; r < NR; ++r)
 #pragma unroll
-    for (int e = 0; e < G::E; ++e) b[r * G::XW + sidx(pass_index<LO, G::LOGE>(tid, e))] = x[r * G::E + e];
+    for (int e = 0; e < G::E; ++e) bt[r * G::XW + sidx(gpass_index<G, G::lo(P), G::kb(P)>(0, e))] = x[r * G::E + e];
 }
 
-template <class G, int LO, int NR>
+template <class G, int P, int NR>
 DI void smem_to_regs(uint32_t* x, const uint32_t* b, int tid) {
+  const uint32_t* bt = b + sidx(gpass_index<G, G::lo(P), G::kb(P)>(tid, 0));
 #pragma unroll
   for (int r = 0; r < NR; ++r)
 #pragma unroll
-    for (int e = 0; e < G::E; ++e) x[r * G::E + e] = b[r * G::XW + sidx(pass_index<LO, G::LOGE>(tid, e))];
+    for (int e = 0; e < G::E; ++e) x[r * G::E + e] = bt[r * G::XW + sidx(gpass_index<G, G::lo(P), G::kb(P)>(0, e))];
 }
 
 template <class G, int P, int NR>
@@ -315,11 +408,11 @@ DI void fwd_from(uint32_t* x, uint32_t* s, const uint2* __restrict__ tw, uint32_
     if constexpr (P > 0) {
       uint32_t* b = xbuf<G, NR>(s, P - 1);  // exchange P-1
       pre_exchange<G, NR>();
-      regs_to_smem<G, G::lo(P - 1), NR>(x, b, tid);
+      regs_to_smem<G, P - 1, NR>(x, b, tid);
       __syncthreads();
-      smem_to_regs<G, G::lo(P), NR>(x, b, tid);
+      smem_to_regs<G, P, NR>(x, b, tid);
     }
-    fwd_stage<G, G::lo(P), 0, NR>(x, tw, p, tid);
+    fwd_stage<G, G::lo(P), G::kb(P), 0, NR>(x, tw, p, tid);
     fwd_from<G, P + 1, NR>(x, s, tw, p, tid);
   }
 }
@@ -332,11 +425,11 @@ DI void inv_from(uint32_t* x, uint32_t* s, const uint2* __restrict__ itw, uint32
       constexpr int XI = (G::REG_TAIL ? 1 : 0) + (G::NFULL - 2 - P);
       uint32_t* b = xbuf<G, NR>(s, XI);
       pre_exchange<G, NR>();
-      regs_to_smem<G, G::lo(P + 1), NR>(x, b, tid);
+      regs_to_smem<G, P + 1, NR>(x, b, tid);
       __syncthreads();
-      smem_to_regs<G, G::lo(P), NR>(x, b, tid);
+      smem_to_regs<G, P, NR>(x, b, tid);
     }
-    inv_stage<G, G::lo(P), G::LOGE - 1, NR>(x, itw, p, tid);
+    inv_stage<G, G::lo(P), G::kb(P), G::kb(P) - 1, NR>(x, itw, p, tid);
     inv_from<G, P - 1, NR>(x, s, itw, p, tid);
   }
 }
@@ -350,7 +443,8 @@ DI int natural_index(int tid, int e) { return e * G::T + tid; }
 
 template <class G>
 DI int spectral_index(int tid, int e) {
-  if constexpr (G::REG_TAIL) return tail_index<G>(tid, e);
+  if constexpr (G::MIXED) return gpass_index<G, 0, G::kb(G::NFULL - 1)>(tid, e);
+  else if constexpr (G::REG_TAIL) return tail_index<G>(tid, e);
   else return pass_index<G::REM, G::LOGE>(tid, e);
 }
 

@@ -20,7 +20,7 @@ struct NttLaunch {
   cudaStream_t stream;
   dim3 grid;
   NttTabs nt;
-  int variant;  // radix of the fused kernels: 0 = default, 4 or 5 = log2 E
+  int variant;  // geometry flags of the fused kernels (RELIN_SINGLE, TENSOR_MIXED, MIXED_PASSES)
   // rows
   uint32_t* rows;
   int limbs, prime_off, inverse;
@@ -38,14 +38,6 @@ struct NttLaunch {
   const uint32_t* pk;
   const uint2* delta;
 };
-
-// Montgomery product x * k' * 2^-32 mod p in [0, 2p) for x, k' < p < 2^30;
-// pinv = -p^-1 mod 2^32.  With k' = k 2^32 mod p this is x * k mod p.
-DI uint32_t mont_mul(uint32_t x, uint32_t kp, uint32_t p, uint32_t pinv) {
-  const uint64_t z = (uint64_t)x * kp;
-  const uint32_t m = (uint32_t)z * pinv;
-  return (uint32_t)((z + (uint64_t)m * p) >> 32);
-}
 
 template <class G>
 DI void load_natural(uint32_t* x, const uint32_t* __restrict__ row, int tid) {
@@ -133,10 +125,8 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
   const size_t ct = blockIdx.y;
   const int L = K + KP;
   const uint32_t p = nt.prime[j];
-  const uint64_t mu = nt.mu[j];
   const uint2* tw = nt.tw + (size_t)j * G::N;
   const uint2* itw = nt.itw + (size_t)j * G::N;
-  const uint2 ninv = nt.ninv[j];
   auto row_of = [&](const uint32_t* base, const uint32_t* ext, int part) -> const uint32_t* {
     return j < K ? base + ((ct * 2 + part) * K + j) * G::N
                  : ext + ((ct * 2 + part) * KP + (j - K)) * G::N;
@@ -144,6 +134,11 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
   uint32_t* o0 = d + ((ct * 3 + 0) * L + j) * G::N;
   uint32_t* o1 = d + ((ct * 3 + 1) * L + j) * G::N;
   uint32_t* o2 = d + ((ct * 3 + 2) * L + j) * G::N;
+  // pointwise products are Montgomery products (x y 2^-32, in [0, 2p)); the
+  // inverse transforms multiply by N^-1 2^32 instead of N^-1
+  const uint32_t pinv = nt.pinv[j];
+  const uint32_t p2 = 2 * p;
+  const uint2 ninv = nt.ninv_m[j];
   uint32_t x[2 * E], y[2 * E];
   if (square) {
     // x = (A0 | A1)
@@ -153,10 +148,10 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const uint32_t a0 = x[e], a1 = x[E + e];
-      const uint32_t c = mul_mod(a0, a1, p, mu);
-      x[e] = mul_mod(a0, a0, p, mu);
-      x[E + e] = add_mod(c, c, p);
-      y[e] = mul_mod(a1, a1, p, mu);
+      const uint32_t c = mont_mul(a0, a1, p, pinv);
+      x[e] = mont_mul(a0, a0, p, pinv);
+      x[E + e] = umin32(2 * c, 2 * c - p2);
+      y[e] = mont_mul(a1, a1, p, pinv);
     }
   } else {
     // x = (A0 | B0), y = (A1 | B1)
@@ -169,9 +164,10 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const uint32_t a0 = x[e], b0 = x[E + e], a1 = y[e], b1 = y[E + e];
-      x[e] = mul_mod(a0, b0, p, mu);
-      x[E + e] = add_mod(mul_mod(a0, b1, p, mu), mul_mod(a1, b0, p, mu), p);
-      y[e] = mul_mod(a1, b1, p, mu);
+      x[e] = mont_mul(a0, b0, p, pinv);
+      // a0 b1 + a1 b0 < 2 p^2 < 2^32 p: one reduction
+      x[E + e] = redc64((uint64_t)a0 * b1 + (uint64_t)a1 * b0, p, pinv);
+      y[e] = mont_mul(a1, b1, p, pinv);
     }
   }
   ntt_inv_pair<G>(x, s, itw, p, ninv, tid);
@@ -181,6 +177,57 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
     o1[natural_index<G>(tid, e)] = x[E + e];
   }
   inv_store<G>(y, s, itw, p, ninv, tid, o2);
+}
+
+// Square tensor for MIXED geometries (T = N/32 threads, two CTAs per SM): one
+// row in registers at a time; A0 and then d0, d1 wait in shared memory
+// (thread-owned slots e*T + tid) behind the single exchange buffer.
+template <class G>
+constexpr int tensor_sq_smem_words() { return G::ntt_smem_words(1) + 2 * G::N; }
+
+template <class G>
+__global__ void __launch_bounds__(G::T, 2)
+    k_tensor_sq(const uint32_t* __restrict__ a, const uint32_t* __restrict__ a_ext,
+                uint32_t* __restrict__ d, int K, int KP, NttTabs nt) {
+  extern __shared__ __align__(16) uint32_t s[];
+  constexpr int E = G::E;
+  const int tid = threadIdx.x;
+  const int j = blockIdx.x;
+  const size_t ct = blockIdx.y;
+  const int L = K + KP;
+  const uint32_t p = nt.prime[j];
+  const uint32_t pinv = nt.pinv[j];
+  const uint32_t p2 = 2 * p;
+  const uint2* tw = nt.tw + (size_t)j * G::N;
+  const uint2* itw = nt.itw + (size_t)j * G::N;
+  const uint2 ninv = nt.ninv_m[j];
+  uint32_t* st0 = s + G::ntt_smem_words(1);
+  uint32_t* st1 = st0 + G::N;
+  auto row_of = [&](int part) -> const uint32_t* {
+    return j < K ? a + ((ct * 2 + part) * K + j) * G::N : a_ext + ((ct * 2 + part) * KP + (j - K)) * G::N;
+  };
+  uint32_t x[E];
+  load_natural<G>(x, row_of(0), tid);
+  ntt_fwd<G>(x, s, tw, p, tid);
+#pragma unroll
+  for (int e = 0; e < E; ++e) st0[e * G::T + tid] = x[e];
+  load_natural<G>(x, row_of(1), tid);
+  ntt_fwd<G>(x, s, tw, p, tid);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t a0 = st0[e * G::T + tid], a1 = x[e];
+    const uint32_t c = mont_mul(a0, a1, p, pinv);
+    st0[e * G::T + tid] = mont_mul(a0, a0, p, pinv);
+    st1[e * G::T + tid] = umin32(2 * c, 2 * c - p2);
+    x[e] = mont_mul(a1, a1, p, pinv);
+  }
+  inv_store<G>(x, s, itw, p, ninv, tid, d + ((ct * 3 + 2) * L + j) * G::N);
+#pragma unroll
+  for (int e = 0; e < E; ++e) x[e] = st0[e * G::T + tid];
+  inv_store<G>(x, s, itw, p, ninv, tid, d + ((ct * 3 + 0) * L + j) * G::N);
+#pragma unroll
+  for (int e = 0; e < E; ++e) x[e] = st1[e * G::T + tid];
+  inv_store<G>(x, s, itw, p, ninv, tid, d + ((ct * 3 + 1) * L + j) * G::N);
 }
 
 // Relinearisation configuration of a geometry: NR digit rows transformed in
@@ -285,6 +332,29 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
       for (int e = 0; e < R * E; ++e) x[e] = reduce64(x[e], p, mu);
     }
     ntt_fwd<G, R>(x, s, tw, p, tid);
+    if constexpr (!ACC64 && R == 2) {
+      // both digits' products summed in 64 bits (< 2 p^2 < 2^32 p), one
+      // Montgomery reduction per pair; keys streamed 16 bytes at a time
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        Acc* acc = part ? acc1 : acc0;
+        const uint4* k0 = reinterpret_cast<const uint4*>(krow(i, part)) + tid;
+        const uint4* k1 = reinterpret_cast<const uint4*>(krow(i + 1, part)) + tid;
+#pragma unroll
+        for (int c = 0; c < E / 4; ++c) {
+          const uint4 u = __ldg(&k0[c * G::T]);
+          const uint4 v = __ldg(&k1[c * G::T]);
+          const uint32_t ku[4] = {u.x, u.y, u.z, u.w}, kv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int l = 0; l < 4; ++l) {
+            const int e = 4 * c + l;
+            const uint32_t m = redc64((uint64_t)x[e] * ku[l] + (uint64_t)x[E + e] * kv[l], p, pinv);
+            const uint32_t sum = (uint32_t)acc[e] + m;
+            acc[e] = umin32(sum, sum - p2);
+          }
+        }
+      }
+    } else {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
 #pragma unroll
@@ -302,6 +372,7 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
           }
         }
       }
+    }
     }
     if constexpr (ACC64) {
       // a reduced value plus 16 products of (p-1)^2 stays below 2^64
@@ -503,19 +574,32 @@ cudaError_t launch_with(int op, const NttLaunch& a) {
   return cudaGetLastError();
 }
 
+// variant bit: square tensors through k_tensor_sq on the MIXED radix-32
+// geometry (two CTAs per SM); independent of the relinearisation key layout
+constexpr int TENSOR_MIXED = 32;
+// variant bit: every fused kernel on the MIXED geometry of the default radix
+// (passes of unequal width instead of a warp-shuffle tail)
+constexpr int MIXED_PASSES = 64;
+
+template <class G>
+cudaError_t launch_tensor_sq(const NttLaunch& a) {
+  static bool configured = false;
+  constexpr int smem = tensor_sq_smem_words<G>() * sizeof(uint32_t);
+  if (!configured) {
+    cudaFuncSetAttribute(k_tensor_sq<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
+  }
+  k_tensor_sq<G><<<a.grid, G::T, smem, a.stream>>>(a.a, a.ae, a.d, a.K, a.KP, a.nt);
+  return cudaGetLastError();
+}
+
 // The key layout (tiled, Montgomery or not) follows the geometry and the
 // relinearisation kernel, so keys are laid out per variant.
 template <int LOGN>
 cudaError_t ntt_launch(int op, const NttLaunch& a) {
-  const int loge = a.variant & 15;
-  if constexpr (LOGN >= 10 && LOGN <= 13 && pick_loge(LOGN) != 3) {
-    if (loge == 3) return launch_with<NttGeom<LOGN, 3>>(op, a);
-  }
-  if constexpr (LOGN >= 10 && pick_loge(LOGN) != 5) {
-    if (loge == 5) return launch_with<NttGeom<LOGN, 5>>(op, a);
-  }
-  if constexpr (LOGN >= 10 && pick_loge(LOGN) != 4) {
-    if (loge == 4) return launch_with<NttGeom<LOGN, 4>>(op, a);
+  if constexpr (LOGN >= 10) {
+    if (op == 1 && a.square && (a.variant & TENSOR_MIXED)) return launch_tensor_sq<NttGeom<LOGN, 5, false, true>>(a);
+    if (a.variant & MIXED_PASSES) return launch_with<NttGeom<LOGN, pick_loge(LOGN), false, true>>(op, a);
   }
   return launch_with<NttGeom<LOGN>>(op, a);
 }
@@ -523,16 +607,12 @@ cudaError_t ntt_launch(int op, const NttLaunch& a) {
 template <class G>
 int mont_of(int v) { return relin_acc64<G>((v & RELIN_SINGLE) != 0) ? 0 : 1; }
 
+
 // does variant v use Montgomery-form rlk?
 template <int LOGN>
 int ntt_variant_mont(int v) {
-  const int loge = v & 15;
-  if constexpr (LOGN >= 10 && LOGN <= 13) {
-    if (loge == 3) return mont_of<NttGeom<LOGN, 3>>(v);
-  }
   if constexpr (LOGN >= 10) {
-    if (loge == 5) return mont_of<NttGeom<LOGN, 5>>(v);
-    if (loge == 4) return mont_of<NttGeom<LOGN, 4>>(v);
+    if (v & MIXED_PASSES) return mont_of<NttGeom<LOGN, pick_loge(LOGN), false, true>>(v);
   }
   return mont_of<NttGeom<LOGN>>(v);
 }

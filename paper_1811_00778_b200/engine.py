@@ -144,7 +144,7 @@ class GpuContext:
         return torch.empty((n, parts, self.K, self.N), dtype=torch.int32, device=f"cuda:{self.device}")
 
     def set_variant(self, variant: int):
-        """NTT radix variant of the fused kernels (0 default, 4 or 5)."""
+        """Geometry flags of the fused kernels (0 default; 16 one-row relinearisation, 32 radix-32 square tensor, 64 mixed-width passes)."""
         _lib.check(_lib.lib().hcnn_ctx_set_option(self.handle, 1, int(variant)), "ntt variant")
 
     def profile(self, enable: bool):
