@@ -291,8 +291,9 @@ def run_ours(args):
         h = torch.empty(u["gin"].data.shape, dtype=torch.int32, pin_memory=True)
         h.copy_(u["gin"].data)
         host_in.append(h)
-    host_out = [torch.empty(o.data.shape, dtype=torch.int32, pin_memory=True) for o in outs]
-    e2e_steps = max(2, min(args.steps, 5))
+    e2e_steps = max(3, args.steps)
+    host_out = [[torch.empty(o.data.shape, dtype=torch.int32, pin_memory=True) for _ in range(e2e_steps)]
+                for o in outs]
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -300,12 +301,10 @@ def run_ours(args):
     e1 = torch.cuda.Event(enable_timing=True)
     w0 = time.perf_counter()
     e0.record(stream)
-    for _ in range(e2e_steps):
-        xs = [E.GpuCipherTensor(u["gin"].shape, h.to("cuda", non_blocking=True), u["gin"].delta,
-                                u["gin"].channel_modulus, u["params"]) for u, h in zip(units, host_in)]
-        os_ = step(xs)
-        for ho, o in zip(host_out, os_):
-            ho.copy_(o.data, non_blocking=True)
+    for u, h, ho in zip(units, host_in, host_out):
+        # public serving API: uploads of step s+1 overlap the evaluation of step s
+        E.eval_network_stream([h] * e2e_steps, u["model"], u["rlk"], u["params"], u["gin"].shape,
+                              u["gin"].delta, E.OpCounter(), outputs=ho)
     e1.record(stream)
     torch.cuda.synchronize()
     wall_e2e = (time.perf_counter() - w0) / e2e_steps
@@ -380,7 +379,7 @@ def run_ours(args):
     images = W["images_per_step"]
     value = images / (ms / 1e3)
     in_bytes = int(sum(h.numel() for h in host_in) * 4)
-    out_bytes = int(sum(h.numel() for h in host_out) * 4)
+    out_bytes = int(sum(ho[0].numel() for ho in host_out) * 4)
     c0 = counters[0]
     line = {
         "metric": METRIC,
@@ -410,7 +409,7 @@ def run_ours(args):
         "e2e": {"value": round(images / (e2e_ms / 1e3), 2), "unit": "images/s",
                 "ms_per_step": round(e2e_ms, 3), "wall_ms_per_step": round(wall_e2e * 1e3, 3),
                 "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": out_bytes,
-                "path": "pinned host u32 ciphertexts -> engine.eval_network -> pinned host logits"},
+                "path": "pinned host u32 ciphertexts -> engine.eval_network_stream (upload of step s+1 overlaps evaluation of step s; two device input buffers) -> pinned host logits", "steps": e2e_steps},
         "gpu_launches": int(launches),
         "kernels": kernels,
         "roofline": roof,

@@ -35,7 +35,8 @@ enum {
   HCNN_ERR_CAPACITY = 3,    /* CapacityError (engine.py:109-112) */
   HCNN_ERR_UNSUPPORTED = 4, /* UnsupportedParametersError (presets.py:72-88) */
   HCNN_ERR_CUDA = 5,        /* device / runtime failure */
-  HCNN_ERR_DOMAIN = 6       /* DomainError (ring.py:147-163) */
+  HCNN_ERR_DOMAIN = 6,      /* DomainError (ring.py:147-163) */
+  HCNN_ERR_FORMAT = 7       /* FormatError (serial.py:53-72) */
 };
 
 enum { HCNN_DOMAIN_COEFF = 0, HCNN_DOMAIN_REF_NTT = 1 };
@@ -143,6 +144,17 @@ int hcnn_hmult_raw(hcnn_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t
 int hcnn_hmult(hcnn_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, size_t n);
 /* 3-part -> 2-part key switch: bfv.relinearize (bfv.py:368-404). */
 int hcnn_relinearize(hcnn_ctx* ctx, const uint32_t* in3, uint32_t* out, size_t n);
+/* HFIR element bodies (serial.py:87-97: u64 LE, position-major then prime)
+ * <-> device ciphertext rows.  rows = ciphertexts x parts; `hfir` is a DEVICE
+ * buffer of rows * N * K u64.  unpack returns HCNN_ERR_FORMAT if a residue is
+ * not below its prime (the device store keeps canonical residues only). */
+int hcnn_hfir_pack(hcnn_ctx* ctx, const uint32_t* rows_in, size_t rows, uint64_t* hfir);
+int hcnn_hfir_unpack(hcnn_ctx* ctx, const uint64_t* hfir, size_t rows, uint32_t* rows_out);
+/* ct x plaintext polynomial for n cts: bfv.hmult_plain (bfv.py:301-318).
+ * pt: HOST pointer to the N centred plaintext coefficients (Plaintext.centered()).
+ * A constant plaintext takes the scalar path (poly_mul_scalar, ring.py:193-196),
+ * any other the NTT path; both equal the reference bit for bit. */
+int hcnn_mul_plain(hcnn_ctx* ctx, const uint32_t* cts, const int64_t* pt, uint32_t* out, size_t n);
 /* Elementwise add of two ct tensors: bfv.hadd (bfv.py:264-274). */
 int hcnn_hadd(hcnn_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, size_t n);
 /* In-place NTT of n_rows rows of N residues; row r uses prime

@@ -318,6 +318,21 @@ def hsquare(pr: Params, c, rlk_ntt) -> tuple:
     return relinearize(pr, hmult_raw(pr, c), rlk_ntt)
 
 
+def hmult_plain(pr: Params, c, poly: np.ndarray) -> tuple:
+    """Ciphertext times plaintext (bfv.py:301-318): the plaintext is lifted at
+    its centred representative (bfv.py:110-112); a constant takes the scalar
+    path (ring.py:193-196), anything else NTT(part) * NTT(lift) -> INTT."""
+    ctx = pr.ctx
+    t = pr.t
+    poly = np.asarray(poly, dtype=np.int64)
+    centered = np.where(poly > t // 2, poly - t, poly)
+    if not centered[1:].any():
+        return tuple(mul_scalar(ctx, part, int(centered[0])) for part in c)
+    lifted = centered[None, :] % ctx.mods
+    lf = ntt_forward(ctx, lifted)
+    return tuple(ntt_inverse(ctx, ntt_forward(ctx, np.asarray(part, dtype=np.int64)) * lf % ctx.mods) for part in c)
+
+
 # ---------------------------------------------------------------------------
 # client side: keys, encryption, decryption (bfv.py:164-250), used only to
 # cross-check the product's host client and to decrypt in tests

@@ -280,11 +280,23 @@ class BfvParams:
 
 @dataclass
 class Plaintext:
+    """Polynomial with coefficients in [0, t) (bfv.py:95-112)."""
+
     poly: np.ndarray
     t: int
 
     def __post_init__(self):
         self.poly = np.asarray(self.poly, dtype=np.int64)
+
+    @staticmethod
+    def constant(value: int, params) -> "Plaintext":
+        poly = np.zeros(params.ring_degree, dtype=np.int64)
+        poly[0] = value % params.t
+        return Plaintext(poly, params.t)
+
+    def centered(self) -> np.ndarray:
+        half = self.t // 2
+        return np.where(self.poly > half, self.poly - self.t, self.poly)
 
 
 @dataclass

@@ -1344,6 +1344,84 @@ int hcnn_relinearize(hcnn_ctx* c, const uint32_t* in3, uint32_t* out, size_t n) 
   });
 }
 
+int hcnn_hfir_pack(hcnn_ctx* c, const uint32_t* rows_in, size_t rows, uint64_t* hfir) {
+  return guarded([&] {
+    c->mark();
+    CK(cudaSetDevice(c->device));
+    const size_t total = rows * c->N;
+    if (!total) return;
+    k_hfir_pack<<<cdiv(total, 256), 256, 0, c->stream>>>(rows_in, hfir, (int)c->K, (int)c->N, rows);
+    c->launched("k_hfir_pack");
+  });
+}
+
+int hcnn_hfir_unpack(hcnn_ctx* c, const uint64_t* hfir, size_t rows, uint32_t* rows_out) {
+  return guarded([&] {
+    c->mark();
+    CK(cudaSetDevice(c->device));
+    const size_t total = rows * c->N;
+    if (!total) return;
+    int* bad = nullptr;
+    CK(cudaMallocAsync((void**)&bad, sizeof(int), c->stream));
+    CK(cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
+    k_hfir_unpack<<<cdiv(total, 256), 256, 0, c->stream>>>(hfir, rows_out, (int)c->K, (int)c->N, rows,
+                                                            c->d_prime, bad);
+    c->launched("k_hfir_unpack");
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaFreeAsync(bad, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (h) fail(HCNN_ERR_FORMAT, "residue not reduced modulo its prime");
+  });
+}
+
+int hcnn_mul_plain(hcnn_ctx* c, const uint32_t* cts, const int64_t* pt, uint32_t* out, size_t n) {
+  return guarded([&] {
+    c->mark();
+    CK(cudaSetDevice(c->device));
+    if (!n) return;
+    const size_t N = c->N, K = c->K;
+    bool constant = true;
+    for (size_t i = 1; i < N && constant; ++i) constant = pt[i] == 0;
+    if (constant) {  // scalar fast path (bfv.py:311-314)
+      std::vector<uint32_t> sres(K);
+      for (size_t i = 0; i < K; ++i) {
+        const int64_t p = (int64_t)c->primes[i];
+        int64_t r = pt[0] % p;
+        sres[i] = (uint32_t)(r < 0 ? r + p : r);
+      }
+      uint32_t* d_s = nullptr;
+      CK(cudaMallocAsync((void**)&d_s, K * sizeof(uint32_t), c->stream));
+      CK(cudaMemcpyAsync(d_s, sres.data(), K * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+      const size_t total = n * 2 * K * N;
+      k_mul_scalar<<<cdiv(total, 256), 256, 0, c->stream>>>(cts, out, d_s, (int)K, (int)N, total, c->d_prime,
+                                                             c->d_mu);
+      c->launched("k_mul_scalar");
+      CK(cudaFreeAsync(d_s, c->stream));
+      CK(cudaStreamSynchronize(c->stream));  // sres is a host temporary
+      return;
+    }
+    int64_t* d_pt = nullptr;
+    uint32_t* rows = nullptr;
+    CK(cudaMallocAsync((void**)&d_pt, N * sizeof(int64_t), c->stream));
+    CK(cudaMallocAsync((void**)&rows, K * N * sizeof(uint32_t), c->stream));
+    CK(cudaMemcpyAsync(d_pt, pt, N * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    k_lift_plain<<<cdiv(N, 256), 256, 0, c->stream>>>(d_pt, rows, (int)N, (int)K, c->d_prime);
+    c->launched("k_lift_plain");
+    launch_ntt_rows(c, rows, K, (int)K, 0, 2);  // NTT domain, tiled layout
+    NttLaunch a{};
+    a.grid = dim3((unsigned)K, (unsigned)n);
+    a.a = cts;
+    a.b = rows;
+    a.out = out;
+    a.K = (int)K;
+    ntt_dispatch(c, 6, a, "k_mul_plain");
+    CK(cudaFreeAsync(d_pt, c->stream));
+    CK(cudaFreeAsync(rows, c->stream));
+    CK(cudaStreamSynchronize(c->stream));  // pt is caller-owned host memory
+  });
+}
+
 int hcnn_hadd(hcnn_ctx* c, const uint32_t* a, const uint32_t* b, uint32_t* out, size_t n) {
   return guarded([&] {
     c->mark();

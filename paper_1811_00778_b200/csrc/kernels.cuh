@@ -446,6 +446,55 @@ __global__ void k_reduce_weights(const int64_t* __restrict__ w, size_t n, uint32
   }
 }
 
+// device rows [r][K][N] u32 <-> HFIR element bodies [r][N][K] u64 (serial.py:87-97)
+__global__ void k_hfir_pack(const uint32_t* __restrict__ in, uint64_t* __restrict__ out, int K, int N,
+                            size_t rows) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;  // (row, n)
+  if (i >= rows * N) return;
+  const size_t r = i / N, n = i % N;
+  const uint32_t* src = in + r * K * N + n;
+  uint64_t* dst = out + i * K;
+  for (int k = 0; k < K; ++k) dst[k] = src[(size_t)k * N];
+}
+
+__global__ void k_hfir_unpack(const uint64_t* __restrict__ in, uint32_t* __restrict__ out, int K, int N,
+                              size_t rows, const uint32_t* __restrict__ primes, int* __restrict__ bad) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * N) return;
+  const size_t r = i / N, n = i % N;
+  const uint64_t* src = in + i * K;
+  uint32_t* dst = out + r * K * N + n;
+  for (int k = 0; k < K; ++k) {
+    const uint64_t v = src[k];
+    if (v >= primes[k]) atomicOr(bad, 1);
+    dst[(size_t)k * N] = (uint32_t)v;
+  }
+}
+
+// centred plaintext coefficients (int64) -> [K][N] residues mod q_i
+__global__ void k_lift_plain(const int64_t* __restrict__ pt, uint32_t* __restrict__ rows, int N, int K,
+                             const uint32_t* __restrict__ primes) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  const int64_t v = pt[n];
+  for (int i = 0; i < K; ++i) {
+    int64_t r = v % (int64_t)primes[i];
+    if (r < 0) r += primes[i];
+    rows[(size_t)i * N + n] = (uint32_t)r;
+  }
+}
+
+// out = in * (s mod q_i): the scalar path of hmult_plain (bfv.py:311-314,
+// ring.py:193-196); sres: [K] residues of the scalar
+__global__ void k_mul_scalar(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                             const uint32_t* __restrict__ sres, int K, int N, size_t total,
+                             const uint32_t* __restrict__ primes, const uint64_t* __restrict__ mus) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int limb = (int)((i / N) % K);
+  out[i] = mul_mod(in[i], sres[limb], primes[limb], mus[limb]);
+}
+
 // reference-order NTT (natural, a(psi^(2k+1))) -> device spectral order
 // in place on [rows][N] via a temp: dst[i] = src[brv(i)]
 __global__ void k_bitrev_rows(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, int N,

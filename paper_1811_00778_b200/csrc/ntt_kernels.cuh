@@ -6,6 +6,7 @@
 //   k_tensor        ct x ct tensor over Q u P: NTT, pointwise, INTT (bfv.py:331-347)
 //   k_relin         digit NTT x rlk MAC, INTT, + (y0, y1)          (bfv.py:368-404)
 //   k_encrypt       public-key encryption from host randomness     (bfv.py:201-216)
+//   k_mul_plain     ct x plaintext polynomial, NTT path           (bfv.py:301-318)
 //   k_ref_to_tiled  reference-order NTT keys -> device tiled layout
 #pragma once
 #include <type_traits>
@@ -177,6 +178,42 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
     o1[natural_index<G>(tid, e)] = x[E + e];
   }
   inv_store<G>(y, s, itw, p, ninv, tid, o2);
+}
+
+// Plaintext-polynomial product (bfv.py:301-318, NTT path): one CTA per (ct,
+// prime of q); a: [B][2][K][N]; pt: [K][N] NTT domain, tiled layout (plain
+// form; the Montgomery 2^-32 is undone by the N^-1 2^32 of the inverse).
+template <class G>
+__global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
+    k_mul_plain(const uint32_t* __restrict__ a, const uint32_t* __restrict__ pt,
+                uint32_t* __restrict__ out, int K, NttTabs nt) {
+  extern __shared__ uint32_t s[];
+  constexpr int E = G::E;
+  const int tid = threadIdx.x;
+  const int j = blockIdx.x;
+  const size_t ct = blockIdx.y;
+  const uint32_t p = nt.prime[j];
+  const uint32_t pinv = nt.pinv[j];
+  uint32_t x[2 * E];
+  load_natural<G>(x, a + ((ct * 2 + 0) * K + j) * G::N, tid);
+  load_natural<G>(x + E, a + ((ct * 2 + 1) * K + j) * G::N, tid);
+  ntt_fwd_pair<G>(x, s, nt.tw + (size_t)j * G::N, p, tid);
+  {
+    uint32_t k[E];
+    load_tiled<G>(k, pt + (size_t)j * G::N, tid);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      x[e] = mont_mul(x[e], k[e], p, pinv);
+      x[E + e] = mont_mul(x[E + e], k[e], p, pinv);
+    }
+  }
+  ntt_inv_pair<G>(x, s, nt.itw + (size_t)j * G::N, p, nt.ninv_m[j], tid);
+#pragma unroll
+  for (int part = 0; part < 2; ++part) {
+    uint32_t* o = out + ((ct * 2 + part) * K + j) * G::N;
+#pragma unroll
+    for (int e = 0; e < E; ++e) o[natural_index<G>(tid, e)] = x[part * E + e];
+  }
 }
 
 // Square tensor for MIXED geometries (T = N/32 threads, two CTAs per SM): one
@@ -522,6 +559,8 @@ void configure_smem() {
   cudaFuncSetAttribute(k_relin<G, relin_acc64<G>(true), 1>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, RelinSmem<G, 1>::BYTES);
   cudaFuncSetAttribute(k_encrypt<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_mul_plain<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       G::ntt_smem_words(pair_nr<G>()) * sizeof(uint32_t));
 }
 
 // variant: bits 0-3 = log2 E of the fused kernels (0 = default geometry);
@@ -567,6 +606,10 @@ cudaError_t launch_with(int op, const NttLaunch& a) {
       break;
     case 5:
       k_to_mont<G><<<a.grid, G::T, 0, a.stream>>>(a.rows, a.limbs, a.nt);
+      break;
+    case 6:
+      k_mul_plain<G><<<a.grid, G::T, G::ntt_smem_words(pair_nr<G>()) * sizeof(uint32_t), a.stream>>>(
+          a.a, a.b, a.out, a.K, a.nt);
       break;
     default:
       return cudaErrorInvalidValue;

@@ -173,16 +173,22 @@ class GpuContext:
             raise ParameterMismatchError("object does not match parameter set")
         if self._rlk_ref is not None and self._rlk_ref() is rlk:
             return
-        comps = rlk.components
-        if len(comps) != self.D:
-            raise ParameterMismatchError("relinearization key has the wrong digit count")
-        host = np.ascontiguousarray(
-            np.stack([np.stack([k0.residues, k1.residues]) for k0, k1 in comps]).astype(np.uint64)
-        )
-        domain = 1
-        first = comps[0][0]
-        if getattr(first, "domain", None) is not None and getattr(first.domain, "value", "ntt") != "ntt":
-            domain = 0
+        coeff = getattr(rlk, "coeff", None)  # hfir.DeviceRelinKey: serialised, coefficient domain
+        if coeff is not None:
+            if coeff.shape[0] != self.D:
+                raise ParameterMismatchError("relinearization key has the wrong digit count")
+            host, domain = np.ascontiguousarray(coeff, dtype=np.uint64), 0
+        else:
+            comps = rlk.components
+            if len(comps) != self.D:
+                raise ParameterMismatchError("relinearization key has the wrong digit count")
+            host = np.ascontiguousarray(
+                np.stack([np.stack([k0.residues, k1.residues]) for k0, k1 in comps]).astype(np.uint64)
+            )
+            domain = 1
+            first = comps[0][0]
+            if getattr(first, "domain", None) is not None and getattr(first.domain, "value", "ntt") != "ntt":
+                domain = 0
         self.bind_stream()
         _lib.check(_lib.lib().hcnn_set_relin_key(self.handle, host.ctypes.data, domain),
                    "hcnn_set_relin_key")
@@ -497,6 +503,72 @@ def eval_network(tensor, model, rlk, params, counter=None, workers: int = 1, cap
         if layer_hook is not None:
             layer_hook(layer.name, x)
     return _ret(x, was_host)
+
+
+def eval_network_stream(batches, model, rlk, params, shape, delta, counter=None, device=None,
+                        layer_hook=None, outputs=None):
+    """Serving loop over encrypted slot-batches held in (pinned) host memory.
+
+    Each batch is one `eval_network` (engine.py:400-423) on the GPU.  Batch
+    i+1's ciphertexts are uploaded on a copy stream into the second of two
+    device input buffers while batch i is evaluated (a buffer is released as
+    soon as the first layer has read it), and batch i's logits go back to
+    pinned host memory on a third stream as soon as its last layer is done.
+
+    batches: iterable of host int32 tensors [n_ct][2][K][N] (u32 residues,
+    (y, x, c) row-major like CipherTensor.cts), all of `shape`.
+    Returns the list of host int32 logit tensors [n_out][2][K][N] (written
+    into `outputs[i]` when given, else freshly pinned); they are complete when
+    the call returns.
+    """
+    counter = counter if counter is not None else OpCounter()
+    dev = torch.device("cuda", _device_index(device))
+    compute = torch.cuda.current_stream(dev)
+    up_stream = torch.cuda.Stream(dev)
+    down_stream = torch.cuda.Stream(dev)
+    up_stream.wait_stream(compute)
+    bufs, free, outs = [None, None], [None, None], []
+    for i, hb in enumerate(batches):
+        slot = i % 2
+        if tuple(hb.shape[1:]) != (2, len(params.ctx.primes), int(params.ctx.ring_degree)):
+            raise ParameterMismatchError("batch layout does not match params")
+        with torch.cuda.stream(up_stream):
+            if free[slot] is not None:
+                up_stream.wait_event(free[slot])
+            if bufs[slot] is None or bufs[slot].shape != hb.shape:
+                bufs[slot] = torch.empty(hb.shape, dtype=torch.int32, device=dev)
+            bufs[slot].copy_(hb, non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(up_stream)
+        compute.wait_event(ready)
+        x = GpuCipherTensor(shape, bufs[slot], delta, params.t, params)
+        released = torch.cuda.Event()
+        state = {"first": True}
+
+        def hook(name, t, _released=released, _state=state):
+            if _state["first"]:  # the first layer has consumed the input buffer
+                _released.record(compute)
+                _state["first"] = False
+            if layer_hook is not None:
+                layer_hook(name, t)
+
+        out = eval_network(x, model, rlk, params, counter, layer_hook=hook)
+        if state["first"]:
+            released.record(compute)
+        free[slot] = released
+        done = torch.cuda.Event()
+        done.record(compute)
+        host = outputs[i] if outputs is not None else torch.empty(out.data.shape, dtype=torch.int32,
+                                                                  pin_memory=True)
+        with torch.cuda.stream(down_stream):
+            down_stream.wait_event(done)
+            host.copy_(out.data, non_blocking=True)
+            out.data.record_stream(down_stream)
+        outs.append(host)
+    compute.wait_stream(down_stream)
+    compute.wait_stream(up_stream)
+    down_stream.synchronize()
+    return outs
 
 
 # ---------------------------------------------------------------- client side

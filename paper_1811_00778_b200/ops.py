@@ -5,6 +5,7 @@ plus batched device-tensor entry points used by tests and the microbench.
     hmult(c1, c2, rlk, params)       bfv.py:419-432
     hmult_raw(c1, c2, params)        bfv.py:407-416
     relinearize(parts3, rlk, params) bfv.py:368-404
+    hmult_plain(c, pt, params)       bfv.py:301-318
     hadd(c1, c2)                     bfv.py:264-274  (via params)
 """
 
@@ -15,7 +16,7 @@ import torch
 
 from . import _lib
 from .engine import GpuContext, context_for, _ptr
-from .errors import MissingKeyError, ParameterMismatchError
+from .errors import EncodingError, MissingKeyError, ParameterMismatchError
 
 
 def _check(params, fp):
@@ -96,7 +97,45 @@ def ntt_device(g: GpuContext, rows: torch.Tensor, limbs: int, prime_offset: int 
     return rows
 
 
+def mul_plain_device(g: GpuContext, x: torch.Tensor, centered) -> torch.Tensor:
+    """x [n][2][K][N] times the plaintext with centred coefficients `centered`."""
+    pt = np.ascontiguousarray(np.asarray(centered, dtype=np.int64).reshape(-1))
+    if pt.size != g.N:
+        raise ParameterMismatchError("plaintext length != ring degree")
+    out = g.empty(x.shape[0])
+    g.bind_stream()
+    _lib.check(_lib.lib().hcnn_mul_plain(g.handle, _ptr(x), pt.ctypes.data, _ptr(out), x.shape[0]),
+               "hcnn_mul_plain")
+    return out
+
+
 # ------------------------------------------------------------- per-ciphertext
+
+
+def hmult_plain(c, pt, params):
+    """Multiply by a plaintext lifted at its centred representative
+    (bfv.py:301-318): scalar path for constants, NTT path otherwise."""
+    _check(params, c.fingerprint)
+    if pt.t != params.t:
+        raise ParameterMismatchError("plaintext modulus mismatch")
+    poly = np.asarray(pt.poly)
+    if poly.shape != (params.ring_degree,):
+        raise EncodingError("plaintext length != ring degree")
+    if (poly < 0).any() or (poly >= params.t).any():
+        raise EncodingError("plaintext coefficient outside [0, t)")
+    half = params.t // 2
+    centered = np.where(poly > half, poly - params.t, poly)
+    g = context_for(params)
+    nparts = len(c.parts)
+    x = _stack([c], g, nparts).reshape(-1, g.K, g.N)
+    if nparts % 2:  # the kernel takes part pairs: pad a 3-part ct with a zero part
+        x = torch.cat([x, torch.zeros_like(x[:1])])
+    out = mul_plain_device(g, x.reshape(-1, 2, g.K, g.N), centered).reshape(-1, g.K, g.N)[:nparts]
+    torch.cuda.current_stream(out.device).synchronize()
+    res = out.cpu().numpy().view(np.uint32).astype(np.int64)
+    el = c.parts[0]
+    parts = tuple(type(el)(el.ctx, np.ascontiguousarray(res[p]), el.domain) for p in range(nparts))
+    return type(c)(parts=parts, fingerprint=params.fingerprint)
 
 
 def hsquare(c, rlk, params):

@@ -20,8 +20,12 @@ Outputs (committed; small):
                                sha256 digests, op counters, decrypted logits.
   set1.json                    N=8192 set 1: digests of keys, one ciphertext,
                                its hmult_raw and hsquare (full-size pin).
+  plain.npz / plain.json       hmult_plain, scalar and NTT paths, 2- and 3-part
+                               ciphertexts (N=64 arrays, N=1024 digests).
+  hfir.npz / hfir.json         HFIR bytes of a cipher tensor, a 3-part
+                               ciphertext and a relinearisation key.
 
-Usage: python tests/golden/make_golden.py [small n1024 cifar64 mnist1024 set1]
+Usage: python tests/golden/make_golden.py [small n1024 cifar64 mnist1024 set1 plain hfir]
 """
 
 from __future__ import annotations
@@ -357,8 +361,78 @@ def make_set1():
         json.dump(meta, fh, indent=1)
 
 
+def make_plain():
+    """hmult_plain (bfv.py:301-318): NTT path (random, sparse, high-degree
+    plaintexts) and scalar path (constants, both signs), 2- and 3-part
+    ciphertexts, at N=64 (t=257) and N=1024 with the set-1 primes."""
+    arrays, meta = {}, {}
+    for tag, n, k, t, seed in (("s", 64, 4, 257, 111), ("m", 1024, 11, MNIST_T, 222)):
+        ctx = ring.RnsContext(n, list(POOL[:k]))
+        params = bfv.BfvParams(ctx, t)
+        sk, pk, rlk = bfv.keygen(params, np.random.default_rng(seed))
+        rng = np.random.default_rng(seed + 1)
+        cts = [bfv.encrypt(pk, bfv.Plaintext(rng.integers(0, t, n), t), params, rng) for _ in range(2)]
+        cts += edge_cts(params, np.random.default_rng(seed + 2))[1:3]
+        pts = [rng.integers(0, t, n)]
+        sparse = np.zeros(n, dtype=np.int64)
+        sparse[[1, n - 1]] = [t - 1, 3]
+        pts.append(sparse)
+        top = np.zeros(n, dtype=np.int64)
+        top[n - 1] = t // 2 + 1
+        pts.append(top)
+        for v in (200 % t, t - 5, 7, 0):
+            pts.append(bfv.Plaintext.constant(v, params).poly)
+        outs = np.stack([np.stack([ct_arr(bfv.hmult_plain(c, bfv.Plaintext(pt, t), params)) for c in cts])
+                         for pt in pts])
+        raw3 = bfv.hmult_raw(cts[0], cts[1], params)
+        out3 = [ct_arr(bfv.hmult_plain(raw3, bfv.Plaintext(pt, t), params)) for pt in pts[:2]]
+        arrays.update({
+            f"{tag}_cts": u32([ct_arr(c) for c in cts]),
+            f"{tag}_pts": np.stack(pts).astype(np.int64),
+            f"{tag}_raw3": u32(ct_arr(raw3)),
+        })
+        meta[tag] = dict(n=n, primes=list(POOL[:k]), t=t)
+        if tag == "s":  # full outputs at N=64, sha256 of the u64 LE residues at N=1024
+            arrays.update({f"{tag}_out": u32(outs), f"{tag}_out3": u32(out3)})
+        else:
+            meta[tag]["out_sha"] = [hashlib.sha256(o.astype("<u8").tobytes()).hexdigest() for o in outs]
+            meta[tag]["out3_sha"] = [hashlib.sha256(np.asarray(o).astype("<u8").tobytes()).hexdigest()
+                                     for o in out3]
+    np.savez_compressed(os.path.join(HERE, "plain.npz"), **arrays)
+    with open(os.path.join(HERE, "plain.json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
+
+
+def make_hfir():
+    """HFIR bytes (serial.py:44-229) of a cipher tensor with fresh and
+    evaluated ciphertexts, a 3-part ciphertext and a relinearisation key:
+    the byte-exact target of the device-side HFIR reader/writer."""
+    ctx = ring.RnsContext(64, list(POOL[:4]))
+    params = bfv.BfvParams(ctx, 257)
+    sk, pk, rlk = bfv.keygen(params, np.random.default_rng(121))
+    rng = np.random.default_rng(122)
+    cts = [bfv.encrypt(pk, bfv.Plaintext(rng.integers(0, 257, 64), 257), params, rng) for _ in range(5)]
+    cts[3] = bfv.hsquare(cts[3], rlk, params)  # is_fresh False
+    tensor = engine.CipherTensor(shape=(1, 5, 1), cts=cts, delta=3 * 2**70 + 5, channel_modulus=257)
+    blob = serial.dump_cipher_tensor(tensor, params)
+    raw3 = bfv.hmult_raw(cts[0], cts[1], params)
+    np.savez_compressed(
+        os.path.join(HERE, "hfir.npz"),
+        tensor=np.frombuffer(blob, dtype=np.uint8),
+        cts=u32([ct_arr(c) for c in cts]),
+        fresh=np.array([c.is_fresh for c in cts]),
+        ct3=np.frombuffer(serial.dump_ciphertext(raw3, params), dtype=np.uint8),
+        raw3=u32(ct_arr(raw3)),
+        rlk_file=np.frombuffer(serial.dump_relin_key(rlk, params), dtype=np.uint8),
+        rlk=u32(rlk_arr(rlk)),
+    )
+    meta = dict(n=64, primes=list(POOL[:4]), t=257, keys_seed=121, delta=tensor.delta, shape=[1, 5, 1])
+    with open(os.path.join(HERE, "hfir.json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["small", "n1024", "cifar64", "set1", "mnist1024"]
+    which = sys.argv[1:] or ["small", "n1024", "cifar64", "set1", "mnist1024", "plain", "hfir"]
     for w in which:
         t0 = time.time()
         globals()["make_" + w]()

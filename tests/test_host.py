@@ -164,3 +164,61 @@ def test_oracle_is_not_imported_by_the_product():
             with open(os.path.join(pkg, fn)) as fh:
                 assert "hcnn_oracle" not in fh.read(), fn
     _ = O
+
+
+# ------------------------------------------------------------------ HFIR (host side)
+
+
+def _hfir():
+    from conftest import load_golden
+
+    return load_golden("hfir")
+
+
+def test_hfir_header_and_errors_match_reference_offsets():
+    """Header parsing and the host-side errors of the device HFIR reader follow
+    serial.py:53-84 (same classes, same byte offsets) -- no GPU needed."""
+    from paper_1811_00778_b200 import bfv as B
+    from paper_1811_00778_b200 import hfir
+    from paper_1811_00778_b200.errors import FormatError, ParameterMismatchError
+
+    meta, a = _hfir()
+    params = B.BfvParams(B.RnsContext(meta["n"], meta["primes"]), meta["t"])
+    blob = a["tensor"].tobytes()
+    import io
+
+    kind, n, primes, t = hfir.read_header(io.BytesIO(blob))
+    assert (kind, n, primes, t) == (hfir.KIND_CIPHER_TENSOR, meta["n"], meta["primes"], meta["t"])
+    assert hfir.header_bytes(hfir.KIND_CIPHER_TENSOR, params) == blob[: 4 + 3 + 6 + 8 * len(primes) + 8]
+    cases = [
+        (b"XFIR" + blob[4:], 0),
+        (blob[:4] + b"\x02\x00" + blob[6:], 4),
+        (blob[:6] + bytes([hfir.KIND_CIPHERTEXT]) + blob[7:], 6),
+        (blob[:10], 10),
+    ]
+    for bad, off in cases:
+        with pytest.raises(FormatError) as ei:
+            hfir.load_cipher_tensor_device(bad, params)
+        assert ei.value.offset == off
+    other = B.BfvParams(B.RnsContext(meta["n"], meta["primes"]), 65537)
+    with pytest.raises(ParameterMismatchError):
+        hfir.load_cipher_tensor_device(blob, other)
+
+
+def test_hfir_relin_key_reader_matches_reference_keys():
+    """load_relin_key_device keeps the serialised coefficient-domain key; its
+    NTT (oracle, reference order) equals the reference's in-memory key."""
+    import hcnn_oracle as O
+
+    from paper_1811_00778_b200 import bfv as B
+    from paper_1811_00778_b200 import hfir
+
+    meta, a = _hfir()
+    params = B.BfvParams(B.RnsContext(meta["n"], meta["primes"]), meta["t"])
+    key = hfir.load_relin_key_device(a["rlk_file"].tobytes(), params)
+    assert key.coeff.shape == a["rlk"].shape and key.base == params.w
+    ctx = O.Context(meta["n"], meta["primes"])
+    for i in range(key.coeff.shape[0]):
+        for part in range(2):
+            got = O.ntt_forward(ctx, key.coeff[i, part].astype(np.int64))
+            assert np.array_equal(got, a["rlk"][i, part].astype(np.int64))

@@ -244,3 +244,27 @@ class TestAgainstLiveReference:
             orlk = [(k0.residues, k1.residues) for k0, k1 in rlk.components]
             got = O.hsquare(pr, (c.parts[0].residues, c.parts[1].residues), orlk)
             assert np.array_equal(np.stack(got), np.stack([p.residues for p in ref.parts]))
+
+
+def test_hmult_plain_golden():
+    """Oracle hmult_plain (scalar and NTT paths, 2- and 3-part) against the
+    reference's outputs (tests/golden/plain.*)."""
+    from conftest import load_golden
+
+    meta, a = load_golden("plain")
+    for tag in ("s", "m"):
+        pr = _params(meta[tag])
+        cts = a[f"{tag}_cts"]
+        for k, pt in enumerate(a[f"{tag}_pts"]):
+            out = np.stack([np.stack(O.hmult_plain(pr, tuple(c.astype(np.int64)), pt)) for c in cts])
+            if tag == "s":
+                assert np.array_equal(out, a["s_out"][k]), k
+            else:
+                assert hashlib.sha256(out.astype("<u8").tobytes()).hexdigest() == meta["m"]["out_sha"][k], k
+        raw3 = tuple(p.astype(np.int64) for p in a[f"{tag}_raw3"])
+        for k, pt in enumerate(a[f"{tag}_pts"][:2]):
+            out3 = np.stack(O.hmult_plain(pr, raw3, pt))
+            if tag == "s":
+                assert np.array_equal(out3, a["s_out3"][k])
+            else:
+                assert hashlib.sha256(out3.astype("<u8").tobytes()).hexdigest() == meta["m"]["out3_sha"][k]
