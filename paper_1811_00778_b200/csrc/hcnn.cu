@@ -555,6 +555,61 @@ __global__ void k_dfma_peak(uint32_t* out, double a, double b, int iters) {
   if (acc == 1.2345) out[0] = 1;
 }
 
+// Harvey forward butterflies in registers (kind 8), 8 independent pairs per
+// thread, fixed Shoup twiddle: the attainable butterfly rate of the integer
+// pipes for the NTT kernels' instruction mix; counts butterflies
+__global__ void k_bfly_peak(uint32_t* out, uint32_t w, uint32_t ws, uint32_t p, int iters) {
+  uint32_t a[8], b[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    a[i] = (threadIdx.x * 7 + i + blockIdx.x) % p;
+    b[i] = (threadIdx.x * 13 + 3 * i + blockIdx.x) % p;
+  }
+  const uint32_t p2 = 2 * p;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uint32_t X = a[i] < a[i] - p2 ? a[i] : a[i] - p2;
+      const uint32_t T = b[i] * w - __umulhi(b[i], ws) * p;
+      a[i] = X + T;
+      b[i] = X - T + p2;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {  // mix the pairs like the next NTT stage
+      const uint32_t t = a[i + 1];
+      a[i + 1] = b[i];
+      b[i] = t;
+    }
+  }
+  uint32_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc ^= a[i] ^ b[i];
+  if (acc == 0x9e3779b9u) out[0] = acc;
+}
+
+// IMAD.WIDE and DFMA interleaved (kind 7): whether the fp64 pipe runs beside
+// the integer multiplier; counts both kinds of operation
+__global__ void k_mix_peak(uint32_t* out, uint32_t a, double da, double db, int iters) {
+  uint64_t x[4];
+  double y[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    x[i] = threadIdx.x * 7 + i + blockIdx.x;
+    y[i] = x[i];
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      x[i] = (uint64_t)(uint32_t)x[i] * a + x[i];
+      y[i] = fma(y[i], da, db);
+    }
+  }
+  uint64_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) acc ^= x[i] ^ (uint64_t)y[i];
+  if (acc == 0x9e3779b9u) out[0] = (uint32_t)acc;
+}
+
 // integer-pipe throughput probe: 8 independent chains per thread
 template <int KIND>
 __global__ void k_int_peak(uint32_t* out, uint32_t a, uint32_t b, int iters) {
@@ -668,6 +723,9 @@ int hcnn_int_peak(int device, int kind, double* ops_per_s) {
         case 3: k_int_peak<3><<<blocks, tpb>>>(out, 0x3e3779b1u, 12345u, iters); break;
         case 4: k_int_peak<4><<<blocks, tpb>>>(out, 0x3e3779b1u, 12345u, iters); break;
         case 6: k_dfma_peak<<<blocks, tpb>>>(out, 0.999999, 1e-9, iters); break;
+        case 7: k_mix_peak<<<blocks, tpb>>>(out, 0x9e3779b1u, 0.999999, 1e-9, iters); break;
+        case 8: k_bfly_peak<<<blocks, tpb>>>(out, 123456789u, 493942125u, 1073643521u, iters); break;
+        case 9: k_bfly_peak<<<blocks / 4, tpb>>>(out, 123456789u, 493942125u, 1073643521u, iters); break;
         default: k_int_peak<5><<<blocks, tpb>>>(out, 0x3e3779b1u, 12345u, iters); break;
       }
     };
@@ -679,7 +737,7 @@ int hcnn_int_peak(int device, int kind, double* ops_per_s) {
     CK(cudaEventSynchronize(e1));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, e0, e1));
-    *ops_per_s = 5.0 * blocks * tpb * (double)iters * 8 / (ms * 1e-3);
+    *ops_per_s = 5.0 * (kind == 9 ? blocks / 4 : blocks) * tpb * (double)iters * 8 / (ms * 1e-3);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaFree(out);
