@@ -171,6 +171,16 @@ class ClockSampler:
 # ---------------------------------------------------------------- work model
 
 
+def ntt_butterflies(name: str, K: int, KP: int, D: int, N: int, cts: float):
+    """NTT butterflies of one launch of an NTT kernel over `cts` ciphertexts."""
+    bfly = (N // 2) * (N.bit_length() - 1)
+    if name == "k_tensor":
+        return (K + KP) * 5 * bfly * cts
+    if name == "k_relin":
+        return K * (D + 2) * bfly * cts
+    return None
+
+
 def kernel_work(name: str, K: int, KP: int, D: int, N: int, cts: float):
     """Algorithmic (HBM bytes, IMAD issue slots) of one launch over `cts`
     ciphertexts.
@@ -375,6 +385,18 @@ def run_ours(args):
                 "share_of_step": round(tot / total_ms, 4),
                 "note": "integer-pipe kernel: tensor cores unused by design; DESIGN.md section 4",
             }
+            nb = ntt_butterflies(dom, g0.K, g0.KP, g0.D, g0.N, n_sq / cnt)
+            if nb:
+                bf = ctypes.c_double()
+                _lib.check(L.hcnn_int_peak(local, 8, ctypes.byref(bf)))
+                ach = nb / avg_s / 1e12
+                roof["bfly"] = {
+                    "achieved_t_bfly_s": round(ach, 3), "peak_t_bfly_s": round(bf.value / 1e12, 3),
+                    "frac": round(ach / (bf.value / 1e12), 4), "butterflies_per_launch": nb,
+                    "peak_source": "measured in bench.py (hcnn_int_peak kind 8: register-resident Harvey "
+                                   "butterflies, the NTT's instruction mix; attainable peak of the integer pipes)",
+                    "note": "counts NTT butterflies only (the kernel's MACs and exchanges are extra work)",
+                }
 
     images = W["images_per_step"]
     value = images / (ms / 1e3)

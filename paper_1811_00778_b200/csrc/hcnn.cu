@@ -587,6 +587,54 @@ __global__ void k_bfly_peak(uint32_t* out, uint32_t w, uint32_t ws, uint32_t p, 
   if (acc == 0x9e3779b9u) out[0] = acc;
 }
 
+// Butterfly cost decomposition probes (kinds 10-12), same chain structure as
+// k_bfly_peak.  10: the quotient of b w / p from the fp64 pipe (exact to +-1:
+// b -> double by the 2^52 trick, one DFMA with the magic 1.5 2^52 rounds it to
+// an integer in the low mantissa word), 2 IMAD for the lazy remainder;
+// 11: only the integer multiplies of a Shoup butterfly; 12: only its adds.
+template <int KIND>
+__global__ void k_bfly_probe(uint32_t* out, uint32_t w, uint32_t ws, uint32_t p, double wd, int iters) {
+  uint32_t a[8], b[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    a[i] = (threadIdx.x * 7 + i + blockIdx.x) % p;
+    b[i] = (threadIdx.x * 13 + 3 * i + blockIdx.x) % p;
+  }
+  const uint32_t p2 = 2 * p;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (KIND == 10) {
+        const uint32_t X = umin_u32(a[i], a[i] - p2);
+        const double bd = __hiloint2double(0x43300000, (int)b[i]) - 4503599627370496.0;
+        const double qd = fma(bd, wd, 6755399441055744.0);
+        const uint32_t q = (uint32_t)__double2loint(qd);
+        const uint32_t T = b[i] * w - q * p;  // in [-p, p)
+        a[i] = X + T + p;
+        b[i] = X - T + p;
+      } else if (KIND == 11) {
+        const uint32_t T = b[i] * w - __umulhi(b[i], ws) * p;
+        b[i] = T ^ a[i];
+        a[i] = T;
+      } else {
+        const uint32_t X = umin_u32(a[i], a[i] - p2);
+        a[i] = X + b[i];
+        b[i] = X - b[i] + p2;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {
+      const uint32_t t = a[i + 1];
+      a[i + 1] = b[i];
+      b[i] = t;
+    }
+  }
+  uint32_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc ^= a[i] ^ b[i];
+  if (acc == 0x9e3779b9u) out[0] = acc;
+}
+
 // IMAD.WIDE and DFMA interleaved (kind 7): whether the fp64 pipe runs beside
 // the integer multiplier; counts both kinds of operation
 __global__ void k_mix_peak(uint32_t* out, uint32_t a, double da, double db, int iters) {
@@ -726,6 +774,9 @@ int hcnn_int_peak(int device, int kind, double* ops_per_s) {
         case 7: k_mix_peak<<<blocks, tpb>>>(out, 0x9e3779b1u, 0.999999, 1e-9, iters); break;
         case 8: k_bfly_peak<<<blocks, tpb>>>(out, 123456789u, 493942125u, 1073643521u, iters); break;
         case 9: k_bfly_peak<<<blocks / 4, tpb>>>(out, 123456789u, 493942125u, 1073643521u, iters); break;
+        case 10: k_bfly_probe<10><<<blocks, tpb>>>(out, 123456789u, 493942125u, 1073643521u, 123456789.0 / 1073643521.0, iters); break;
+        case 11: k_bfly_probe<11><<<blocks, tpb>>>(out, 123456789u, 493942125u, 1073643521u, 0.0, iters); break;
+        case 12: k_bfly_probe<12><<<blocks, tpb>>>(out, 123456789u, 493942125u, 1073643521u, 0.0, iters); break;
         default: k_int_peak<5><<<blocks, tpb>>>(out, 0x3e3779b1u, 12345u, iters); break;
       }
     };

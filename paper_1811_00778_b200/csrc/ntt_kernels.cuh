@@ -216,14 +216,15 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
   }
 }
 
-// Square tensor for MIXED geometries (T = N/32 threads, two CTAs per SM): one
+// Square tensor for MIXED geometries (T = N/32 threads; two CTAs per SM up to
+// N = 8192, 128 registers per thread above): one
 // row in registers at a time; A0 and then d0, d1 wait in shared memory
 // (thread-owned slots e*T + tid) behind the single exchange buffer.
 template <class G>
 constexpr int tensor_sq_smem_words() { return G::ntt_smem_words(1) + 2 * G::N; }
 
 template <class G>
-__global__ void __launch_bounds__(G::T, 2)
+__global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
     k_tensor_sq(const uint32_t* __restrict__ a, const uint32_t* __restrict__ a_ext,
                 uint32_t* __restrict__ d, int K, int KP, NttTabs nt) {
   extern __shared__ __align__(16) uint32_t s[];
