@@ -64,8 +64,9 @@ enum {
   HCNN_Q_KERNELS = 6,  /* kernels launched since creation */
   HCNN_Q_NTT_VARIANT = 7
 };
-/* Tuning options.  HCNN_OPT_NTT_VARIANT: log2 of the residues each thread
- * keeps in the fused NTT kernels (0 = default per ring degree, 4 or 5). */
+/* Tuning options.  HCNN_OPT_NTT_VARIANT: geometry flags of the fused NTT
+ * kernels (0 default; 16 one-row relinearisation, 32 radix-32 square tensor,
+ * 64 mixed-width passes).  Results are identical for every setting. */
 enum { HCNN_OPT_NTT_VARIANT = 1 };
 int hcnn_ctx_set_option(hcnn_ctx* ctx, int key, int64_t value);
 int64_t hcnn_ctx_query(hcnn_ctx* ctx, int what);

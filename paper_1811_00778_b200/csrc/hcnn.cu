@@ -1369,6 +1369,50 @@ int hcnn_fc(hcnn_ctx* c, const uint32_t* in, uint32_t* out, int n_in, int n_out,
     const unsigned tpb = c->N >= 512 ? 128 : (c->N / 4 >= 32 ? c->N / 4 : 32);
     constexpr int OB = 8;
     dim3 grid(cdiv(c->N / 4, tpb), 2 * c->K, cdiv(n_out, OB));
+    int obs = 0;  // outputs per block of the split-K kernel: a divisor of n_out
+    for (int cand : {16, 10, 8, 5, 4, 2, 1})
+      if (n_out % cand == 0) {
+        obs = cand;
+        break;
+      }
+    if (wt->wd && wt->flush >= 16 && c->N >= 256) {
+      // split the inputs so that the grid covers the GPU ~8 times over; the
+      // block's weights (OB x chunk doubles) are staged in shared memory
+      const int nob = n_out / obs;
+      const unsigned bx = cdiv(c->N / 2, tpb);
+      const size_t base_blocks = (size_t)bx * 2 * c->K * nob;
+      int S = (int)std::min<size_t>(64, std::max<size_t>(1, (8 * 148 + base_blocks - 1) / base_blocks));
+      S = std::min(S, std::max(1, n_in / 32));
+      int chunk = (n_in + S - 1) / S;
+      while ((size_t)obs * chunk * sizeof(double) > 64 * 1024) chunk = (chunk + 1) / 2;
+      S = (n_in + chunk - 1) / chunk;
+      const size_t rows = (size_t)n_out * 2 * c->K;
+      uint32_t* ws = S > 1 ? (uint32_t*)c->workspace((size_t)S * rows * c->N * sizeof(uint32_t)) : out;
+      const dim3 gs(bx, 2 * c->K, (unsigned)(nob * S));
+      const size_t smem = (size_t)obs * chunk * sizeof(double);
+      switch (obs) {
+#define X(OBS)                                                                                             \
+  case OBS: {                                                                                              \
+    static bool cfg = false;                                                                               \
+    if (!cfg) {                                                                                            \
+      cudaFuncSetAttribute(k_fc_f64_split<OBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);   \
+      cfg = true;                                                                                          \
+    }                                                                                                      \
+    k_fc_f64_split<OBS><<<gs, tpb, smem, c->stream>>>(in, ws, wt->wd, n_in, n_out, (int)c->K, (int)c->N,   \
+                                                      wt->flush, chunk, nob, c->d_prime);                  \
+    break;                                                                                                 \
+  }
+        X(16) X(10) X(8) X(5) X(4) X(2) X(1)
+#undef X
+      }
+      c->launched("k_fc");
+      if (S > 1) {
+        const size_t quads = rows * c->N / 4;
+        k_fc_reduce<<<cdiv(quads, 256), 256, 0, c->stream>>>(ws, out, S, rows, (int)c->K, (int)c->N, c->d_prime);
+        c->launched("k_fc_reduce");
+      }
+      return;
+    }
     if (wt->wd && wt->flush >= 8) {
       k_fc_f64<OB, 256><<<grid, tpb, 0, c->stream>>>(in, out, wt->wd, n_in, n_out, (int)c->K, (int)c->N, wt->flush, c->d_prime);
       c->launched("k_fc");

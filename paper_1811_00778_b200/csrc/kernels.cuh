@@ -393,6 +393,90 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// Split-K dense layer: blockIdx.z = (output block, input split).  Each block
+// sums inputs [split*chunk, +chunk) for OB outputs of one (part, limb) over a
+// slab of 2 * blockDim coefficients (2 per thread, 8-byte loads) and writes
+// the reduced partial sum; k_fc_reduce adds the S partials mod p.  The block's
+// OB x chunk weights are staged in shared memory once.  Every input ciphertext
+// is read once per output block.  ws: [S][n_out][2][K][N] u32.
+template <int OB>
+__global__ void __launch_bounds__(128)
+    k_fc_f64_split(const uint32_t* __restrict__ in, uint32_t* __restrict__ ws,
+                   const double* __restrict__ wd, int n_in, int n_out, int K, int N, int flush,
+                   int chunk, int nob_blocks, const uint32_t* __restrict__ primes) {
+  extern __shared__ double wsd[];  // [OB][chunk]
+  const int ob = blockIdx.z % nob_blocks, split = blockIdx.z / nob_blocks;
+  const int o0 = ob * OB;
+  const int i0 = split * chunk, len = min(n_in, i0 + chunk) - i0;
+  for (int idx = threadIdx.x; idx < OB * chunk; idx += blockDim.x) {
+    const int o = idx / chunk, i = idx % chunk;
+    wsd[idx] = i < len ? wd[(size_t)(o0 + o) * n_in + i0 + i] : 0.0;
+  }
+  __syncthreads();
+  const int pair = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pair * 2 >= N) return;
+  const int limb = blockIdx.y % K, part = blockIdx.y / K;
+  const double p = (double)primes[limb];
+  const double pinv = 1.0 / p;
+  double acc[OB][2];
+#pragma unroll
+  for (int o = 0; o < OB; ++o) acc[o][0] = acc[o][1] = 0.0;
+  const size_t ct_stride = (size_t)K * N;  // uint2 per ciphertext
+  const uint2* base = reinterpret_cast<const uint2*>(in + ((size_t)part * K + limb) * N) + pair +
+                      (size_t)i0 * ct_stride;
+  int cnt = 0;
+  constexpr int U = 8;
+  for (int i = 0; i < len; i += U) {
+    uint2 xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = __ldg(base + (size_t)min(i + u, len - 1) * ct_stride);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (i + u >= len) break;
+      const double x0 = u32_to_f64(xv[u].x), x1 = u32_to_f64(xv[u].y);
+#pragma unroll
+      for (int o = 0; o < OB; ++o) {
+        const double w = wsd[o * chunk + i + u];
+        acc[o][0] = fma(w, x0, acc[o][0]);
+        acc[o][1] = fma(w, x1, acc[o][1]);
+      }
+    }
+    cnt += U;
+    if (cnt >= flush - U) {
+      cnt = 0;
+#pragma unroll
+      for (int o = 0; o < OB; ++o) {
+        acc[o][0] = fold_mod(acc[o][0], p, pinv);
+        acc[o][1] = fold_mod(acc[o][1], p, pinv);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < OB; ++o) {
+    const uint2 r = make_uint2(f64_mod(acc[o][0], p, pinv), f64_mod(acc[o][1], p, pinv));
+    *(reinterpret_cast<uint2*>(ws + ((((size_t)split * n_out + o0 + o) * 2 + part) * K + limb) * N) + pair) = r;
+  }
+}
+
+// out = sum over S partial sums mod p; ws [S][rows][N], rows = n_out * 2 * K
+__global__ void k_fc_reduce(const uint32_t* __restrict__ ws, uint32_t* __restrict__ out, int S, size_t rows,
+                            int K, int N, const uint32_t* __restrict__ primes) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;  // uint4 index
+  const size_t quads = rows * N / 4;
+  if (i >= quads) return;
+  const uint32_t p = primes[(i * 4 / N) % K];
+  const uint4* src = reinterpret_cast<const uint4*>(ws) + i;
+  uint4 a = src[0];
+  for (int s = 1; s < S; ++s) {
+    const uint4 b = src[(size_t)s * quads];
+    a.x = add_mod(a.x, b.x, p);
+    a.y = add_mod(a.y, b.y, p);
+    a.z = add_mod(a.z, b.z, p);
+    a.w = add_mod(a.w, b.w, p);
+  }
+  reinterpret_cast<uint4*>(out)[i] = a;
+}
+
 __global__ void k_weights_f64(const int64_t* __restrict__ w, size_t n, double* __restrict__ out) {
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t < n) out[t] = (double)w[t];
