@@ -151,6 +151,15 @@ int hcnn_relinearize(hcnn_ctx* ctx, const uint32_t* in3, uint32_t* out, size_t n
  * not below its prime (the device store keeps canonical residues only). */
 int hcnn_hfir_pack(hcnn_ctx* ctx, const uint32_t* rows_in, size_t rows, uint64_t* hfir);
 int hcnn_hfir_unpack(hcnn_ctx* ctx, const uint64_t* hfir, size_t rows, uint32_t* rows_out);
+/* Key generation from host-drawn randomness (bfv.keygen, bfv.py:164-188): the
+ * NTT-domain arithmetic on the device, bit-identical keys.  s_bits: N binary
+ * coefficients; a_ref: [1+D][K][N] uniform residues in the reference NTT order
+ * (row 0 for pk, row 1+i for rlk component i); e: [1+D][N] Gaussian noise.
+ * Outputs (HOST, reference NTT order): pk_out [2][K][N] = (b, a), rlk_out
+ * [D][2][K][N] = (k0_i, a_i).  The keys are also installed in the context
+ * (public, relinearisation and decryption key). */
+int hcnn_keygen(hcnn_ctx* ctx, const uint8_t* s_bits, const uint64_t* a_ref, const int8_t* e,
+                uint64_t* pk_out, uint64_t* rlk_out);
 /* ct x plaintext polynomial for n cts: bfv.hmult_plain (bfv.py:301-318).
  * pt: HOST pointer to the N centred plaintext coefficients (Plaintext.centered()).
  * A constant plaintext takes the scalar path (poly_mul_scalar, ring.py:193-196),

@@ -821,6 +821,14 @@ int hcnn_ctx_create(hcnn_ctx** out, uint32_t n, uint32_t k, const uint64_t* prim
     auto c = std::make_unique<hcnn_ctx>();
     c->device = device;
     CK(cudaSetDevice(device));
+    {
+      // keep stream-ordered allocations (workspace, temporaries) in the pool
+      // across synchronisations instead of returning them to the driver
+      cudaMemPool_t pool;
+      CK(cudaDeviceGetDefaultMemPool(&pool, device));
+      uint64_t keep = ~0ull;
+      CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
     c->stream = c->own_stream;
     c->N = n;
@@ -1145,6 +1153,80 @@ int hcnn_set_secret_key(hcnn_ctx* c, const uint8_t* s_bits) {
     CK(cudaFreeAsync(ds, c->stream));
     CK(cudaStreamSynchronize(c->stream));
   });
+}
+
+int hcnn_keygen(hcnn_ctx* c, const uint8_t* s_bits, const uint64_t* a_ref, const int8_t* e, uint64_t* pk_out,
+                uint64_t* rlk_out) {
+  const int st = guarded([&] {
+    if (!s_bits || !a_ref || !e || !pk_out || !rlk_out) fail(HCNN_ERR_PARAM, "keygen: null buffer");
+    CK(cudaSetDevice(c->device));
+    const size_t N = c->N, K = c->K, D = c->D, R = 1 + D;
+    const unsigned logn = c->logN;
+    // secret key rows in the device NTT order (also the decryption key)
+    uint8_t* ds = nullptr;
+    CK(cudaMallocAsync((void**)&ds, N, c->stream));
+    CK(cudaMemcpyAsync(ds, s_bits, N, cudaMemcpyHostToDevice, c->stream));
+    if (!c->d_sk) CK(cudaMalloc((void**)&c->d_sk, K * N * sizeof(uint32_t)));
+    k_sk_rows<<<cdiv(N, 256), 256, 0, c->stream>>>(ds, c->d_sk, (int)K, (int)N);
+    c->launched("k_sk_rows");
+    launch_ntt_rows(c, c->d_sk, K, (int)K, 0, 0);
+    // a (reference NTT order) -> device order; e -> NTT
+    const size_t rows = R * K, count = rows * N;
+    uint64_t* stage = nullptr;
+    uint32_t *da = nullptr, *adev = nullptr, *erow = nullptr, *out = nullptr, *dw = nullptr;
+    int8_t* de = nullptr;
+    CK(cudaMallocAsync((void**)&stage, count * sizeof(uint64_t), c->stream));
+    CK(cudaMallocAsync((void**)&da, count * sizeof(uint32_t), c->stream));
+    CK(cudaMallocAsync((void**)&adev, count * sizeof(uint32_t), c->stream));
+    CK(cudaMallocAsync((void**)&erow, count * sizeof(uint32_t), c->stream));
+    CK(cudaMallocAsync((void**)&out, count * sizeof(uint32_t), c->stream));
+    CK(cudaMallocAsync((void**)&de, R * N, c->stream));
+    CK(cudaMallocAsync((void**)&dw, rows * sizeof(uint32_t), c->stream));
+    CK(cudaMemcpyAsync(stage, a_ref, count * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
+    k_narrow<<<cdiv(count, 256), 256, 0, c->stream>>>(stage, da, count);
+    c->launched("k_narrow");
+    k_bitrev_rows<<<dim3(cdiv(N, 256), (unsigned)rows), 256, 0, c->stream>>>(da, adev, (int)N, (int)logn);
+    c->launched("k_bitrev_rows");
+    CK(cudaMemcpyAsync(de, e, R * N, cudaMemcpyHostToDevice, c->stream));
+    k_embed_small<<<cdiv(R * N, 256), 256, 0, c->stream>>>(de, erow, (int)R, (int)K, (int)N, c->d_prime);
+    c->launched("k_embed_small");
+    launch_ntt_rows(c, erow, rows, (int)K, 0, 0);
+    // w^i mod q_k (row 0, the public key, takes no s^2 term)
+    std::vector<uint32_t> wres(rows, 0);
+    for (size_t k = 0; k < K; ++k) {
+      u64 wp = 1 % c->primes[k];
+      const u64 w = (u64)(((u128)1 << c->log2w) % c->primes[k]);
+      for (size_t r = 1; r < R; ++r) {
+        wres[r * K + k] = (uint32_t)wp;
+        wp = mulmod64(wp, w, c->primes[k]);
+      }
+    }
+    CK(cudaMemcpyAsync(dw, wres.data(), rows * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+    k_keygen_combine<<<cdiv(count, 256), 256, 0, c->stream>>>(adev, erow, c->d_sk, dw, out, (int)R, (int)K,
+                                                             (int)N, c->d_prime, c->d_mu);
+    c->launched("k_keygen_combine");
+    // back to the reference order, widened to u64
+    k_bitrev_rows<<<dim3(cdiv(N, 256), (unsigned)rows), 256, 0, c->stream>>>(out, da, (int)N, (int)logn);
+    c->launched("k_bitrev_rows");
+    k_widen<<<cdiv(count, 256), 256, 0, c->stream>>>(da, stage, count);
+    c->launched("k_widen");
+    std::vector<uint64_t> host(count);
+    CK(cudaMemcpyAsync(host.data(), stage, count * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    for (void* ptr : {(void*)stage, (void*)da, (void*)adev, (void*)erow, (void*)out, (void*)de, (void*)dw, (void*)ds})
+      CK(cudaFreeAsync(ptr, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    const size_t row_n = K * N;
+    std::memcpy(pk_out, host.data(), row_n * sizeof(uint64_t));
+    std::memcpy(pk_out + row_n, a_ref, row_n * sizeof(uint64_t));
+    for (size_t i = 0; i < D; ++i) {
+      std::memcpy(rlk_out + (2 * i) * row_n, host.data() + (1 + i) * row_n, row_n * sizeof(uint64_t));
+      std::memcpy(rlk_out + (2 * i + 1) * row_n, a_ref + (1 + i) * row_n, row_n * sizeof(uint64_t));
+    }
+  });
+  if (st) return st;
+  // install the new keys in the context
+  const int s1 = hcnn_set_public_key(c, pk_out, HCNN_DOMAIN_REF_NTT);
+  return s1 ? s1 : hcnn_set_relin_key(c, rlk_out, HCNN_DOMAIN_REF_NTT);
 }
 
 int hcnn_decrypt(hcnn_ctx* c, const uint32_t* cts, uint64_t* m, size_t n) {
@@ -1550,15 +1632,15 @@ int hcnn_mul_plain(hcnn_ctx* c, const uint32_t* cts, const int64_t* pt, uint32_t
       k_mul_scalar<<<cdiv(total, 256), 256, 0, c->stream>>>(cts, out, d_s, (int)K, (int)N, total, c->d_prime,
                                                              c->d_mu);
       c->launched("k_mul_scalar");
-      CK(cudaFreeAsync(d_s, c->stream));
-      CK(cudaStreamSynchronize(c->stream));  // sres is a host temporary
+      CK(cudaFreeAsync(d_s, c->stream));  // sres (pageable) was consumed by the copy call
       return;
     }
     int64_t* d_pt = nullptr;
     uint32_t* rows = nullptr;
     CK(cudaMallocAsync((void**)&d_pt, N * sizeof(int64_t), c->stream));
     CK(cudaMallocAsync((void**)&rows, K * N * sizeof(uint32_t), c->stream));
-    CK(cudaMemcpyAsync(d_pt, pt, N * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    const std::vector<int64_t> hpt(pt, pt + N);  // pageable copy: staged before the call returns
+    CK(cudaMemcpyAsync(d_pt, hpt.data(), N * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
     k_lift_plain<<<cdiv(N, 256), 256, 0, c->stream>>>(d_pt, rows, (int)N, (int)K, c->d_prime);
     c->launched("k_lift_plain");
     launch_ntt_rows(c, rows, K, (int)K, 0, 2);  // NTT domain, tiled layout
@@ -1571,7 +1653,6 @@ int hcnn_mul_plain(hcnn_ctx* c, const uint32_t* cts, const int64_t* pt, uint32_t
     ntt_dispatch(c, 6, a, "k_mul_plain");
     CK(cudaFreeAsync(d_pt, c->stream));
     CK(cudaFreeAsync(rows, c->stream));
-    CK(cudaStreamSynchronize(c->stream));  // pt is caller-owned host memory
   });
 }
 

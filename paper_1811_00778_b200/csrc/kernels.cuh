@@ -579,6 +579,38 @@ __global__ void k_mul_scalar(const uint32_t* __restrict__ in, uint32_t* __restri
   out[i] = mul_mod(in[i], sres[limb], primes[limb], mus[limb]);
 }
 
+// small signed coefficients (int8 [R][N]) -> residues [R][K][N]
+__global__ void k_embed_small(const int8_t* __restrict__ e, uint32_t* __restrict__ rows, int R, int K, int N,
+                              const uint32_t* __restrict__ primes) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;  // (r, n)
+  if (i >= (size_t)R * N) return;
+  const size_t r = i / N, n = i % N;
+  const int v = e[i];
+  for (int k = 0; k < K; ++k) rows[(r * K + k) * N + n] = v < 0 ? primes[k] - (uint32_t)(-v) : (uint32_t)v;
+}
+
+// key rows in the NTT domain (bfv.py:164-188), R = 1 + D rows [R][K][N]:
+// row 0 = b = e - a s, row 1+i = k0_i = w^i s^2 - (a_i s + e_i); wres [R][K]
+__global__ void k_keygen_combine(const uint32_t* __restrict__ a, const uint32_t* __restrict__ e,
+                                 const uint32_t* __restrict__ s, const uint32_t* __restrict__ wres,
+                                 uint32_t* __restrict__ out, int R, int K, int N,
+                                 const uint32_t* __restrict__ primes, const uint64_t* __restrict__ mus) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (size_t)R * K * N) return;
+  const size_t row = i / N, n = i % N;
+  const int r = (int)(row / K), k = (int)(row % K);
+  const uint32_t p = primes[k];
+  const uint64_t mu = mus[k];
+  const uint32_t sv = s[(size_t)k * N + n];
+  const uint32_t as = mul_mod(a[i], sv, p, mu);
+  if (r == 0) {
+    out[i] = sub_mod(e[i], as, p);
+  } else {
+    const uint32_t s2w = mul_mod(mul_mod(sv, sv, p, mu), wres[r * K + k], p, mu);
+    out[i] = sub_mod(s2w, add_mod(as, e[i], p), p);
+  }
+}
+
 // reference-order NTT (natural, a(psi^(2k+1))) -> device spectral order
 // in place on [rows][N] via a temp: dst[i] = src[brv(i)]
 __global__ void k_bitrev_rows(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, int N,

@@ -616,6 +616,39 @@ def draw_encryption_noise(rng, count: int, n: int):
     return u, e1, e2
 
 
+def keygen_device(params, rng, device=None):
+    """(sk, pk, rlk) like bfv.keygen(params, rng) (bfv.py:164-188), with the
+    NTT-domain key arithmetic on the GPU (hcnn_keygen).  The randomness is drawn
+    on the host in the reference's order (s, a, e, then a_i, e_i per digit),
+    so the keys are bit-identical; they are also installed in the context."""
+    from . import bfv as _b
+
+    g = context_for(params, device)
+    ctx = params.ctx
+    n, k, d = g.N, g.K, g.D
+    s_bits = rng.integers(0, 2, n, dtype=np.int64)
+    a_rows = np.empty((1 + d, k, n), dtype=np.uint64)
+    e_rows = np.empty((1 + d, n), dtype=np.int8)
+    for r in range(1 + d):
+        a_rows[r] = _b._uniform(ctx, rng)
+        e_rows[r] = _b._gauss(rng, n)
+    pk_out = np.empty((2, k, n), dtype=np.uint64)
+    rlk_out = np.empty((d, 2, k, n), dtype=np.uint64)
+    s8 = np.ascontiguousarray(s_bits.astype(np.uint8))
+    g.bind_stream()
+    _lib.check(_lib.lib().hcnn_keygen(g.handle, s8.ctypes.data, a_rows.ctypes.data, e_rows.ctypes.data,
+                                      pk_out.ctypes.data, rlk_out.ctypes.data), "hcnn_keygen")
+    el = lambda arr: _b.RingElem(ctx, arr.astype(np.int64), _b.Domain.NTT)  # noqa: E731
+    m = ctx._modcol
+    s_ntt = ctx.ntt.forward(s_bits[None, :] % m)  # client-side copy of the secret in the NTT domain
+    sk = _b.SecretKey(s_bits=s_bits, s_ntt=el(s_ntt), s2_ntt=el(s_ntt * s_ntt % m))
+    pk = _b.PublicKey(el(pk_out[0]), el(pk_out[1]), params.fingerprint)
+    rlk = _b.RelinKey([(el(rlk_out[i, 0]), el(rlk_out[i, 1])) for i in range(d)], params.w, params.fingerprint)
+    g._pk_ref = weakref.ref(pk)
+    g._rlk_ref = weakref.ref(rlk)
+    return sk, pk, rlk
+
+
 def encrypt_device(pk, polys, params, rng, device=None) -> torch.Tensor:
     """Encrypt plaintext polys [P][N] (in [0, t)) on the GPU; same bytes as P
     successive bfv.encrypt calls with this rng (bfv.py:201-216)."""
