@@ -68,7 +68,20 @@ struct NttTabs {
   const uint32_t* pinv;   // [K+KP]        -p^-1 mod 2^32 (Montgomery)
   const uint2* ninv_m;    // [K+KP]        N^-1 2^32 mod p, Shoup: undoes the 2^-32
                           //               of Montgomery pointwise products
+  const uint2* ninv_w;    // [K+KP]        psi^-N/2 N^-1: the last inverse stage's twiddle, scaled
+  const uint2* ninv_mw;   // [K+KP]        psi^-N/2 N^-1 2^32
 };
+
+// Output scaling of an inverse transform, folded into its last stage (whose
+// butterflies all share the twiddle psi^-N/2): n for the sum, nw for the
+// difference.
+struct InvScale {
+  uint2 n, nw;
+};
+
+DI InvScale inv_scale(const NttTabs& nt, int j, bool mont) {
+  return mont ? InvScale{nt.ninv_m[j], nt.ninv_mw[j]} : InvScale{nt.ninv[j], nt.ninv_w[j]};
+}
 
 // fixed point of the CRT overflow estimates: 59 fractional bits
 constexpr int FRAC_BITS = 59;

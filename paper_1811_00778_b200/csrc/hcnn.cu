@@ -212,7 +212,7 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
   // NTT tables
   std::vector<uint32_t> hp(L);
   std::vector<uint64_t> hmu(L);
-  std::vector<uint2> htw((size_t)L * N), hitw((size_t)L * N), hninv(2 * L);
+  std::vector<uint2> htw((size_t)L * N), hitw((size_t)L * N), hninv(4 * L);
   std::vector<uint32_t> hpinv(L);
   c->psi.resize(L);
   for (uint32_t j = 0; j < L; ++j) {
@@ -242,6 +242,10 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
     hninv[j] = make_uint2(ninv, shoup_of(ninv, (uint32_t)p));
     const uint32_t ninv_m = (uint32_t)mont_form(ninv, p);
     hninv[L + j] = make_uint2(ninv_m, shoup_of(ninv_m, (uint32_t)p));
+    const uint32_t wl = (uint32_t)ipw[N / 2];  // twiddle of the last inverse stage (itw[1])
+    const uint32_t nw = (uint32_t)mulmod64(wl, ninv, p), nmw = (uint32_t)mulmod64(wl, ninv_m, p);
+    hninv[2 * L + j] = make_uint2(nw, shoup_of(nw, (uint32_t)p));
+    hninv[3 * L + j] = make_uint2(nmw, shoup_of(nmw, (uint32_t)p));
   }
 
   // exact base conversion and scaling constants
@@ -327,15 +331,16 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
   CK(cudaMalloc(&c->d_mu, L * sizeof(uint64_t)));
   CK(cudaMalloc(&c->d_tw, (size_t)L * N * sizeof(uint2)));
   CK(cudaMalloc(&c->d_itw, (size_t)L * N * sizeof(uint2)));
-  CK(cudaMalloc(&c->d_ninv, 2 * L * sizeof(uint2)));
+  CK(cudaMalloc(&c->d_ninv, 4 * L * sizeof(uint2)));
   CK(cudaMalloc(&c->d_pinv, L * sizeof(uint32_t)));
   CK(cudaMemcpy(c->d_pinv, hpinv.data(), L * sizeof(uint32_t), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_prime, hp.data(), L * sizeof(uint32_t), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_mu, hmu.data(), L * sizeof(uint64_t), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_tw, htw.data(), (size_t)L * N * sizeof(uint2), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_itw, hitw.data(), (size_t)L * N * sizeof(uint2), cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(c->d_ninv, hninv.data(), 2 * L * sizeof(uint2), cudaMemcpyHostToDevice));
-  c->nt = NttTabs{c->d_prime, c->d_mu, c->d_tw, c->d_itw, c->d_ninv, c->d_pinv, c->d_ninv + L};
+  CK(cudaMemcpy(c->d_ninv, hninv.data(), 4 * L * sizeof(uint2), cudaMemcpyHostToDevice));
+  c->nt = NttTabs{c->d_prime, c->d_mu, c->d_tw, c->d_itw, c->d_ninv, c->d_pinv, c->d_ninv + L, c->d_ninv + 2 * L,
+                 c->d_ninv + 3 * L};
 }
 
 // ---------------------------------------------------------------- dispatch

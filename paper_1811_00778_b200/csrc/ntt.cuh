@@ -184,33 +184,48 @@ DI void fwd_stage(uint32_t* x, const uint2* __restrict__ tw, uint32_t p, int tid
 }
 
 // inverse (GS) stage SS of a pass (SS descending = bits ascending); values
-// in [0, 2p)
+// in [0, 2p).  The last stage (s = 0, one twiddle psi^-N/2 for every
+// butterfly) also applies the output scaling: sum * n, difference * nw, both
+// fully reduced.
 template <class G, int LO, int KB, int SS, int NR>
-DI void inv_stage(uint32_t* x, const uint2* __restrict__ itw, uint32_t p, int tid) {
+DI void inv_stage(uint32_t* x, const uint2* __restrict__ itw, uint32_t p, int tid, const InvScale& sc) {
   if constexpr (SS >= 0) {
     constexpr int bpos = LO + KB - 1 - SS;
     constexpr int s = G::LOGN - 1 - bpos;
     constexpr int half = 1 << (KB - 1 - SS);
     const uint32_t p2 = 2 * p;
+    if constexpr (s == 0) {
 #pragma unroll
-    for (int g = 0; g < (G::E >> KB); ++g) {
-      const int o = (g << G::LOGT) | tid;
-      // twiddles in chunks of TWC pairs, loaded just before their butterflies
-      constexpr int TWC = (1 << SS) < TW_CHUNK ? (1 << SS) : TW_CHUNK;
+      for (int e = 0; e < G::E; ++e) {
+        if (e & half) continue;
 #pragma unroll
-      for (int tc = 0; tc < (1 << SS); tc += TWC) {
-        uint2 w[TWC];
-        load_tw<TWC>(w, itw, (1 << s) + ((o >> LO) << SS) + tc);
+        for (int r = 0; r < NR; ++r) {
+          const uint32_t X = x[r * G::E + e], Y = x[r * G::E + (e | half)];
+          x[r * G::E + e] = mul_shoup(X + Y, sc.n.x, sc.n.y, p);
+          x[r * G::E + (e | half)] = mul_shoup(X - Y + p2, sc.nw.x, sc.nw.y, p);
+        }
+      }
+    } else {
 #pragma unroll
-        for (int el = tc << (KB - SS); el < (tc + TWC) << (KB - SS); ++el) {
-          if (el & half) continue;
-          const int e = (g << KB) | el;
+      for (int g = 0; g < (G::E >> KB); ++g) {
+        const int o = (g << G::LOGT) | tid;
+        // twiddles in chunks of TWC pairs, loaded just before their butterflies
+        constexpr int TWC = (1 << SS) < TW_CHUNK ? (1 << SS) : TW_CHUNK;
 #pragma unroll
-          for (int r = 0; r < NR; ++r) bfly_inv(x[r * G::E + e], x[r * G::E + (e | half)], w[(el >> (KB - SS)) - tc], p, p2);
+        for (int tc = 0; tc < (1 << SS); tc += TWC) {
+          uint2 w[TWC];
+          load_tw<TWC>(w, itw, (1 << s) + ((o >> LO) << SS) + tc);
+#pragma unroll
+          for (int el = tc << (KB - SS); el < (tc + TWC) << (KB - SS); ++el) {
+            if (el & half) continue;
+            const int e = (g << KB) | el;
+#pragma unroll
+            for (int r = 0; r < NR; ++r) bfly_inv(x[r * G::E + e], x[r * G::E + (e | half)], w[(el >> (KB - SS)) - tc], p, p2);
+          }
         }
       }
     }
-    inv_stage<G, LO, KB, SS - 1, NR>(x, itw, p, tid);
+    inv_stage<G, LO, KB, SS - 1, NR>(x, itw, p, tid, sc);
   }
 }
 
@@ -418,7 +433,7 @@ DI void fwd_from(uint32_t* x, uint32_t* s, const uint2* __restrict__ tw, uint32_
 }
 
 template <class G, int P, int NR>
-DI void inv_from(uint32_t* x, uint32_t* s, const uint2* __restrict__ itw, uint32_t p, int tid) {
+DI void inv_from(uint32_t* x, uint32_t* s, const uint2* __restrict__ itw, uint32_t p, int tid, const InvScale& sc) {
   if constexpr (P >= 0) {
     if constexpr (P < G::NFULL - 1) {
       // exchange index continues after the register-tail exchange (if any)
@@ -429,8 +444,8 @@ DI void inv_from(uint32_t* x, uint32_t* s, const uint2* __restrict__ itw, uint32
       __syncthreads();
       smem_to_regs<G, P, NR>(x, b, tid);
     }
-    inv_stage<G, G::lo(P), G::kb(P), G::kb(P) - 1, NR>(x, itw, p, tid);
-    inv_from<G, P - 1, NR>(x, s, itw, p, tid);
+    inv_stage<G, G::lo(P), G::kb(P), G::kb(P) - 1, NR>(x, itw, p, tid, sc);
+    inv_from<G, P - 1, NR>(x, s, itw, p, tid, sc);
   }
 }
 
@@ -490,9 +505,10 @@ DI void store_tiled(const uint32_t* x, uint32_t* __restrict__ row, int tid) {
 }
 
 // Forward negacyclic NTT of NR rows of one prime: natural layout in (values
-// < 4p), spectral layout out, fully reduced to [0, p).  `s`:
+// < 4p), spectral layout out, fully reduced to [0, p) (FULL) or to [0, 2p)
+// when the result only feeds Montgomery products.  `s`:
 // G::ntt_smem_words(NR) words of shared memory.
-template <class G, int NR = 1>
+template <class G, int NR = 1, bool FULL = true>
 DI void ntt_fwd(uint32_t* x, uint32_t* s, const uint2* __restrict__ tw, uint32_t p, int tid) {
   fwd_from<G, 0, NR>(x, s, tw, p, tid);
   if constexpr (G::SHFL_TAIL) {
@@ -516,14 +532,15 @@ DI void ntt_fwd(uint32_t* x, uint32_t* s, const uint2* __restrict__ tw, uint32_t
 #pragma unroll
   for (int e = 0; e < NR * G::E; ++e) {
     const uint32_t v = umin32(x[e], x[e] - p2);
-    x[e] = umin32(v, v - p);
+    x[e] = FULL ? umin32(v, v - p) : v;
   }
 }
 
 // Inverse negacyclic NTT of NR rows: spectral layout in (values < 2p),
-// natural layout out, times N^-1, reduced to [0, p).
+// natural layout out, scaled by sc (N^-1, folded into the last stage),
+// reduced to [0, p).
 template <class G, int NR = 1>
-DI void ntt_inv(uint32_t* x, uint32_t* s, const uint2* __restrict__ itw, uint32_t p, uint2 ninv,
+DI void ntt_inv(uint32_t* x, uint32_t* s, const uint2* __restrict__ itw, uint32_t p, const InvScale& sc,
                 int tid) {
   if constexpr (G::SHFL_TAIL) {
     inv_shfl<G, 0, NR>(x, itw, p, tid);
@@ -541,10 +558,8 @@ DI void ntt_inv(uint32_t* x, uint32_t* s, const uint2* __restrict__ itw, uint32_
 #pragma unroll
       for (int e = 0; e < G::E; ++e) x[r * G::E + e] = b[r * G::XW + sidx(pass_index<G::REM, G::LOGE>(tid, e))];
   }
-  inv_from<G, G::NFULL - 1, NR>(x, s, itw, p, tid);
+  inv_from<G, G::NFULL - 1, NR>(x, s, itw, p, tid, sc);
   post_transform<G, NR>();
-#pragma unroll
-  for (int e = 0; e < NR * G::E; ++e) x[e] = mul_shoup(x[e], ninv.x, ninv.y, p);
 }
 
 }  // namespace hcnn

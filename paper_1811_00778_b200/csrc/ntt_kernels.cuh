@@ -47,7 +47,7 @@ DI void load_natural(uint32_t* x, const uint32_t* __restrict__ row, int tid) {
 }
 
 template <class G>
-DI void inv_store(uint32_t* x, uint32_t* s, const uint2* itw, uint32_t p, uint2 ninv, int tid,
+DI void inv_store(uint32_t* x, uint32_t* s, const uint2* itw, uint32_t p, const InvScale& ninv, int tid,
                   uint32_t* __restrict__ row) {
   ntt_inv<G>(x, s, itw, p, ninv, tid);
 #pragma unroll
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
   if (inverse == 1) {
 #pragma unroll
     for (int e = 0; e < G::E; ++e) x[e] = r[spectral_index<G>(tid, e)];
-    ntt_inv<G>(x, s, nt.itw + (size_t)j * G::N, p, nt.ninv[j], tid);
+    ntt_inv<G>(x, s, nt.itw + (size_t)j * G::N, p, inv_scale(nt, j, false), tid);
 #pragma unroll
     for (int e = 0; e < G::E; ++e) r[natural_index<G>(tid, e)] = x[e];
     return;
@@ -90,18 +90,18 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
 template <class G>
 __host__ __device__ constexpr int pair_nr() { return G::fits(2) ? 2 : 1; }
 
-template <class G>
+template <class G, bool FULL = true>
 DI void ntt_fwd_pair(uint32_t* x, uint32_t* s, const uint2* tw, uint32_t p, int tid) {
   if constexpr (pair_nr<G>() == 2) {
-    ntt_fwd<G, 2>(x, s, tw, p, tid);
+    ntt_fwd<G, 2, FULL>(x, s, tw, p, tid);
   } else {
-    ntt_fwd<G>(x, s, tw, p, tid);
-    ntt_fwd<G>(x + G::E, s, tw, p, tid);
+    ntt_fwd<G, 1, FULL>(x, s, tw, p, tid);
+    ntt_fwd<G, 1, FULL>(x + G::E, s, tw, p, tid);
   }
 }
 
 template <class G>
-DI void ntt_inv_pair(uint32_t* x, uint32_t* s, const uint2* itw, uint32_t p, uint2 ninv, int tid) {
+DI void ntt_inv_pair(uint32_t* x, uint32_t* s, const uint2* itw, uint32_t p, const InvScale& ninv, int tid) {
   if constexpr (pair_nr<G>() == 2) {
     ntt_inv<G, 2>(x, s, itw, p, ninv, tid);
   } else {
@@ -139,13 +139,13 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
   // inverse transforms multiply by N^-1 2^32 instead of N^-1
   const uint32_t pinv = nt.pinv[j];
   const uint32_t p2 = 2 * p;
-  const uint2 ninv = nt.ninv_m[j];
+  const InvScale ninv = inv_scale(nt, j, true);
   uint32_t x[2 * E], y[2 * E];
   if (square) {
     // x = (A0 | A1)
     load_natural<G>(x, row_of(a, a_ext, 0), tid);
     load_natural<G>(x + E, row_of(a, a_ext, 1), tid);
-    ntt_fwd_pair<G>(x, s, tw, p, tid);
+    ntt_fwd_pair<G, false>(x, s, tw, p, tid);  // [0, 2p): products < 4p^2 < 2^32 p
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const uint32_t a0 = x[e], a1 = x[E + e];
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
   uint32_t x[2 * E];
   load_natural<G>(x, a + ((ct * 2 + 0) * K + j) * G::N, tid);
   load_natural<G>(x + E, a + ((ct * 2 + 1) * K + j) * G::N, tid);
-  ntt_fwd_pair<G>(x, s, nt.tw + (size_t)j * G::N, p, tid);
+  ntt_fwd_pair<G, false>(x, s, nt.tw + (size_t)j * G::N, p, tid);  // [0, 2p) feeds Montgomery products
   {
     uint32_t k[E];
     load_tiled<G>(k, pt + (size_t)j * G::N, tid);
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
       x[E + e] = mont_mul(x[E + e], k[e], p, pinv);
     }
   }
-  ntt_inv_pair<G>(x, s, nt.itw + (size_t)j * G::N, p, nt.ninv_m[j], tid);
+  ntt_inv_pair<G>(x, s, nt.itw + (size_t)j * G::N, p, inv_scale(nt, j, true), tid);
 #pragma unroll
   for (int part = 0; part < 2; ++part) {
     uint32_t* o = out + ((ct * 2 + part) * K + j) * G::N;
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
   const uint32_t p2 = 2 * p;
   const uint2* tw = nt.tw + (size_t)j * G::N;
   const uint2* itw = nt.itw + (size_t)j * G::N;
-  const uint2 ninv = nt.ninv_m[j];
+  const InvScale ninv = inv_scale(nt, j, true);
   uint32_t* st0 = s + G::ntt_smem_words(1);
   uint32_t* st1 = st0 + G::N;
   auto row_of = [&](int part) -> const uint32_t* {
@@ -369,7 +369,8 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
 #pragma unroll
       for (int e = 0; e < R * E; ++e) x[e] = reduce64(x[e], p, mu);
     }
-    ntt_fwd<G, R>(x, s, tw, p, tid);
+    // Montgomery MACs take the digit spectra in [0, 2p) (paired sums < 4p^2 < 2^32 p)
+    ntt_fwd<G, R, ACC64>(x, s, tw, p, tid);
     if constexpr (!ACC64 && R == 2) {
       // both digits' products summed in 64 bits (< 2 p^2 < 2^32 p), one
       // Montgomery reduction per pair; keys streamed 16 bytes at a time
@@ -437,7 +438,7 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
     i += R;
   }
   const uint2* itw = nt.itw + (size_t)j * G::N;
-  const uint2 ninv = nt.ninv[j];
+  const InvScale ninv = inv_scale(nt, j, false);
   // both parts through the inverse (in lockstep when NR = 2)
   uint32_t x[2 * E];
 #pragma unroll
@@ -496,7 +497,7 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
     load_tiled<G>(y, pk + ((size_t)part * K + j) * G::N, tid);
 #pragma unroll
     for (int e = 0; e < G::E; ++e) y[e] = mul_mod(x[e], y[e], p, mu);
-    ntt_inv<G>(y, s, nt.itw + (size_t)j * G::N, p, nt.ninv[j], tid);
+    ntt_inv<G>(y, s, nt.itw + (size_t)j * G::N, p, inv_scale(nt, j, false), tid);
     const int8_t* er = (part ? e2 : e1) + ct * G::N;
     uint32_t* o = out + ((ct * 2 + part) * K + j) * G::N;
 #pragma unroll
