@@ -842,6 +842,9 @@ int hcnn_ctx_create(hcnn_ctx** out, uint32_t n, uint32_t k, const uint64_t* prim
     c->K = k;
     c->t = t;
     c->log2w = log2w;
+    // default geometry per ring degree (profiles/r1_micro_sweep.jsonl): the
+    // shuffle-tail radix-16 kernels up to 2^13, mixed-width passes at 2^14
+    c->variant = c->logN == 14 ? 64 : 0;
     build_tables(c.get(), q, t);
     *out = c.release();
   });

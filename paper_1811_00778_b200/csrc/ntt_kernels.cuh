@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
 // Transforms of two rows x[0, E) and x[E, 2E): in lockstep when the
 // geometry's shared memory allows, else one after the other.
 template <class G>
-__host__ __device__ constexpr int pair_nr() { return G::fits(2) ? 2 : 1; }
+__host__ __device__ constexpr int pair_nr() { return G::E < 32 && G::fits(2) ? 2 : 1; }
 
 template <class G, bool FULL = true>
 DI void ntt_fwd_pair(uint32_t* x, uint32_t* s, const uint2* tw, uint32_t p, int tid) {

@@ -125,9 +125,9 @@ class GpuContext:
         self.handle = h
         self.KP = int(L.hcnn_ctx_query(h, 2))
         self.D = int(L.hcnn_ctx_query(h, 3))
-        variant = int(os.environ.get("HCNN_NTT_VARIANT", "0"))
-        if variant and self.N >= 1024:
-            _lib.check(L.hcnn_ctx_set_option(h, 1, variant), "hcnn_ctx_set_option")
+        variant = os.environ.get("HCNN_NTT_VARIANT")
+        if variant is not None and self.N >= 1024:
+            _lib.check(L.hcnn_ctx_set_option(h, 1, int(variant)), "hcnn_ctx_set_option")
         self._rlk_ref = None
         self._weights = {}
         self._finalizer = weakref.finalize(self, L.hcnn_ctx_destroy, h)
