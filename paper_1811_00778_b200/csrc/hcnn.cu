@@ -95,7 +95,7 @@ struct hcnn_ctx {
   bool rlk_reduce = false;
   uint8_t* ws = nullptr;
   size_t ws_bytes = 0;
-  size_t ws_limit = size_t(2) << 30;
+  size_t ws_limit = size_t(6) << 30;  // whole MNIST layers (800 cts at set 1) in one chunk
   int64_t launches = 0;
 
   uint8_t* workspace(size_t bytes) {
