@@ -640,6 +640,64 @@ __global__ void k_bfly_probe(uint32_t* out, uint32_t w, uint32_t ws, uint32_t p,
   if (acc == 0x9e3779b9u) out[0] = acc;
 }
 
+// Base-conversion dot products (kinds 13-15): per output j, sum_{i<11} x_i
+// c_ij mod p for 13 outputs, as in k_scale / k_extend.  13: lazy 64-bit
+// integer sums (IMAD.WIDE) + Montgomery REDC; 14: exact FP64 (c split into
+// 15-bit halves, two DFMA per term, fp64 reduction); 15: outputs alternate
+// between the two.  Counts dot products (of 11 terms).
+DI uint32_t dot_int(const uint32_t* x, const uint32_t* c, uint32_t p, uint32_t pinv) {
+  uint64_t a = 0;
+#pragma unroll
+  for (int i = 0; i < 11; ++i) a += (uint64_t)x[i] * c[i];
+  const uint32_t m = (uint32_t)a * pinv;
+  return (uint32_t)((a + (uint64_t)m * p) >> 32);
+}
+
+DI uint32_t dot_f64(const double* xd, const double* ch, const double* cl, double p, double pinv) {
+  double h = 0, l = 0;
+#pragma unroll
+  for (int i = 0; i < 11; ++i) {
+    h = fma(xd[i], ch[i], h);
+    l = fma(xd[i], cl[i], l);
+  }
+  const double qh = rint(h * pinv);
+  const double rh = fma(-qh, p, h);  // |rh| <= p
+  const double t = fma(rh, 32768.0, l);
+  const double q2 = rint(t * pinv);
+  double r = fma(-q2, p, t);
+  r = r < 0 ? r + p : r;
+  return (uint32_t)__double2loint(r + 4503599627370496.0);
+}
+
+template <int KIND>
+__global__ void k_dot_probe(uint32_t* out, uint32_t seed, int iters) {
+  const uint32_t p = 1073643521u, pinv = 0x3fff7fffu;
+  uint32_t x[11];
+  double xd[11];
+#pragma unroll
+  for (int i = 0; i < 11; ++i) x[i] = (seed * (threadIdx.x + 3 * i + 1) + blockIdx.x) & 0x3fffffff;
+  uint32_t acc = 0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 11; ++i) xd[i] = __hiloint2double(0x43300000, (int)x[i]) - 4503599627370496.0;
+#pragma unroll
+    for (int j = 0; j < 13; ++j) {
+      uint32_t c[11];
+      double ch[11], cl[11];
+#pragma unroll
+      for (int i = 0; i < 11; ++i) {
+        c[i] = (0x9e3779b9u * (i + 1) + 0x7f4a7c15u * j) & 0x3fffffff;
+        ch[i] = (double)(c[i] >> 15);
+        cl[i] = (double)(c[i] & 0x7fff);
+      }
+      const bool use_f = KIND == 14 || (KIND == 15 && (j & 1));
+      acc += use_f ? dot_f64(xd, ch, cl, (double)p, 1.0 / p) : dot_int(x, c, p, pinv);
+    }
+    x[it % 11] ^= acc;
+  }
+  if (acc == 0x12345u) out[0] = acc;
+}
+
 // IMAD.WIDE and DFMA interleaved (kind 7): whether the fp64 pipe runs beside
 // the integer multiplier; counts both kinds of operation
 __global__ void k_mix_peak(uint32_t* out, uint32_t a, double da, double db, int iters) {
@@ -781,6 +839,9 @@ int hcnn_int_peak(int device, int kind, double* ops_per_s) {
         case 9: k_bfly_peak<<<blocks / 4, tpb>>>(out, 123456789u, 493942125u, 1073643521u, iters); break;
         case 10: k_bfly_probe<10><<<blocks, tpb>>>(out, 123456789u, 493942125u, 1073643521u, 123456789.0 / 1073643521.0, iters); break;
         case 11: k_bfly_probe<11><<<blocks, tpb>>>(out, 123456789u, 493942125u, 1073643521u, 0.0, iters); break;
+        case 13: k_dot_probe<13><<<blocks, tpb>>>(out, 12345u, iters / 16); break;
+        case 14: k_dot_probe<14><<<blocks, tpb>>>(out, 12345u, iters / 16); break;
+        case 15: k_dot_probe<15><<<blocks, tpb>>>(out, 12345u, iters / 16); break;
         case 12: k_bfly_probe<12><<<blocks, tpb>>>(out, 123456789u, 493942125u, 1073643521u, 0.0, iters); break;
         default: k_int_peak<5><<<blocks, tpb>>>(out, 0x3e3779b1u, 12345u, iters); break;
       }
@@ -794,6 +855,7 @@ int hcnn_int_peak(int device, int kind, double* ops_per_s) {
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, e0, e1));
     *ops_per_s = 5.0 * (kind == 9 ? blocks / 4 : blocks) * tpb * (double)iters * 8 / (ms * 1e-3);
+    if (kind >= 13 && kind <= 15) *ops_per_s = 5.0 * blocks * tpb * (double)(iters / 16) * 13 / (ms * 1e-3);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaFree(out);

@@ -1,10 +1,11 @@
 """Timeline of engine.eval_network_stream (events on the three streams)."""
 import json
+import os
 import sys
 import time
 
 sys.argv = ["bench.py"]
-sys.path.insert(0, ".")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
 import bench

@@ -1,6 +1,7 @@
+import os
 import sys, time, json
 sys.argv = ["bench.py"]
-sys.path.insert(0, ".")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import bench
 from paper_1811_00778_b200 import engine as E
