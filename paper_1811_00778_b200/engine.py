@@ -803,6 +803,28 @@ class ChannelResult:
         self.residues[t] = logits
 
 
+def run_channels(images, model, crt_system, params_for_channel, keys_for_channel, rng, workers: int = 1,
+                 counter=None) -> ChannelResult:
+    """One evaluation per plaintext-CRT channel (engine.py:459-491), every step
+    on the GPU: slot encoding and encryption from the shared host rng (same
+    draw order as the reference), eval_network, exact decryption and slot
+    decoding.  Channels are independent; distributed.py deals them to ranks."""
+    batch = len(images)
+    moduli = tuple(getattr(crt_system, "moduli", crt_system))
+    result = ChannelResult(moduli=moduli, batch_size=batch)
+    for i, t in enumerate(moduli):
+        params = params_for_channel(i)
+        if params.t != t:
+            raise ParameterMismatchError(f"channel {i}: params t != system t")
+        sk, pk, rlk = keys_for_channel(i)
+        layout = PackingLayout(batch_size=batch, slot_count=params.ring_degree)
+        tensor = pack_images_device(images, layout, None, pk, params, rng, delta=model.spec.input_scale)
+        logits_ct = eval_network(tensor, reduce_model(model, t), rlk, params, counter, workers)
+        mat = unpack_tensor_device(logits_ct, sk, params, batch)  # (batch, outputs)
+        result.add(t, mat.T.copy())
+    return result
+
+
 def reconstruct_logits(result, crt_moduli) -> np.ndarray:
     """Signed logits from per-channel residues (engine.py:494-506)."""
     moduli = tuple(getattr(crt_moduli, "moduli", crt_moduli))
