@@ -1536,12 +1536,13 @@ int hcnn_fc(hcnn_ctx* c, const uint32_t* in, uint32_t* out, int n_in, int n_out,
       int S = (int)std::min<size_t>(64, std::max<size_t>(1, (8 * 148 + base_blocks - 1) / base_blocks));
       S = std::min(S, std::max(1, n_in / 32));
       int chunk = (n_in + S - 1) / S;
-      while ((size_t)obs * chunk * sizeof(double) > 64 * 1024) chunk = (chunk + 1) / 2;
+      const int obp = obs + (obs & 1);
+      while ((size_t)obp * chunk * sizeof(double) > 64 * 1024) chunk = (chunk + 1) / 2;
       S = (n_in + chunk - 1) / chunk;
       const size_t rows = (size_t)n_out * 2 * c->K;
       uint32_t* ws = S > 1 ? (uint32_t*)c->workspace((size_t)S * rows * c->N * sizeof(uint32_t)) : out;
       const dim3 gs(bx, 2 * c->K, (unsigned)(nob * S));
-      const size_t smem = (size_t)obs * chunk * sizeof(double);
+      const size_t smem = (size_t)obp * chunk * sizeof(double);
       switch (obs) {
 #define X(OBS)                                                                                             \
   case OBS: {                                                                                              \

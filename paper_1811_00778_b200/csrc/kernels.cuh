@@ -227,6 +227,17 @@ DI double u32_to_f64(uint32_t x) {  // exact, without a conversion instruction
   return __hiloint2double(0x43300000, (int)x) - 4503599627370496.0;
 }
 
+// CNT consecutive doubles from 16-byte aligned shared memory (CNT even)
+template <int CNT>
+DI void lds_pairs(double* w, const double* src) {
+#pragma unroll
+  for (int k = 0; k < CNT / 2; ++k) {
+    const double2 v = reinterpret_cast<const double2*>(src)[k];
+    w[2 * k] = v.x;
+    w[2 * k + 1] = v.y;
+  }
+}
+
 DI double fold_mod(double acc, double p, double pinv) {
   const double qd = floor(acc * pinv);
   return fma(-qd, p, acc);  // exact: |result| < 2p
@@ -404,13 +415,14 @@ __global__ void __launch_bounds__(128)
     k_fc_f64_split(const uint32_t* __restrict__ in, uint32_t* __restrict__ ws,
                    const double* __restrict__ wd, int n_in, int n_out, int K, int N, int flush,
                    int chunk, int nob_blocks, const uint32_t* __restrict__ primes) {
-  extern __shared__ double wsd[];  // [OB][chunk]
+  extern __shared__ double wsd[];  // [chunk][OBP]: an input's OB weights are one run of 16-byte loads
+  constexpr int OBP = OB + (OB & 1);
   const int ob = blockIdx.z % nob_blocks, split = blockIdx.z / nob_blocks;
   const int o0 = ob * OB;
   const int i0 = split * chunk, len = min(n_in, i0 + chunk) - i0;
-  for (int idx = threadIdx.x; idx < OB * chunk; idx += blockDim.x) {
-    const int o = idx / chunk, i = idx % chunk;
-    wsd[idx] = i < len ? wd[(size_t)(o0 + o) * n_in + i0 + i] : 0.0;
+  for (int idx = threadIdx.x; idx < OBP * chunk; idx += blockDim.x) {
+    const int i = idx / OBP, o = idx % OBP;
+    wsd[idx] = (i < len && o < OB) ? wd[(size_t)(o0 + o) * n_in + i0 + i] : 0.0;
   }
   __syncthreads();
   const int pair = blockIdx.x * blockDim.x + threadIdx.x;
@@ -434,11 +446,12 @@ __global__ void __launch_bounds__(128)
     for (int u = 0; u < U; ++u) {
       if (i + u >= len) break;
       const double x0 = u32_to_f64(xv[u].x), x1 = u32_to_f64(xv[u].y);
+      double wv[OBP];
+      lds_pairs<OBP>(wv, wsd + (i + u) * OBP);
 #pragma unroll
       for (int o = 0; o < OB; ++o) {
-        const double w = wsd[o * chunk + i + u];
-        acc[o][0] = fma(w, x0, acc[o][0]);
-        acc[o][1] = fma(w, x1, acc[o][1]);
+        acc[o][0] = fma(wv[o], x0, acc[o][0]);
+        acc[o][1] = fma(wv[o], x1, acc[o][1]);
       }
     }
     cnt += U;
