@@ -1541,7 +1541,7 @@ int hcnn_fc(hcnn_ctx* c, const uint32_t* in, uint32_t* out, int n_in, int n_out,
       S = (n_in + chunk - 1) / chunk;
       const size_t rows = (size_t)n_out * 2 * c->K;
       uint32_t* ws = S > 1 ? (uint32_t*)c->workspace((size_t)S * rows * c->N * sizeof(uint32_t)) : out;
-      const dim3 gs(bx, 2 * c->K, (unsigned)(nob * S));
+      const dim3 gs((unsigned)(nob * S), 2 * c->K, bx);  // output blocks fastest (L2 reuse of input slabs)
       const size_t smem = (size_t)obp * chunk * sizeof(double);
       switch (obs) {
 #define X(OBS)                                                                                             \

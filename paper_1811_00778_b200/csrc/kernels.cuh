@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-// Split-K dense layer: blockIdx.z = (output block, input split).  Each block
+// Split-K dense layer: blockIdx.x = (output block, input split), z = slab.  Each block
 // sums inputs [split*chunk, +chunk) for OB outputs of one (part, limb) over a
 // slab of 2 * blockDim coefficients (2 per thread, 8-byte loads) and writes
 // the reduced partial sum; k_fc_reduce adds the S partials mod p.  The block's
@@ -417,7 +417,9 @@ __global__ void __launch_bounds__(128)
                    int chunk, int nob_blocks, const uint32_t* __restrict__ primes) {
   extern __shared__ double wsd[];  // [chunk][OBP]: an input's OB weights are one run of 16-byte loads
   constexpr int OBP = OB + (OB & 1);
-  const int ob = blockIdx.z % nob_blocks, split = blockIdx.z / nob_blocks;
+  // output block fastest in the launch order: the blocks sharing one input
+  // slab run together and read it from L2, not DRAM, after the first
+  const int ob = blockIdx.x % nob_blocks, split = blockIdx.x / nob_blocks;
   const int o0 = ob * OB;
   const int i0 = split * chunk, len = min(n_in, i0 + chunk) - i0;
   for (int idx = threadIdx.x; idx < OBP * chunk; idx += blockDim.x) {
@@ -425,7 +427,7 @@ __global__ void __launch_bounds__(128)
     wsd[idx] = (i < len && o < OB) ? wd[(size_t)(o0 + o) * n_in + i0 + i] : 0.0;
   }
   __syncthreads();
-  const int pair = blockIdx.x * blockDim.x + threadIdx.x;
+  const int pair = blockIdx.z * blockDim.x + threadIdx.x;
   if (pair * 2 >= N) return;
   const int limb = blockIdx.y % K, part = blockIdx.y / K;
   const double p = (double)primes[limb];
