@@ -440,10 +440,18 @@ __global__ void __launch_bounds__(128)
                       (size_t)i0 * ct_stride;
   int cnt = 0;
   constexpr int U = 8;
+  // software-pipelined: the next U inputs are in flight while these are summed
+  uint2 nxt[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) nxt[u] = __ldg(base + (size_t)min(u, len - 1) * ct_stride);
   for (int i = 0; i < len; i += U) {
     uint2 xv[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) xv[u] = __ldg(base + (size_t)min(i + u, len - 1) * ct_stride);
+    for (int u = 0; u < U; ++u) xv[u] = nxt[u];
+    if (i + U < len) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) nxt[u] = __ldg(base + (size_t)min(i + U + u, len - 1) * ct_stride);
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (i + u >= len) break;
