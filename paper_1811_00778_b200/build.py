@@ -45,6 +45,8 @@ def _compile(args):
 
 def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> str:
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _newest_source():
+        if not os.path.exists(EXAMPLE) or os.path.getmtime(EXAMPLE) < os.path.getmtime(EXAMPLE + ".c"):
+            build_example()
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     units = [(os.path.join(CSRC, "hcnn.cu"), os.path.join(BUILD, "hcnn.o"), [])]
@@ -66,9 +68,25 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
+    build_example()
     if verbose:
         print(f"built {LIB}")
     return LIB
+
+
+EXAMPLE = os.path.join(os.path.dirname(PKG), "examples", "capi_hsquare")
+
+
+def build_example() -> str:
+    """examples/capi_hsquare: a plain C program calling the C ABI (gcc, linked
+    against the in-tree library with an $ORIGIN-relative rpath)."""
+    src = EXAMPLE + ".c"
+    cmd = ["gcc", "-O2", "-std=c11", "-I", os.path.join(os.path.dirname(PKG), "include"), src, "-o", EXAMPLE,
+           "-L", PKG, "-lhcnn_b200", "-Wl,-rpath,$ORIGIN/../paper_1811_00778_b200"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"gcc failed for {src}:\n{r.stderr[-4000:]}")
+    return EXAMPLE
 
 
 if __name__ == "__main__":

@@ -222,3 +222,26 @@ def test_hfir_relin_key_reader_matches_reference_keys():
         for part in range(2):
             got = O.ntt_forward(ctx, key.coeff[i, part].astype(np.int64))
             assert np.array_equal(got, a["rlk"][i, part].astype(np.int64))
+
+
+def test_plain_c_program_links_and_fails_loudly_without_a_gpu(tmp_path):
+    """The C example resolves the in-tree library; without a CUDA device the
+    first ABI call returns HCNN_ERR_CUDA (5) instead of computing anything."""
+    import struct
+    import subprocess
+
+    import torch
+
+    exe = os.path.join(ROOT, "examples", "capi_hsquare")
+    if not os.path.exists(exe):
+        pytest.skip("example not built")
+    ldd = subprocess.run(["ldd", exe], capture_output=True, text=True).stdout
+    assert "libhcnn_b200.so =>" in ldd and "not found" not in ldd
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: covered by the gpu test")
+    src = tmp_path / "in.bin"
+    with open(src, "wb") as fh:
+        fh.write(struct.pack("<IIIQI", 64, 1, 0, 257, 16))
+        fh.write(struct.pack("<Q", 1073643521))
+    r = subprocess.run([exe, str(src), str(tmp_path / "out.bin")], capture_output=True, text=True)
+    assert r.returncode == 5, (r.returncode, r.stderr)
