@@ -802,11 +802,11 @@ void layout_key(hcnn_ctx* c, const uint32_t* raw, int domain, size_t rows, uint3
 }
 
 void prepare_keys(hcnn_ctx* c) {
-  if (c->keys_variant == (c->variant & ~32)) return;
+  if (c->keys_variant == (c->variant & ~(32 | 512))) return;
   if (c->d_rlk_raw)
     layout_key(c, c->d_rlk_raw, c->rlk_domain, (size_t)c->D * 2 * c->K, &c->d_rlk, variant_mont(c, c->variant));
   if (c->d_pk_raw) layout_key(c, c->d_pk_raw, c->pk_domain, 2 * (size_t)c->K, &c->d_pk, 0);
-  c->keys_variant = c->variant & ~32;
+  c->keys_variant = c->variant & ~(32 | 512);
 }
 
 }  // namespace
@@ -985,7 +985,7 @@ int hcnn_ctx_set_option(hcnn_ctx* c, int key, int64_t value) {
       // geometry flags of the fused kernels (ntt_kernels.cuh): +16 one-row
       // relinearisation transforms, +32 square tensors on the radix-32 mixed
       // geometry, +64 mixed-width passes instead of a warp-shuffle tail
-      if (value & ~(int64_t)(16 | 32 | 64)) fail(HCNN_ERR_PARAM, "NTT variant flags are 16, 32 and 64");
+      if (value & ~(int64_t)(16 | 32 | 64 | 512)) fail(HCNN_ERR_PARAM, "NTT variant flags are 16, 32, 64 and 512");
       if ((value & (32 | 64)) && c->logN < 10) fail(HCNN_ERR_UNSUPPORTED, "mixed geometries need N >= 1024");
       c->variant = (int)value;
     } else {

@@ -1,0 +1,158 @@
+// NTT of one row split over a CLUSTER of two CTAs (N = 2^15): each CTA holds
+// half of the row in registers (512 threads x 32 residues, 128 registers per
+// thread, where one 1024-thread CTA would have only 64 and spill), and the
+// exchange between the two halves goes through distributed shared memory.
+//
+// Geometry: the radix-32 MIXED geometry (passes of 5 + 5 + 5 bits, no tail)
+// over T = 1024 VIRTUAL threads, vtid = rank * 512 + tid.  With those pass
+// maps the forward's first exchange sends half of every thread's residues to
+// the other CTA (the rank bit of the element index comes from the register
+// index) and the second exchange is CTA-local; the inverse mirrors that.
+// Each CTA's exchange buffer is COMPACT: the element index with the exchange's
+// rank bit squeezed out (2^14 words + padding), so two rows fit in 227 KB.
+// Barriers are cluster barriers (arrive.release / wait.acquire), one per
+// exchange with two alternating buffers.
+#pragma once
+#include "ntt.cuh"
+#include "tma.cuh"
+
+namespace hcnn {
+
+DI uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+DI void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// shared::cluster address of `local` (a shared::cta address) in CTA `rank`
+DI uint32_t map_rank(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+
+DI void st_cluster(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+// element index with bit RB removed
+template <int RB>
+DI int squeeze(int idx) {
+  return ((idx >> (RB + 1)) << RB) | (idx & ((1 << RB) - 1));
+}
+
+template <class G>
+struct ClusterGeom {
+  static_assert(G::MIXED && G::LOGE == 5 && G::LOGN == 15, "cluster NTT: 2^15 on the radix-32 mixed geometry");
+  static constexpr int TC = G::T / 2;                  // threads per CTA
+  static constexpr int HALF = G::N / 2;                // residues per CTA
+  static constexpr int XW = (HALF + 2 * (HALF >> 5) + 2 + 3) & ~3;  // padded compact row
+  __host__ __device__ static constexpr int smem_words(int nr) { return 2 * nr * XW; }
+};
+
+// Exchange between pass P_OUT (registers now) and P_IN (registers after): the
+// CTA that reads element idx in pass P_IN is bit RB of idx.  Writes go to that
+// CTA's buffer (through DSMEM when it is the other one), reads are local.
+template <class G, int P_OUT, int P_IN, int RB, int NR>
+DI void cluster_exchange(uint32_t* x, uint32_t* buf, int vtid, uint32_t rank) {
+  using C = ClusterGeom<G>;
+  const uint32_t base_local = smem_u32(buf);
+  const uint32_t base_other = map_rank(base_local, rank ^ 1u);
+  const uint32_t base_self = map_rank(base_local, rank);
+#pragma unroll
+  for (int r = 0; r < NR; ++r)
+#pragma unroll
+    for (int e = 0; e < G::E; ++e) {
+      const int idx = gpass_index<G, G::lo(P_OUT), G::kb(P_OUT)>(vtid, e);
+      const uint32_t dst = (uint32_t)((idx >> RB) & 1);
+      const uint32_t off = (uint32_t)(r * C::XW + sidx(squeeze<RB>(idx))) * 4u;
+      st_cluster((dst == rank ? base_self : base_other) + off, x[r * G::E + e]);
+    }
+  cluster_sync_all();
+#pragma unroll
+  for (int r = 0; r < NR; ++r)
+#pragma unroll
+    for (int e = 0; e < G::E; ++e)
+      x[r * G::E + e] = buf[r * C::XW + sidx(squeeze<RB>(gpass_index<G, G::lo(P_IN), G::kb(P_IN)>(vtid, e)))];
+}
+
+// rank bit of the element index in pass P's map: the top virtual-thread bit
+// lands at bit LOGT - 1 below lo(P), else LOGT - 1 + kb(P)
+template <class G, int P>
+__host__ __device__ constexpr int rank_bit() {
+  return (G::LOGT - 1) < G::lo(P) ? (G::LOGT - 1) : (G::LOGT - 1 + G::kb(P));
+}
+
+// Forward: natural layout in (values < 4p), spectral layout out, reduced to
+// [0, p) (FULL) or [0, 2p).  s: ClusterGeom::smem_words(NR) words.
+template <class G, int NR = 1, bool FULL = true>
+DI void ntt_fwd_cl(uint32_t* x, uint32_t* s, const uint2* __restrict__ tw, uint32_t p, int vtid,
+                   uint32_t rank) {
+  using C = ClusterGeom<G>;
+  fwd_stage<G, G::lo(0), G::kb(0), 0, NR>(x, tw, p, vtid);
+  cluster_exchange<G, 0, 1, rank_bit<G, 1>(), NR>(x, s, vtid, rank);
+  fwd_stage<G, G::lo(1), G::kb(1), 0, NR>(x, tw, p, vtid);
+  cluster_exchange<G, 1, 2, rank_bit<G, 2>(), NR>(x, s + NR * C::XW, vtid, rank);
+  fwd_stage<G, G::lo(2), G::kb(2), 0, NR>(x, tw, p, vtid);
+  const uint32_t p2 = 2 * p;
+#pragma unroll
+  for (int e = 0; e < NR * G::E; ++e) {
+    const uint32_t v = umin32(x[e], x[e] - p2);
+    x[e] = FULL ? umin32(v, v - p) : v;
+  }
+}
+
+// Inverse: spectral layout in (values < 2p), natural layout out, scaled by
+// sc (folded into the last stage), reduced to [0, p).
+template <class G, int NR = 1>
+DI void ntt_inv_cl(uint32_t* x, uint32_t* s, const uint2* __restrict__ itw, uint32_t p, const InvScale& sc,
+                   int vtid, uint32_t rank) {
+  using C = ClusterGeom<G>;
+  inv_stage<G, G::lo(2), G::kb(2), G::kb(2) - 1, NR>(x, itw, p, vtid, sc);
+  cluster_exchange<G, 2, 1, rank_bit<G, 1>(), NR>(x, s, vtid, rank);
+  inv_stage<G, G::lo(1), G::kb(1), G::kb(1) - 1, NR>(x, itw, p, vtid, sc);
+  cluster_exchange<G, 1, 0, rank_bit<G, 0>(), NR>(x, s + NR * C::XW, vtid, rank);
+  inv_stage<G, G::lo(0), G::kb(0), G::kb(0) - 1, NR>(x, itw, p, vtid, sc);
+}
+
+// Rows of N = 2^15 residues, one cluster of two CTAs per row (grid.x = 2 rows):
+// like k_ntt_rows (inverse: 0 forward to spectral positions, 1 inverse, 2
+// forward to the tiled layout).
+template <class G>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G::T / 2, 1)
+    k_ntt_rows_cl(uint32_t* __restrict__ data, int limbs, int prime_off, int inverse, NttTabs nt) {
+  extern __shared__ __align__(16) uint32_t s[];
+  const uint32_t rank = cluster_rank();
+  const int vtid = (int)rank * ClusterGeom<G>::TC + threadIdx.x;
+  const int row = blockIdx.x / 2;
+  const int j = prime_off + row % limbs;
+  uint32_t* r = data + (size_t)row * G::N;
+  const uint32_t p = nt.prime[j];
+  uint32_t x[G::E];
+  cluster_sync_all();  // both CTAs running before any DSMEM store
+  if (inverse == 1) {
+#pragma unroll
+    for (int e = 0; e < G::E; ++e) x[e] = r[spectral_index<G>(vtid, e)];
+    ntt_inv_cl<G>(x, s, nt.itw + (size_t)j * G::N, p, inv_scale(nt, j, false), vtid, rank);
+#pragma unroll
+    for (int e = 0; e < G::E; ++e) r[natural_index<G>(vtid, e)] = x[e];
+  } else {
+#pragma unroll
+    for (int e = 0; e < G::E; ++e) x[e] = r[natural_index<G>(vtid, e)];
+    ntt_fwd_cl<G>(x, s, nt.tw + (size_t)j * G::N, p, vtid, rank);
+    if (inverse == 2) {
+#pragma unroll
+      for (int e = 0; e < G::E; ++e) r[tiled_index<G>(vtid, e)] = x[e];
+    } else {
+#pragma unroll
+      for (int e = 0; e < G::E; ++e) r[spectral_index<G>(vtid, e)] = x[e];
+    }
+  }
+  // (every DSMEM store precedes a cluster barrier both CTAs pass: no exit sync)
+}
+
+}  // namespace hcnn

@@ -13,6 +13,7 @@
 
 #include "common.cuh"
 #include "ntt.cuh"
+#include "ntt_cluster.cuh"
 #include "tma.cuh"
 
 namespace hcnn {
@@ -640,8 +641,25 @@ cudaError_t launch_tensor_sq(const NttLaunch& a) {
 
 // The key layout (tiled, Montgomery or not) follows the geometry and the
 // relinearisation kernel, so keys are laid out per variant.
+// variant bit: N = 2^15 NTT rows on 2-CTA clusters (ntt_cluster.cuh)
+constexpr int CLUSTER_ROWS = 512;
+
 template <int LOGN>
 cudaError_t ntt_launch(int op, const NttLaunch& a) {
+  if constexpr (LOGN == 15) {
+    if (op == 0 && (a.variant & CLUSTER_ROWS)) {
+      using GC = NttGeom<15, 5, false, true>;
+      constexpr int smem = ClusterGeom<GC>::smem_words(1) * sizeof(uint32_t);
+      static bool cfg = false;
+      if (!cfg) {
+        cudaFuncSetAttribute(k_ntt_rows_cl<GC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cfg = true;
+      }
+      k_ntt_rows_cl<GC><<<dim3(2 * a.grid.x), GC::T / 2, smem, a.stream>>>(a.rows, a.limbs, a.prime_off,
+                                                                           a.inverse, a.nt);
+      return cudaGetLastError();
+    }
+  }
   if constexpr (LOGN >= 10) {
     if (op == 1 && a.square && (a.variant & TENSOR_MIXED)) return launch_tensor_sq<NttGeom<LOGN, 5, false, true>>(a);
     if (a.variant & MIXED_PASSES) return launch_with<NttGeom<LOGN, pick_loge(LOGN), false, true>>(op, a);
