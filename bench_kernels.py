@@ -35,6 +35,12 @@ def primes_1mod(two_n: int, count: int, avoid=()):
     return out
 
 
+def _lib_query(g, what):
+    from paper_1811_00778_b200 import _lib
+
+    return _lib.lib().hcnn_ctx_query(g.handle, what)
+
+
 def main():
     import torch
 
@@ -47,7 +53,8 @@ def main():
     ap.add_argument("--ks", default="6,11,12")
     ap.add_argument("--cts", type=int, default=128)
     ap.add_argument("--rows", type=int, default=4096)
-    ap.add_argument("--variants", default="0")
+    ap.add_argument("--variants", default="default",
+                    help="comma list of hcnn_ctx_set_option NTT flags; 'default' = the library's per-N choice")
     ap.add_argument("--reps", type=int, default=3)
     a = ap.parse_args()
     t = 5522259017729
@@ -56,8 +63,11 @@ def main():
             primes = list(POOL[:k]) if n <= 16384 else primes_1mod(2 * n, k)
             tt = t if (t - 1) % (2 * n) == 0 else 65537 if n <= 32768 else 65537
             params = B.BfvParams(B.RnsContext(n, primes), tt)
-            for variant in [int(v) for v in a.variants.split(",")]:
-                os.environ["HCNN_NTT_VARIANT"] = str(variant)
+            for variant in a.variants.split(","):
+                if variant == "default":
+                    os.environ.pop("HCNN_NTT_VARIANT", None)
+                else:
+                    os.environ["HCNN_NTT_VARIANT"] = str(int(variant))
                 E._CTXS.clear()
                 g = E.context_for(params)
                 sk, pk, rlk = B.keygen(params, np.random.default_rng(1))
@@ -80,7 +90,8 @@ def main():
                 g.profile(False)
                 logn = n.bit_length() - 1
                 bfly = n // 2 * logn
-                line = {"n": n, "k": k, "kp": g.KP, "digits": g.D, "variant": variant, "cts": a.cts,
+                line = {"n": n, "k": k, "kp": g.KP, "digits": g.D,
+                        "variant": int(_lib_query(g, 7)), "cts": a.cts,
                         "ntt_rows": a.rows}
                 cnt, tot = prof["k_ntt_rows"]
                 per = tot / cnt  # ms per launch (fwd or inv of `rows` rows)

@@ -641,23 +641,39 @@ cudaError_t launch_tensor_sq(const NttLaunch& a) {
 
 // The key layout (tiled, Montgomery or not) follows the geometry and the
 // relinearisation kernel, so keys are laid out per variant.
-// variant bit: N = 2^15 NTT rows on 2-CTA clusters (ntt_cluster.cuh)
+// variant bit (default at N = 2^15): relinearisation on 2-CTA clusters
+// (ntt_cluster.cuh) with keys in the radix-32 mixed layout
 constexpr int CLUSTER_ROWS = 512;
 
 template <int LOGN>
 cudaError_t ntt_launch(int op, const NttLaunch& a) {
   if constexpr (LOGN == 15) {
-    if (op == 0 && (a.variant & CLUSTER_ROWS)) {
+    if (a.variant & CLUSTER_ROWS) {
+      // rows and relinearisation on 2-CTA clusters; the key-layout kernels on
+      // the same (radix-32 mixed) geometry; the tensor keeps the default one
       using GC = NttGeom<15, 5, false, true>;
       constexpr int smem = ClusterGeom<GC>::smem_words(1) * sizeof(uint32_t);
       static bool cfg = false;
       if (!cfg) {
         cudaFuncSetAttribute(k_ntt_rows_cl<GC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_relin_cl<GC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cfg = true;
       }
-      k_ntt_rows_cl<GC><<<dim3(2 * a.grid.x), GC::T / 2, smem, a.stream>>>(a.rows, a.limbs, a.prime_off,
-                                                                           a.inverse, a.nt);
-      return cudaGetLastError();
+      if (op == 0 && a.inverse == 2) {  // forward to the tiled key layout of GC
+        k_ntt_rows_cl<GC><<<dim3(2 * a.grid.x), GC::T / 2, smem, a.stream>>>(a.rows, a.limbs, a.prime_off,
+                                                                             a.inverse, a.nt);
+        return cudaGetLastError();
+      }
+      if (op == 2) {
+        if (a.rlk_mont != 1) return cudaErrorInvalidValue;
+        k_relin_cl<GC><<<dim3(2 * a.grid.x, a.grid.y), GC::T / 2, smem, a.stream>>>(
+            a.dig, a.y3, a.rlk, a.out, a.K, a.D, a.reduce_digits, a.nt);
+        return cudaGetLastError();
+      }
+      // rows in the spectral / natural layouts and the tensor: the one-CTA
+      // kernels (faster there); everything that reads tiled keys: GC
+      if (op == 0 || op == 1) return launch_with<NttGeom<LOGN>>(op, a);
+      return launch_with<GC>(op, a);
     }
   }
   if constexpr (LOGN >= 10) {
@@ -674,6 +690,9 @@ int mont_of(int v) { return relin_acc64<G>((v & RELIN_SINGLE) != 0) ? 0 : 1; }
 // does variant v use Montgomery-form rlk?
 template <int LOGN>
 int ntt_variant_mont(int v) {
+  if constexpr (LOGN == 15) {
+    if (v & CLUSTER_ROWS) return 1;  // k_relin_cl: Montgomery-form keys
+  }
   if constexpr (LOGN >= 10) {
     if (v & MIXED_PASSES) return mont_of<NttGeom<LOGN, pick_loge(LOGN), false, true>>(v);
   }
