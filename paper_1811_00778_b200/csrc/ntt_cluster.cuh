@@ -156,20 +156,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G::T / 2, 1)
   // (every DSMEM store precedes a cluster barrier both CTAs pass: no exit sync)
 }
 
+// ---- TMEM as accumulator storage (the relinearisation's 2 x 32 running sums
+// per thread would not fit beside a 32-residue row in 128 registers).  One
+// warp allocates 256 columns; warp w uses lanes 32 (w % 4) + lane and columns
+// 64 (w / 4) + [0, 64): part 0 in the first 32, part 1 in the next 32.
+DI void tmem_alloc256(uint32_t* slot) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(slot)) : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+DI void tmem_dealloc256(uint32_t base) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(base) : "memory");
+}
+
+DI void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+DI void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+DI void tmem_ld16(uint32_t addr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+DI void tmem_st16(uint32_t addr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16};" ::"r"(addr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
 // Relinearisation (bfv.py:368-404) at N = 2^15 on 2-CTA clusters: one cluster
 // per (ct, prime of q); each digit row goes through the cluster forward NTT
 // and is multiply-accumulated with the key (tiled layout of G, Montgomery
-// form) into u32 accumulators in [0, 2p); the two parts then go through the
-// cluster inverse and are added to (y0, y1).  Digits are read straight from
-// global memory.  grid: (2 K, B).  (Measured: 55 vs 60 us per ciphertext for
-// the one-CTA 1024-thread kernel; both spill, this one less.)
+// form) into u32 accumulators in [0, 2p) held in TMEM; the two parts then go
+// through the cluster inverse and are added to (y0, y1).  Digits are read
+// straight from global memory.  grid: (2 K, B).
 template <class G>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G::T / 2, 1)
     k_relin_cl(const uint32_t* __restrict__ dig, const uint32_t* __restrict__ y3,
                const uint32_t* __restrict__ rlk, uint32_t* __restrict__ out, int K, int D,
                int reduce_digits, NttTabs nt) {
   extern __shared__ __align__(16) uint32_t s[];
+  __shared__ uint32_t tmem_slot;
   constexpr int E = G::E;
+  static_assert(E == 32 && G::T / 2 == 512, "TMEM plan: 16 warps x 32 lanes x 64 columns");
   const uint32_t rank = cluster_rank();
   const int vtid = (int)rank * ClusterGeom<G>::TC + threadIdx.x;
   const int j = blockIdx.x / 2;
@@ -179,9 +216,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G::T / 2, 1)
   const uint32_t pinv = nt.pinv[j];
   const uint32_t p2 = 2 * p;
   const uint2* tw = nt.tw + (size_t)j * G::N;
-  uint32_t acc[2][E];
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tmem_alloc256(&tmem_slot);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tacc = tmem_slot + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(warp >> 2) * 64;
+  {
+    uint32_t z[16];
 #pragma unroll
-  for (int e = 0; e < E; ++e) acc[0][e] = acc[1][e] = 0;
+    for (int e = 0; e < 16; ++e) z[e] = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tmem_st16(tacc + 16 * c, z);
+  }
   const uint32_t* dig_ct = dig + ct * D * G::N;
   cluster_sync_all();  // both CTAs running before any DSMEM store
   for (int i = 0; i < D; ++i) {
@@ -197,14 +244,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G::T / 2, 1)
     for (int part = 0; part < 2; ++part) {
       const uint4* kr = reinterpret_cast<const uint4*>(rlk + ((size_t)(i * 2 + part) * K + j) * G::N) + vtid;
 #pragma unroll
-      for (int c = 0; c < E / 4; ++c) {
-        const uint4 kv = __ldg(&kr[c * G::T]);
-        const uint32_t k4[4] = {kv.x, kv.y, kv.z, kv.w};
+      for (int h = 0; h < 2; ++h) {  // 16 accumulators at a time
+        uint32_t a[16];
+        tmem_ld16(tacc + part * 32 + h * 16, a);
 #pragma unroll
-        for (int l = 0; l < 4; ++l) {
-          const uint32_t v = acc[part][4 * c + l] + mont_mul(x[4 * c + l], k4[l], p, pinv);
-          acc[part][4 * c + l] = umin32(v, v - p2);
+        for (int c = 0; c < 4; ++c) {
+          const uint4 kv = __ldg(&kr[(h * 4 + c) * G::T]);
+          const uint32_t k4[4] = {kv.x, kv.y, kv.z, kv.w};
+#pragma unroll
+          for (int l = 0; l < 4; ++l) {
+            const uint32_t v = a[4 * c + l] + mont_mul(x[16 * h + 4 * c + l], k4[l], p, pinv);
+            a[4 * c + l] = umin32(v, v - p2);
+          }
         }
+        tmem_st16(tacc + part * 32 + h * 16, a);
       }
     }
   }
@@ -212,15 +265,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G::T / 2, 1)
   const InvScale ninv = inv_scale(nt, j, false);
 #pragma unroll
   for (int part = 0; part < 2; ++part) {
-    ntt_inv_cl<G>(acc[part], s, itw, p, ninv, vtid, rank);
+    uint32_t x[E];
+    tmem_ld16(tacc + part * 32, x);
+    tmem_ld16(tacc + part * 32 + 16, x + 16);
+    ntt_inv_cl<G>(x, s, itw, p, ninv, vtid, rank);
     const uint32_t* yr = y3 + ((ct * 3 + part) * K + j) * G::N;
     uint32_t* o = out + ((ct * 2 + part) * K + j) * G::N;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int idx = natural_index<G>(vtid, e);
-      o[idx] = add_mod(acc[part][e], yr[idx], p);
+      o[idx] = add_mod(x[e], yr[idx], p);
     }
   }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  if (warp == 0) tmem_dealloc256(tmem_slot);
 }
 
 }  // namespace hcnn
