@@ -263,7 +263,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G::T / 2, 1)
   }
   const uint2* itw = nt.itw + (size_t)j * G::N;
   const InvScale ninv = inv_scale(nt, j, false);
-#pragma unroll
+#pragma unroll 1
   for (int part = 0; part < 2; ++part) {
     uint32_t x[E];
     tmem_ld16(tacc + part * 32, x);
