@@ -298,14 +298,40 @@ struct RelinSmem {
 // Digits go through the forward NTT NR at a time (a single one first when the
 // count is odd); ACC64: lazy 64-bit accumulators (reduced before 16 products
 // pile up); otherwise u32 accumulators in [0, 2p) fed by Montgomery products.
-template <class G, bool ACC64, int NR>
+// TM: the running sums live in TMEM instead of registers (E = 16: one
+// 32x32b.x16 load / store per part and digit group; warp w uses lanes
+// 32 (w % 4) + lane and columns 2E (w / 4) + [0, 2E)).
+template <class G>
+__host__ __device__ constexpr uint32_t relin_tmem_cols() {
+  return 2 * G::E * (G::T / 128) <= 128 ? 128 : 2 * G::E * (G::T / 128) <= 256 ? 256 : 512;
+}
+
+DI void tmem_alloc_cols(uint32_t* slot, uint32_t cols) {
+  if (cols == 128)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(slot)) : "memory");
+  else if (cols == 256)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(slot)) : "memory");
+  else
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(slot)) : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+DI void tmem_dealloc_cols(uint32_t base, uint32_t cols) {
+  if (cols == 128) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(base) : "memory");
+  else if (cols == 256) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(base) : "memory");
+  else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(base) : "memory");
+}
+
+template <class G, bool ACC64, int NR, bool TM = false>
 __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
     k_relin(const uint32_t* __restrict__ dig, const uint32_t* __restrict__ y3,
             const uint32_t* __restrict__ rlk, uint32_t* __restrict__ out, int K, int D,
             int reduce_digits, NttTabs nt) {
   using SM = RelinSmem<G, NR>;
   constexpr int E = G::E;
+  static_assert(!TM || (E == 16 && !ACC64), "TMEM running sums: E = 16, Montgomery accumulators");
   extern __shared__ __align__(16) uint32_t s[];
+  __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x;
   const int j = blockIdx.x;
   const size_t ct = blockIdx.y;
@@ -315,9 +341,24 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
   const uint32_t p2 = 2 * p;
   const uint2* tw = nt.tw + (size_t)j * G::N;
   using Acc = typename std::conditional<ACC64, uint64_t, uint32_t>::type;
-  Acc acc0[E], acc1[E];
+  Acc acc0[TM ? 1 : E], acc1[TM ? 1 : E];
+  uint32_t tacc = 0;
+  if constexpr (TM) {
+    const int warp = tid >> 5;
+    if (warp == 0) tmem_alloc_cols(&tmem_slot, relin_tmem_cols<G>());
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    tacc = tmem_slot + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(warp >> 2) * 2 * E;
+    uint32_t z[16];
 #pragma unroll
-  for (int e = 0; e < E; ++e) acc0[e] = acc1[e] = 0;
+    for (int e = 0; e < 16; ++e) z[e] = 0;
+    tmem_st16(tacc, z);
+    tmem_st16(tacc + E, z);
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc0[e] = acc1[e] = 0;
+  }
 
   const uint32_t* dig_ct = dig + ct * D * G::N;
   auto krow = [&](int i, int part) { return rlk + ((size_t)(i * 2 + part) * K + j) * G::N; };
@@ -377,7 +418,8 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
       // Montgomery reduction per pair; keys streamed 16 bytes at a time
 #pragma unroll
       for (int part = 0; part < 2; ++part) {
-        Acc* acc = part ? acc1 : acc0;
+        uint32_t ta[TM ? E : 1];
+        if constexpr (TM) tmem_ld16(tacc + part * E, ta);
         const uint4* k0 = reinterpret_cast<const uint4*>(krow(i, part)) + tid;
         const uint4* k1 = reinterpret_cast<const uint4*>(krow(i + 1, part)) + tid;
 #pragma unroll
@@ -389,26 +431,44 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
           for (int l = 0; l < 4; ++l) {
             const int e = 4 * c + l;
             const uint32_t m = redc64((uint64_t)x[e] * ku[l] + (uint64_t)x[E + e] * kv[l], p, pinv);
-            const uint32_t sum = (uint32_t)acc[e] + m;
-            acc[e] = umin32(sum, sum - p2);
+            if constexpr (TM) {
+              const uint32_t sum = ta[e] + m;
+              ta[e] = umin32(sum, sum - p2);
+            } else {
+              Acc* acc = part ? acc1 : acc0;
+              const uint32_t sum = (uint32_t)acc[e] + m;
+              acc[e] = umin32(sum, sum - p2);
+            }
           }
         }
+        if constexpr (TM) tmem_st16(tacc + part * E, ta);
       }
     } else {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
 #pragma unroll
       for (int part = 0; part < 2; ++part) {
-        Acc* acc = part ? acc1 : acc0;
         uint32_t k[E];
         load_tiled<G>(k, krow(i + r, part), tid);
+        if constexpr (TM) {
+          uint32_t ta[E];
+          tmem_ld16(tacc + part * E, ta);
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-          if constexpr (ACC64) {
-            acc[e] += (uint64_t)x[r * E + e] * k[e];
-          } else {
-            const uint32_t v = acc[e] + mont_mul(x[r * E + e], k[e], p, pinv);
-            acc[e] = umin32(v, v - p2);
+          for (int e = 0; e < E; ++e) {
+            const uint32_t v = ta[e] + mont_mul(x[r * E + e], k[e], p, pinv);
+            ta[e] = umin32(v, v - p2);
+          }
+          tmem_st16(tacc + part * E, ta);
+        } else {
+          Acc* acc = part ? acc1 : acc0;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            if constexpr (ACC64) {
+              acc[e] += (uint64_t)x[r * E + e] * k[e];
+            } else {
+              const uint32_t v = acc[e] + mont_mul(x[r * E + e], k[e], p, pinv);
+              acc[e] = umin32(v, v - p2);
+            }
           }
         }
       }
@@ -442,14 +502,23 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
   const InvScale ninv = inv_scale(nt, j, false);
   // both parts through the inverse (in lockstep when NR = 2)
   uint32_t x[2 * E];
+  if constexpr (TM) {
+    tmem_ld16(tacc, x);
+    tmem_ld16(tacc + E, x + E);
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if ((tid >> 5) == 0) tmem_dealloc_cols(tmem_slot, relin_tmem_cols<G>());
+  } else {
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    if constexpr (ACC64) {
-      x[e] = reduce64(acc0[e], p, mu);
-      x[E + e] = reduce64(acc1[e], p, mu);
-    } else {  // in [0, 2p): valid inverse input
-      x[e] = acc0[e];
-      x[E + e] = acc1[e];
+    for (int e = 0; e < E; ++e) {
+      if constexpr (ACC64) {
+        x[e] = reduce64(acc0[e], p, mu);
+        x[E + e] = reduce64(acc1[e], p, mu);
+      } else {  // in [0, 2p): valid inverse input
+        x[e] = acc0[e];
+        x[E + e] = acc1[e];
+      }
     }
   }
   if constexpr (NR == 2) {
@@ -569,12 +638,27 @@ void configure_smem() {
 // variant: bits 0-3 = log2 E of the fused kernels (0 = default geometry);
 // RELIN_SINGLE = one-row relinearisation transforms
 constexpr int RELIN_SINGLE = 16;
+// relinearisation running sums in TMEM instead of registers
+constexpr int RELIN_TMEM = 1024;
 
 template <class G, bool SINGLE>
 cudaError_t launch_relin(const NttLaunch& a) {
   constexpr int NR = relin_nr<G>(SINGLE);
   constexpr bool ACC64 = relin_acc64<G>(SINGLE);
   if (a.rlk_mont != (ACC64 ? 0 : 1)) return cudaErrorInvalidValue;
+  if constexpr (!ACC64 && G::E == 16) {
+    if (a.variant & RELIN_TMEM) {
+      static bool cfg = false;
+      if (!cfg) {
+        cudaFuncSetAttribute(k_relin<G, false, NR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             RelinSmem<G, NR>::BYTES);
+        cfg = true;
+      }
+      k_relin<G, false, NR, true><<<a.grid, G::T, RelinSmem<G, NR>::BYTES, a.stream>>>(
+          a.dig, a.y3, a.rlk, a.out, a.K, a.D, a.reduce_digits, a.nt);
+      return cudaSuccess;
+    }
+  }
   k_relin<G, ACC64, NR><<<a.grid, G::T, RelinSmem<G, NR>::BYTES, a.stream>>>(
       a.dig, a.y3, a.rlk, a.out, a.K, a.D, a.reduce_digits, a.nt);
   return cudaSuccess;
