@@ -1476,11 +1476,10 @@ int hcnn_conv(hcnn_ctx* c, const uint32_t* in, uint32_t* out, int h, int w, int 
       switch (fb) {
 #define X(FB)                                                                                           \
   case FB: {                                                                                            \
-    static bool cfg = false;                                                                            \
-    if (!cfg) {                                                                                         \
+    static std::atomic<uint64_t> cfg{0};                                                                \
+    per_device_once(cfg, [] {                                                                           \
       cudaFuncSetAttribute(k_conv_f64<FB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);     \
-      cfg = true;                                                                                       \
-    }                                                                                                   \
+    });                                                                                                 \
     k_conv_f64<FB><<<gridp, tpb, smem_d, c->stream>>>(in, out, wt->wd, g, (int)c->K, (int)c->N, wt->flush, c->d_prime); \
     break;                                                                                              \
   }
@@ -1549,11 +1548,10 @@ int hcnn_fc(hcnn_ctx* c, const uint32_t* in, uint32_t* out, int n_in, int n_out,
       switch (obs) {
 #define X(OBS)                                                                                             \
   case OBS: {                                                                                              \
-    static bool cfg = false;                                                                               \
-    if (!cfg) {                                                                                            \
+    static std::atomic<uint64_t> cfg{0};                                                                   \
+    per_device_once(cfg, [] {                                                                              \
       cudaFuncSetAttribute(k_fc_f64_split<OBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);   \
-      cfg = true;                                                                                          \
-    }                                                                                                      \
+    });                                                                                                    \
     k_fc_f64_split<OBS><<<gs, tpb, smem, c->stream>>>(in, ws, wt->wd, n_in, n_out, (int)c->K, (int)c->N,   \
                                                       wt->flush, chunk, nob, c->d_prime);                  \
     break;                                                                                                 \

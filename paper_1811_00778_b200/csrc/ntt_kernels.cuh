@@ -9,6 +9,7 @@
 //   k_mul_plain     ct x plaintext polynomial, NTT path           (bfv.py:301-318)
 //   k_ref_to_tiled  reference-order NTT keys -> device tiled layout
 #pragma once
+#include <atomic>
 #include <type_traits>
 
 #include "common.cuh"
@@ -620,6 +621,18 @@ __global__ void k_to_mont(uint32_t* __restrict__ rows, int limbs, NttTabs nt) {
   }
 }
 
+// Kernel attributes (dynamic smem opt-in) are per device: run `fn` once per
+// device the process launches on (a 64-bit mask of device ordinals).
+template <class Fn>
+inline void per_device_once(std::atomic<uint64_t>& done, Fn fn) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  fn();
+  done.fetch_or(bit, std::memory_order_release);
+}
+
 template <class G>
 void configure_smem() {
   const int smem = G::ntt_smem_words(1) * sizeof(uint32_t);
@@ -648,12 +661,11 @@ cudaError_t launch_relin(const NttLaunch& a) {
   if (a.rlk_mont != (ACC64 ? 0 : 1)) return cudaErrorInvalidValue;
   if constexpr (!ACC64 && G::E == 16) {
     if (a.variant & RELIN_TMEM) {
-      static bool cfg = false;
-      if (!cfg) {
+      static std::atomic<uint64_t> cfg{0};
+      per_device_once(cfg, [] {
         cudaFuncSetAttribute(k_relin<G, false, NR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              RelinSmem<G, NR>::BYTES);
-        cfg = true;
-      }
+      });
       k_relin<G, false, NR, true><<<a.grid, G::T, RelinSmem<G, NR>::BYTES, a.stream>>>(
           a.dig, a.y3, a.rlk, a.out, a.K, a.D, a.reduce_digits, a.nt);
       return cudaSuccess;
@@ -666,11 +678,8 @@ cudaError_t launch_relin(const NttLaunch& a) {
 
 template <class G>
 cudaError_t launch_with(int op, const NttLaunch& a) {
-  static bool configured = false;
-  if (!configured) {
-    configure_smem<G>();
-    configured = true;
-  }
+  static std::atomic<uint64_t> configured{0};
+  per_device_once(configured, [] { configure_smem<G>(); });
   const size_t smem = G::ntt_smem_words(1) * sizeof(uint32_t);
   switch (op) {
     case 0:
@@ -713,12 +722,11 @@ constexpr int MIXED_PASSES = 64;
 
 template <class G>
 cudaError_t launch_tensor_sq(const NttLaunch& a) {
-  static bool configured = false;
+  static std::atomic<uint64_t> configured{0};
   constexpr int smem = tensor_sq_smem_words<G>() * sizeof(uint32_t);
-  if (!configured) {
+  per_device_once(configured, [] {
     cudaFuncSetAttribute(k_tensor_sq<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    configured = true;
-  }
+  });
   k_tensor_sq<G><<<a.grid, G::T, smem, a.stream>>>(a.a, a.ae, a.d, a.K, a.KP, a.nt);
   return cudaGetLastError();
 }
@@ -737,12 +745,11 @@ cudaError_t ntt_launch(int op, const NttLaunch& a) {
       // the same (radix-32 mixed) geometry; the tensor keeps the default one
       using GC = NttGeom<15, 5, false, true>;
       constexpr int smem = ClusterGeom<GC>::smem_words(1) * sizeof(uint32_t);
-      static bool cfg = false;
-      if (!cfg) {
+      static std::atomic<uint64_t> cfg{0};
+      per_device_once(cfg, [] {
         cudaFuncSetAttribute(k_ntt_rows_cl<GC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(k_relin_cl<GC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cfg = true;
-      }
+      });
       if (op == 0 && a.inverse == 2) {  // forward to the tiled key layout of GC
         k_ntt_rows_cl<GC><<<dim3(2 * a.grid.x), GC::T / 2, smem, a.stream>>>(a.rows, a.limbs, a.prime_off,
                                                                              a.inverse, a.nt);
