@@ -460,7 +460,8 @@ def run_ours(args):
                 "path": ("pinned host u32 ciphertexts -> distributed.eval_network_groups (every rank uploads the batch) -> "
                          "pinned host logits on rank 0") if groups else
                         "pinned host u32 ciphertexts -> engine.eval_network_stream (upload of step s+1 overlaps "
-                        "evaluation of step s; two device input buffers) -> pinned host logits", "steps": e2e_steps},
+                        "evaluation of step s; two device input buffers; the first batch streamed by row bands into "
+                        "conv1 + square1) -> pinned host logits", "steps": e2e_steps},
         "gpu_launches": int(launches),
         "kernels": kernels,
         "roofline": roof,

@@ -144,8 +144,14 @@ class GpuContext:
         return torch.empty((n, parts, self.K, self.N), dtype=torch.int32, device=f"cuda:{self.device}")
 
     def set_variant(self, variant: int):
-        """Geometry flags of the fused kernels (0 default; 16 one-row relinearisation, 32 radix-32 square tensor, 64 mixed-width passes)."""
+        """Geometry flags of the fused kernels (include/hcnn_b200.h: 16 one-row
+        relinearisation, 32 radix-32 square tensor, 64 mixed-width passes, 512
+        2-CTA cluster rows at 2^15, 1024 relinearisation sums in TMEM)."""
         _lib.check(_lib.lib().hcnn_ctx_set_option(self.handle, 1, int(variant)), "ntt variant")
+
+    def variant(self) -> int:
+        """Geometry flags in effect (the per-N default unless set)."""
+        return int(_lib.lib().hcnn_ctx_query(self.handle, 7))
 
     def profile(self, enable: bool):
         _lib.check(_lib.lib().hcnn_profile(self.handle, int(bool(enable))))
@@ -490,7 +496,12 @@ def eval_network(tensor, model, rlk, params, counter=None, workers: int = 1, cap
     layer_hook receives GpuCipherTensors (their .cts download on demand)."""
     counter = counter if counter is not None else OpCounter()
     x, was_host = _as_gpu(tensor, params)
-    for layer, weights in zip(model.spec.layers, model.weights):
+    x = _eval_layers(x, model, 0, rlk, params, counter, workers, capacity, layer_hook)
+    return _ret(x, was_host)
+
+
+def _eval_layers(x, model, start, rlk, params, counter, workers=1, capacity=None, layer_hook=None):
+    for layer, weights in list(zip(model.spec.layers, model.weights))[start:]:
         k = kind_of(layer)
         if k == "conv":
             x = eval_conv(x, layer, weights, params, counter, workers, capacity)
@@ -502,11 +513,85 @@ def eval_network(tensor, model, rlk, params, counter=None, workers: int = 1, cap
             x = eval_fc(x, layer, weights, params, counter, workers)
         if layer_hook is not None:
             layer_hook(layer.name, x)
-    return _ret(x, was_host)
+    return x
+
+
+_COPY_STREAMS: dict = {}
+
+
+def _copy_streams(dev):
+    """One upload and one download stream per device, reused across calls (a
+    fresh stream per call would also strand the caching allocator's blocks on
+    streams that are never used again)."""
+    key = dev.index
+    if key not in _COPY_STREAMS:
+        _COPY_STREAMS[key] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+    return _COPY_STREAMS[key]
+
+
+def _bandable(model, shape) -> bool:
+    """First layers are an unpadded convolution followed by a square: the
+    convolution's output rows depend on a contiguous band of input rows."""
+    layers = model.spec.layers
+    return (len(layers) >= 2 and kind_of(layers[0]) == "conv" and not layers[0].padded
+            and kind_of(layers[1]) == "square" and shape[0] >= 2)
+
+
+def _banded_head(hb, buf, shape, delta, model, rlk, params, counter, up_stream, compute, bands, layer_hook):
+    """conv1 + square1 of one batch by output-row bands, each band starting as
+    soon as the input rows it reads are uploaded (the upload of the next band
+    overlaps the square of this one).  Same kernels, same results and counters
+    as eval_conv + eval_square on the whole tensor (engine.py:237-364).
+    Returns (square output tensor, event after the last read of `buf`)."""
+    conv, weights = model.spec.layers[0], np.asarray(model.weights[0])
+    h, w, c = shape
+    f, kh, kw, cg = weights.shape
+    if c != cg * conv.groups:
+        raise ParameterMismatchError(f"{conv.name}: channel mismatch")
+    sh, sw = conv.stride
+    oh, ow = (h - kh) // sh + 1, (w - kw) // sw + 1
+    g = context_for(params, buf.device)
+    if rlk is None:
+        raise MissingKeyError("relinearization key required for hsquare")
+    g.set_relin_key(rlk)
+    wt = g.weights(weights)
+    cout, sq = g.empty(oh * ow * f), g.empty(oh * ow * f)
+    L = _lib.lib()
+    row = w * c  # ciphertexts per input row
+    cuts = [round(b * oh / bands) for b in range(bands + 1)]
+    uploaded = 0
+    for y0, y1 in zip(cuts, cuts[1:]):
+        if y1 == y0:
+            continue
+        hi = (y1 - 1) * sh + kh
+        if hi > uploaded:
+            with torch.cuda.stream(up_stream):
+                buf[uploaded * row:hi * row].copy_(hb[uploaded * row:hi * row], non_blocking=True)
+                ready = torch.cuda.Event()
+                ready.record(up_stream)
+            compute.wait_event(ready)
+            uploaded = hi
+        g.bind_stream()
+        lo = y0 * sh
+        _lib.check(L.hcnn_conv(g.handle, _ptr(buf[lo * row:]), _ptr(cout[y0 * ow * f:]), hi - lo, w, c, wt, f,
+                               kh, kw, sh, sw, 0, conv.groups), conv.name)
+        n = (y1 - y0) * ow * f
+        _lib.check(L.hcnn_square(g.handle, _ptr(cout[y0 * ow * f:]), _ptr(sq[y0 * ow * f:]), n), "square")
+    released = torch.cuda.Event()
+    released.record(compute)
+    _count(counter, *_conv_counts(h, w, conv, weights))
+    counter.hsquare += oh * ow * f
+    d1 = delta * conv.weight_scale
+    x1 = GpuCipherTensor((oh, ow, f), cout, d1, params.t, params)
+    x2 = GpuCipherTensor((oh, ow, f), sq, d1 * d1, params.t, params)
+    if layer_hook is not None:
+        layer_hook(conv.name, x1)
+        layer_hook(model.spec.layers[1].name, x2)
+    return x2, released
 
 
 def eval_network_stream(batches, model, rlk, params, shape, delta, counter=None, device=None,
-                        layer_hook=None, outputs=None):
+                        layer_hook=None, outputs=None, bands: int = 6):
     """Serving loop over encrypted slot-batches held in (pinned) host memory.
 
     Each batch is one `eval_network` (engine.py:400-423) on the GPU.  Batch
@@ -517,6 +602,10 @@ def eval_network_stream(batches, model, rlk, params, shape, delta, counter=None,
 
     batches: iterable of host int32 tensors [n_ct][2][K][N] (u32 residues,
     (y, x, c) row-major like CipherTensor.cts), all of `shape`.
+    The first batch has no evaluation to hide its upload behind: when the
+    network starts with an unpadded convolution and a square, its upload is
+    split into `bands` output-row bands and each band's conv1 + square1 starts
+    as soon as its input rows are on the device (bands=1 turns this off).
     Returns the list of host int32 logit tensors [n_out][2][K][N] (written
     into `outputs[i]` when given, else freshly pinned); they are complete when
     the call returns.
@@ -524,38 +613,48 @@ def eval_network_stream(batches, model, rlk, params, shape, delta, counter=None,
     counter = counter if counter is not None else OpCounter()
     dev = torch.device("cuda", _device_index(device))
     compute = torch.cuda.current_stream(dev)
-    up_stream = torch.cuda.Stream(dev)
-    down_stream = torch.cuda.Stream(dev)
+    up_stream, down_stream = _copy_streams(dev)
     up_stream.wait_stream(compute)
+    down_stream.wait_stream(compute)
     bufs, free, outs = [None, None], [None, None], []
     for i, hb in enumerate(batches):
         slot = i % 2
         if tuple(hb.shape[1:]) != (2, len(params.ctx.primes), int(params.ctx.ring_degree)):
             raise ParameterMismatchError("batch layout does not match params")
-        with torch.cuda.stream(up_stream):
-            if free[slot] is not None:
-                up_stream.wait_event(free[slot])
-            if bufs[slot] is None or bufs[slot].shape != hb.shape:
-                bufs[slot] = torch.empty(hb.shape, dtype=torch.int32, device=dev)
-            bufs[slot].copy_(hb, non_blocking=True)
-            ready = torch.cuda.Event()
-            ready.record(up_stream)
-        compute.wait_event(ready)
-        x = GpuCipherTensor(shape, bufs[slot], delta, params.t, params)
-        released = torch.cuda.Event()
-        state = {"first": True}
+        if bufs[slot] is None or bufs[slot].shape != hb.shape:
+            # allocated on the compute stream (which reads it), written by the
+            # copy stream: record_stream keeps the block until both are done
+            bufs[slot] = torch.empty(hb.shape, dtype=torch.int32, device=dev)
+            bufs[slot].record_stream(up_stream)
+        if i == 0 and bands > 1 and _bandable(model, shape):
+            # nothing to overlap the first upload with: stream it by row bands
+            # into conv1 + square1 instead
+            x, free[slot] = _banded_head(hb, bufs[slot], shape, delta, model, rlk, params, counter, up_stream,
+                                         compute, bands, layer_hook)
+            out = _eval_layers(x, model, 2, rlk, params, counter, layer_hook=layer_hook)
+        else:
+            with torch.cuda.stream(up_stream):
+                if free[slot] is not None:
+                    up_stream.wait_event(free[slot])
+                bufs[slot].copy_(hb, non_blocking=True)
+                ready = torch.cuda.Event()
+                ready.record(up_stream)
+            compute.wait_event(ready)
+            x = GpuCipherTensor(shape, bufs[slot], delta, params.t, params)
+            released = torch.cuda.Event()
+            state = {"first": True}
 
-        def hook(name, t, _released=released, _state=state):
-            if _state["first"]:  # the first layer has consumed the input buffer
-                _released.record(compute)
-                _state["first"] = False
-            if layer_hook is not None:
-                layer_hook(name, t)
+            def hook(name, t, _released=released, _state=state):
+                if _state["first"]:  # the first layer has consumed the input buffer
+                    _released.record(compute)
+                    _state["first"] = False
+                if layer_hook is not None:
+                    layer_hook(name, t)
 
-        out = eval_network(x, model, rlk, params, counter, layer_hook=hook)
-        if state["first"]:
-            released.record(compute)
-        free[slot] = released
+            out = eval_network(x, model, rlk, params, counter, layer_hook=hook)
+            if state["first"]:
+                released.record(compute)
+            free[slot] = released
         done = torch.cuda.Event()
         done.record(compute)
         host = outputs[i] if outputs is not None else torch.empty(out.data.shape, dtype=torch.int32,
