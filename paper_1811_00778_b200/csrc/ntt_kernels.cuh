@@ -112,17 +112,60 @@ DI void ntt_inv_pair(uint32_t* x, uint32_t* s, const uint2* itw, uint32_t p, con
   }
 }
 
+// TMEM as per-thread stash (no tensor-core use): warp w owns lanes
+// 32 (w % 4) + [0, 32) and columns W (w / 4) + [0, W) of the CTA's allocation
+// (W = 2E for the relinearisation sums, E for the tensor's parked row).
+template <class G, int W>
+__host__ __device__ constexpr uint32_t tmem_stash_cols() {
+  return W * (G::T / 128) <= 128 ? 128 : W * (G::T / 128) <= 256 ? 256 : 512;
+}
+
+DI void tmem_alloc_cols(uint32_t* slot, uint32_t cols) {
+  if (cols == 128)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(slot)) : "memory");
+  else if (cols == 256)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(slot)) : "memory");
+  else
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(slot)) : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+DI void tmem_dealloc_cols(uint32_t base, uint32_t cols) {
+  if (cols == 128) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(base) : "memory");
+  else if (cols == 256) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(base) : "memory");
+  else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(base) : "memory");
+}
+
+DI uint32_t tmem_stash_alloc(uint32_t* slot, uint32_t cols, int tid, int width) {
+  const int warp = tid >> 5;
+  if (warp == 0) tmem_alloc_cols(slot, cols);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  return *slot + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(warp >> 2) * width;
+}
+
+DI void tmem_stash_free(uint32_t base, uint32_t cols, int tid) {
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  if ((tid >> 5) == 0) tmem_dealloc_cols(base, cols);
+}
+
 // One CTA per (ct, prime of Q u P).  a/b: [B][2][K][N]; ae/be: [B][2][KP][N]
 // (exact extensions); d: [B][3][K+KP][N] exact tensor parts, coefficient domain.
 // The four (two for a square) forward transforms run as row pairs and the
 // inverse of d0, d1 as a pair, sharing twiddle loads and barriers.
-template <class G>
+// TM (E = 16, squares only): one row in registers at a time, A0 and then
+// d1, d2 parked in TMEM (flag TENSOR_TMEM).
+template <class G, bool TM = false>
 __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
     k_tensor(const uint32_t* __restrict__ a, const uint32_t* __restrict__ a_ext,
              const uint32_t* __restrict__ b, const uint32_t* __restrict__ b_ext,
              uint32_t* __restrict__ d, int K, int KP, int square, NttTabs nt) {
   extern __shared__ uint32_t s[];
   constexpr int E = G::E;
+  static_assert(!TM || E == 16, "TMEM stash: E = 16");
   const int tid = threadIdx.x;
   const int j = blockIdx.x;
   const size_t ct = blockIdx.y;
@@ -142,6 +185,43 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
   const uint32_t pinv = nt.pinv[j];
   const uint32_t p2 = 2 * p;
   const InvScale ninv = inv_scale(nt, j, true);
+  if constexpr (TM) {
+    // square only (the dispatch sends general products to TM = false): the
+    // transforms run one row at a time and the waiting rows sit in TMEM
+    __shared__ uint32_t tmem_slot;
+    constexpr uint32_t COLS = tmem_stash_cols<G, 2 * E>();
+    const uint32_t tp = tmem_stash_alloc(&tmem_slot, COLS, tid, 2 * E);
+    uint32_t x[E];
+    // rolled loops: one copy of each transform's code (five inlined
+    // transforms would hoist enough addressing to spill at 64 registers)
+#pragma unroll 1
+    for (int r = 0; r < 2; ++r) {
+      load_natural<G>(x, row_of(a, a_ext, r), tid);
+      ntt_fwd<G, 1, false>(x, s, tw, p, tid);
+      if (r == 0) tmem_st16(tp, x);  // A0
+    }
+    {  // x = A1
+      uint32_t a0[E], t[E];
+      tmem_ld16(tp, a0);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const uint32_t c = mont_mul(a0[e], x[e], p, pinv);
+        t[e] = umin32(2 * c, 2 * c - p2);
+      }
+      tmem_st16(tp, t);  // d1
+#pragma unroll
+      for (int e = 0; e < E; ++e) t[e] = mont_mul(x[e], x[e], p, pinv);
+      tmem_st16(tp + E, t);  // d2
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = mont_mul(a0[e], a0[e], p, pinv);  // d0
+    }
+#pragma unroll 1
+    for (int r = 0; r < 3; ++r) {
+      if (r > 0) tmem_ld16(tp + (r - 1) * E, x);
+      inv_store<G>(x, s, itw, p, ninv, tid, r == 0 ? o0 : r == 1 ? o1 : o2);
+    }
+    tmem_stash_free(tmem_slot, COLS, tid);
+  } else {
   uint32_t x[2 * E], y[2 * E];
   if (square) {
     // x = (A0 | A1)
@@ -180,6 +260,7 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
     o1[natural_index<G>(tid, e)] = x[E + e];
   }
   inv_store<G>(y, s, itw, p, ninv, tid, o2);
+  }  // !TM
 }
 
 // Plaintext-polynomial product (bfv.py:301-318, NTT path): one CTA per (ct,
@@ -302,27 +383,6 @@ struct RelinSmem {
 // TM: the running sums live in TMEM instead of registers (E = 16: one
 // 32x32b.x16 load / store per part and digit group; warp w uses lanes
 // 32 (w % 4) + lane and columns 2E (w / 4) + [0, 2E)).
-template <class G>
-__host__ __device__ constexpr uint32_t relin_tmem_cols() {
-  return 2 * G::E * (G::T / 128) <= 128 ? 128 : 2 * G::E * (G::T / 128) <= 256 ? 256 : 512;
-}
-
-DI void tmem_alloc_cols(uint32_t* slot, uint32_t cols) {
-  if (cols == 128)
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(slot)) : "memory");
-  else if (cols == 256)
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(slot)) : "memory");
-  else
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(slot)) : "memory");
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-}
-
-DI void tmem_dealloc_cols(uint32_t base, uint32_t cols) {
-  if (cols == 128) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(base) : "memory");
-  else if (cols == 256) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(base) : "memory");
-  else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(base) : "memory");
-}
-
 template <class G, bool ACC64, int NR, bool TM = false>
 __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
     k_relin(const uint32_t* __restrict__ dig, const uint32_t* __restrict__ y3,
@@ -345,12 +405,7 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
   Acc acc0[TM ? 1 : E], acc1[TM ? 1 : E];
   uint32_t tacc = 0;
   if constexpr (TM) {
-    const int warp = tid >> 5;
-    if (warp == 0) tmem_alloc_cols(&tmem_slot, relin_tmem_cols<G>());
-    tmem_fence_before();
-    __syncthreads();
-    tmem_fence_after();
-    tacc = tmem_slot + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(warp >> 2) * 2 * E;
+    tacc = tmem_stash_alloc(&tmem_slot, tmem_stash_cols<G, 2 * G::E>(), tid, 2 * E);
     uint32_t z[16];
 #pragma unroll
     for (int e = 0; e < 16; ++e) z[e] = 0;
@@ -506,10 +561,7 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
   if constexpr (TM) {
     tmem_ld16(tacc, x);
     tmem_ld16(tacc + E, x + E);
-    tmem_fence_before();
-    __syncthreads();
-    tmem_fence_after();
-    if ((tid >> 5) == 0) tmem_dealloc_cols(tmem_slot, relin_tmem_cols<G>());
+    tmem_stash_free(tmem_slot, tmem_stash_cols<G, 2 * G::E>(), tid);
   } else {
 #pragma unroll
     for (int e = 0; e < E; ++e) {
@@ -639,6 +691,9 @@ void configure_smem() {
   cudaFuncSetAttribute(k_ntt_rows<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_tensor<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        G::ntt_smem_words(pair_nr<G>()) * sizeof(uint32_t));
+  if constexpr (G::E == 16)
+    cudaFuncSetAttribute(k_tensor<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         G::ntt_smem_words(pair_nr<G>()) * sizeof(uint32_t));
   cudaFuncSetAttribute(k_relin<G, relin_acc64<G>(false), relin_nr<G>(false)>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, RelinSmem<G, relin_nr<G>(false)>::BYTES);
   cudaFuncSetAttribute(k_relin<G, relin_acc64<G>(true), 1>,
@@ -653,6 +708,8 @@ void configure_smem() {
 constexpr int RELIN_SINGLE = 16;
 // relinearisation running sums in TMEM instead of registers
 constexpr int RELIN_TMEM = 1024;
+// square tensor with one row in registers and the others parked in TMEM
+constexpr int TENSOR_TMEM = 2048;
 
 template <class G, bool SINGLE>
 cudaError_t launch_relin(const NttLaunch& a) {
@@ -686,6 +743,13 @@ cudaError_t launch_with(int op, const NttLaunch& a) {
       k_ntt_rows<G><<<a.grid, G::T, smem, a.stream>>>(a.rows, a.limbs, a.prime_off, a.inverse, a.nt);
       break;
     case 1:
+      if constexpr (G::E == 16) {
+        if ((a.variant & TENSOR_TMEM) && a.square) {
+          k_tensor<G, true><<<a.grid, G::T, G::ntt_smem_words(pair_nr<G>()) * sizeof(uint32_t), a.stream>>>(
+              a.a, a.ae, a.b, a.be, a.d, a.K, a.KP, a.square, a.nt);
+          break;
+        }
+      }
       k_tensor<G><<<a.grid, G::T, G::ntt_smem_words(pair_nr<G>()) * sizeof(uint32_t), a.stream>>>(
           a.a, a.ae, a.b, a.be, a.d, a.K, a.KP, a.square, a.nt);
       break;
