@@ -67,9 +67,10 @@ enum {
 /* Tuning options.  HCNN_OPT_NTT_VARIANT: geometry flags of the fused NTT
  * kernels: 16 one-row relinearisation, 32 radix-32 square tensor, 64
  * mixed-width passes, 512 two-CTA cluster rows (N = 2^15), 1024
- * relinearisation sums in TMEM, 2048 square tensor with rows parked in TMEM.
- * Default per N: 64|1024|2048 at 2^14, 512 at 2^15, 0 otherwise.  Results
- * are identical for every setting. */
+ * relinearisation sums in TMEM, 2048 square tensor with one-row transforms
+ * and rows parked in TMEM, 4096 square tensor with pair transforms and d2
+ * parked in TMEM.  Default per N: 64|1024|4096 at 2^14, 512 at 2^15, 0
+ * otherwise.  Results are identical for every setting. */
 enum { HCNN_OPT_NTT_VARIANT = 1 };
 int hcnn_ctx_set_option(hcnn_ctx* ctx, int key, int64_t value);
 int64_t hcnn_ctx_query(hcnn_ctx* ctx, int what);

@@ -158,14 +158,14 @@ DI void tmem_stash_free(uint32_t base, uint32_t cols, int tid) {
 // inverse of d0, d1 as a pair, sharing twiddle loads and barriers.
 // TM (E = 16, squares only): one row in registers at a time, A0 and then
 // d1, d2 parked in TMEM (flag TENSOR_TMEM).
-template <class G, bool TM = false>
+template <class G, int TM = 0>
 __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
     k_tensor(const uint32_t* __restrict__ a, const uint32_t* __restrict__ a_ext,
              const uint32_t* __restrict__ b, const uint32_t* __restrict__ b_ext,
              uint32_t* __restrict__ d, int K, int KP, int square, NttTabs nt) {
   extern __shared__ uint32_t s[];
   constexpr int E = G::E;
-  static_assert(!TM || E == 16, "TMEM stash: E = 16");
+  static_assert(TM == 0 || E == 16, "TMEM stash: E = 16");
   const int tid = threadIdx.x;
   const int j = blockIdx.x;
   const size_t ct = blockIdx.y;
@@ -185,8 +185,40 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
   const uint32_t pinv = nt.pinv[j];
   const uint32_t p2 = 2 * p;
   const InvScale ninv = inv_scale(nt, j, true);
-  if constexpr (TM) {
-    // square only (the dispatch sends general products to TM = false): the
+  if constexpr (TM == 2) {
+    // square only: A0, A1 transformed as a pair, d2 parked in TMEM while d0,
+    // d1 go through their inverse pair
+    __shared__ uint32_t tmem_slot2;
+    constexpr uint32_t COLS = tmem_stash_cols<G, E>();
+    const uint32_t tp = tmem_stash_alloc(&tmem_slot2, COLS, tid, E);
+    uint32_t x[2 * E];
+    load_natural<G>(x, row_of(a, a_ext, 0), tid);
+    load_natural<G>(x + E, row_of(a, a_ext, 1), tid);
+    ntt_fwd_pair<G, false>(x, s, tw, p, tid);
+    {
+      uint32_t t[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) t[e] = mont_mul(x[E + e], x[E + e], p, pinv);
+      tmem_st16(tp, t);  // d2
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t a0 = x[e], a1 = x[E + e];
+      const uint32_t c = mont_mul(a0, a1, p, pinv);
+      x[e] = mont_mul(a0, a0, p, pinv);
+      x[E + e] = umin32(2 * c, 2 * c - p2);
+    }
+    ntt_inv_pair<G>(x, s, itw, p, ninv, tid);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      o0[natural_index<G>(tid, e)] = x[e];
+      o1[natural_index<G>(tid, e)] = x[E + e];
+    }
+    tmem_ld16(tp, x);
+    tmem_stash_free(tmem_slot2, COLS, tid);
+    inv_store<G>(x, s, itw, p, ninv, tid, o2);
+  } else if constexpr (TM == 1) {
+    // square only (the dispatch sends general products to TM = 0): the
     // transforms run one row at a time and the waiting rows sit in TMEM
     __shared__ uint32_t tmem_slot;
     constexpr uint32_t COLS = tmem_stash_cols<G, 2 * E>();
@@ -691,9 +723,12 @@ void configure_smem() {
   cudaFuncSetAttribute(k_ntt_rows<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_tensor<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        G::ntt_smem_words(pair_nr<G>()) * sizeof(uint32_t));
-  if constexpr (G::E == 16)
-    cudaFuncSetAttribute(k_tensor<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if constexpr (G::E == 16) {
+    cudaFuncSetAttribute(k_tensor<G, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          G::ntt_smem_words(pair_nr<G>()) * sizeof(uint32_t));
+    cudaFuncSetAttribute(k_tensor<G, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         G::ntt_smem_words(pair_nr<G>()) * sizeof(uint32_t));
+  }
   cudaFuncSetAttribute(k_relin<G, relin_acc64<G>(false), relin_nr<G>(false)>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, RelinSmem<G, relin_nr<G>(false)>::BYTES);
   cudaFuncSetAttribute(k_relin<G, relin_acc64<G>(true), 1>,
@@ -710,6 +745,8 @@ constexpr int RELIN_SINGLE = 16;
 constexpr int RELIN_TMEM = 1024;
 // square tensor with one row in registers and the others parked in TMEM
 constexpr int TENSOR_TMEM = 2048;
+// square tensor with the pair transforms kept and only d2 parked in TMEM
+constexpr int TENSOR_TMEM_PAIR = 4096;
 
 template <class G, bool SINGLE>
 cudaError_t launch_relin(const NttLaunch& a) {
@@ -744,8 +781,13 @@ cudaError_t launch_with(int op, const NttLaunch& a) {
       break;
     case 1:
       if constexpr (G::E == 16) {
+        if ((a.variant & TENSOR_TMEM_PAIR) && a.square) {
+          k_tensor<G, 2><<<a.grid, G::T, G::ntt_smem_words(pair_nr<G>()) * sizeof(uint32_t), a.stream>>>(
+              a.a, a.ae, a.b, a.be, a.d, a.K, a.KP, a.square, a.nt);
+          break;
+        }
         if ((a.variant & TENSOR_TMEM) && a.square) {
-          k_tensor<G, true><<<a.grid, G::T, G::ntt_smem_words(pair_nr<G>()) * sizeof(uint32_t), a.stream>>>(
+          k_tensor<G, 1><<<a.grid, G::T, G::ntt_smem_words(pair_nr<G>()) * sizeof(uint32_t), a.stream>>>(
               a.a, a.ae, a.b, a.be, a.d, a.K, a.KP, a.square, a.nt);
           break;
         }
