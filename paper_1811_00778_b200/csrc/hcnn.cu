@@ -907,7 +907,7 @@ int hcnn_ctx_create(hcnn_ctx** out, uint32_t n, uint32_t k, const uint64_t* prim
     // default geometry per ring degree (profiles/r1_micro_sweep.jsonl): the
     // shuffle-tail radix-16 kernels up to 2^13, mixed-width passes at 2^14,
     // 2-CTA cluster relinearisation at 2^15
-    c->variant = c->logN == 14 ? (64 | 1024 | 4096) : c->logN == 15 ? 512 : 0;
+    c->variant = c->logN == 14 ? (64 | 1024 | 4096) : c->logN == 15 ? (512 | 2048) : 0;
     build_tables(c.get(), q, t);
     *out = c.release();
   });

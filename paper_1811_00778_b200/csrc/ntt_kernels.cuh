@@ -136,6 +136,18 @@ DI void tmem_dealloc_cols(uint32_t base, uint32_t cols) {
   else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(base) : "memory");
 }
 
+template <int E>
+DI void tmem_st_row(uint32_t taddr, const uint32_t* v) {
+#pragma unroll
+  for (int c = 0; c < E / 16; ++c) tmem_st16(taddr + 16 * c, v + 16 * c);
+}
+
+template <int E>
+DI void tmem_ld_row(uint32_t taddr, uint32_t* v) {
+#pragma unroll
+  for (int c = 0; c < E / 16; ++c) tmem_ld16(taddr + 16 * c, v + 16 * c);
+}
+
 DI uint32_t tmem_stash_alloc(uint32_t* slot, uint32_t cols, int tid, int width) {
   const int warp = tid >> 5;
   if (warp == 0) tmem_alloc_cols(slot, cols);
@@ -165,7 +177,7 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
              uint32_t* __restrict__ d, int K, int KP, int square, NttTabs nt) {
   extern __shared__ uint32_t s[];
   constexpr int E = G::E;
-  static_assert(TM == 0 || E == 16, "TMEM stash: E = 16");
+  static_assert(TM == 0 || E % 16 == 0, "TMEM stash: rows of 16-column chunks");
   const int tid = threadIdx.x;
   const int j = blockIdx.x;
   const size_t ct = blockIdx.y;
@@ -199,7 +211,7 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
       uint32_t t[E];
 #pragma unroll
       for (int e = 0; e < E; ++e) t[e] = mont_mul(x[E + e], x[E + e], p, pinv);
-      tmem_st16(tp, t);  // d2
+      tmem_st_row<E>(tp, t);  // d2
     }
 #pragma unroll
     for (int e = 0; e < E; ++e) {
@@ -214,7 +226,7 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
       o0[natural_index<G>(tid, e)] = x[e];
       o1[natural_index<G>(tid, e)] = x[E + e];
     }
-    tmem_ld16(tp, x);
+    tmem_ld_row<E>(tp, x);
     tmem_stash_free(tmem_slot2, COLS, tid);
     inv_store<G>(x, s, itw, p, ninv, tid, o2);
   } else if constexpr (TM == 1) {
@@ -230,26 +242,26 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
     for (int r = 0; r < 2; ++r) {
       load_natural<G>(x, row_of(a, a_ext, r), tid);
       ntt_fwd<G, 1, false>(x, s, tw, p, tid);
-      if (r == 0) tmem_st16(tp, x);  // A0
+      if (r == 0) tmem_st_row<E>(tp, x);  // A0
     }
     {  // x = A1
       uint32_t a0[E], t[E];
-      tmem_ld16(tp, a0);
+      tmem_ld_row<E>(tp, a0);
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const uint32_t c = mont_mul(a0[e], x[e], p, pinv);
         t[e] = umin32(2 * c, 2 * c - p2);
       }
-      tmem_st16(tp, t);  // d1
+      tmem_st_row<E>(tp, t);  // d1
 #pragma unroll
       for (int e = 0; e < E; ++e) t[e] = mont_mul(x[e], x[e], p, pinv);
-      tmem_st16(tp + E, t);  // d2
+      tmem_st_row<E>(tp + E, t);  // d2
 #pragma unroll
       for (int e = 0; e < E; ++e) x[e] = mont_mul(a0[e], a0[e], p, pinv);  // d0
     }
 #pragma unroll 1
     for (int r = 0; r < 3; ++r) {
-      if (r > 0) tmem_ld16(tp + (r - 1) * E, x);
+      if (r > 0) tmem_ld_row<E>(tp + (r - 1) * E, x);
       inv_store<G>(x, s, itw, p, ninv, tid, r == 0 ? o0 : r == 1 ? o1 : o2);
     }
     tmem_stash_free(tmem_slot, COLS, tid);
@@ -723,7 +735,7 @@ void configure_smem() {
   cudaFuncSetAttribute(k_ntt_rows<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_tensor<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        G::ntt_smem_words(pair_nr<G>()) * sizeof(uint32_t));
-  if constexpr (G::E == 16) {
+  if constexpr (G::E % 16 == 0 && G::E * (G::T / 128) <= 256) {
     cudaFuncSetAttribute(k_tensor<G, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          G::ntt_smem_words(pair_nr<G>()) * sizeof(uint32_t));
     cudaFuncSetAttribute(k_tensor<G, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -780,7 +792,7 @@ cudaError_t launch_with(int op, const NttLaunch& a) {
       k_ntt_rows<G><<<a.grid, G::T, smem, a.stream>>>(a.rows, a.limbs, a.prime_off, a.inverse, a.nt);
       break;
     case 1:
-      if constexpr (G::E == 16) {
+      if constexpr (G::E % 16 == 0 && G::E * (G::T / 128) <= 256) {
         if ((a.variant & TENSOR_TMEM_PAIR) && a.square) {
           k_tensor<G, 2><<<a.grid, G::T, G::ntt_smem_words(pair_nr<G>()) * sizeof(uint32_t), a.stream>>>(
               a.a, a.ae, a.b, a.be, a.d, a.K, a.KP, a.square, a.nt);
