@@ -66,7 +66,7 @@ enum {
 };
 /* Tuning options.  HCNN_OPT_NTT_VARIANT: geometry flags of the fused NTT
  * kernels: 16 one-row relinearisation, 32 radix-32 square tensor, 64
- * mixed-width passes, 512 two-CTA cluster rows (N = 2^15), 1024
+ * mixed-width passes, 512 two-CTA cluster rows (N = 2^14, 2^15), 1024
  * relinearisation sums in TMEM, 2048 square tensor with one-row transforms
  * and rows parked in TMEM, 4096 square tensor with pair transforms and d2
  * parked in TMEM.  Default per N: 64|1024|4096 at 2^14, 512|2048 at 2^15,

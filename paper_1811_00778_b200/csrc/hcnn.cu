@@ -989,7 +989,8 @@ int hcnn_ctx_set_option(hcnn_ctx* c, int key, int64_t value) {
       if (value & ~(int64_t)(16 | 32 | 64 | 512 | 1024 | 2048 | 4096))
         fail(HCNN_ERR_PARAM, "NTT variant flags are 16, 32, 64, 512, 1024, 2048 and 4096");
       if ((value & (32 | 64)) && c->logN < 10) fail(HCNN_ERR_UNSUPPORTED, "mixed geometries need N >= 1024");
-      if ((value & 512) && c->logN != 15) fail(HCNN_ERR_UNSUPPORTED, "cluster kernels are for N = 2^15");
+      if ((value & 512) && c->logN != 15 && c->logN != 14)
+        fail(HCNN_ERR_UNSUPPORTED, "cluster kernels are for N = 2^14 and 2^15");
       c->variant = (int)value;
     } else {
       fail(HCNN_ERR_PARAM, "unknown option");

@@ -48,7 +48,9 @@ DI int squeeze(int idx) {
 
 template <class G>
 struct ClusterGeom {
-  static_assert(G::MIXED && G::LOGE == 5 && G::LOGN == 15, "cluster NTT: 2^15 on the radix-32 mixed geometry");
+  static_assert(G::MIXED && G::LOGE == 5 && (G::LOGN == 15 || G::LOGN == 14),
+                "cluster NTT: 2^14 / 2^15 on the radix-32 mixed geometry");
+  static_assert(G::NFULL == 3, "cluster NTT: three register passes, two exchanges");
   static constexpr int TC = G::T / 2;                  // threads per CTA
   static constexpr int HALF = G::N / 2;                // residues per CTA
   static constexpr int XW = (HALF + 2 * (HALF >> 5) + 2 + 3) & ~3;  // padded compact row
@@ -124,7 +126,7 @@ DI void ntt_inv_cl(uint32_t* x, uint32_t* s, const uint2* __restrict__ itw, uint
 // like k_ntt_rows (inverse: 0 forward to spectral positions, 1 inverse, 2
 // forward to the tiled layout).
 template <class G>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G::T / 2, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G::T / 2, (G::T / 2 <= 256 ? 2 : 1))
     k_ntt_rows_cl(uint32_t* __restrict__ data, int limbs, int prime_off, int inverse, NttTabs nt) {
   extern __shared__ __align__(16) uint32_t s[];
   const uint32_t rank = cluster_rank();
@@ -199,14 +201,14 @@ DI void tmem_st16(uint32_t addr, const uint32_t* v) {
 // through the cluster inverse and are added to (y0, y1).  Digits are read
 // straight from global memory.  grid: (2 K, B).
 template <class G>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G::T / 2, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G::T / 2, (G::T / 2 <= 256 ? 2 : 1))
     k_relin_cl(const uint32_t* __restrict__ dig, const uint32_t* __restrict__ y3,
                const uint32_t* __restrict__ rlk, uint32_t* __restrict__ out, int K, int D,
                int reduce_digits, NttTabs nt) {
   extern __shared__ __align__(16) uint32_t s[];
   __shared__ uint32_t tmem_slot;
   constexpr int E = G::E;
-  static_assert(E == 32 && G::T / 2 == 512, "TMEM plan: 16 warps x 32 lanes x 64 columns");
+  static_assert(E == 32 && (G::T / 2 == 512 || G::T / 2 == 256), "TMEM plan: 8 or 16 warps x 32 lanes x 64 columns");
   const uint32_t rank = cluster_rank();
   const int vtid = (int)rank * ClusterGeom<G>::TC + threadIdx.x;
   const int j = blockIdx.x / 2;

@@ -857,11 +857,11 @@ constexpr int CLUSTER_ROWS = 512;
 
 template <int LOGN>
 cudaError_t ntt_launch(int op, const NttLaunch& a) {
-  if constexpr (LOGN == 15) {
+  if constexpr (LOGN == 15 || LOGN == 14) {
     if (a.variant & CLUSTER_ROWS) {
       // rows and relinearisation on 2-CTA clusters; the key-layout kernels on
-      // the same (radix-32 mixed) geometry; the tensor keeps the default one
-      using GC = NttGeom<15, 5, false, true>;
+      // the same (radix-32 mixed) geometry; the tensor keeps the one-CTA one
+      using GC = NttGeom<LOGN, 5, false, true>;
       constexpr int smem = ClusterGeom<GC>::smem_words(1) * sizeof(uint32_t);
       static std::atomic<uint64_t> cfg{0};
       per_device_once(cfg, [] {
@@ -879,10 +879,9 @@ cudaError_t ntt_launch(int op, const NttLaunch& a) {
             a.dig, a.y3, a.rlk, a.out, a.K, a.D, a.reduce_digits, a.nt);
         return cudaGetLastError();
       }
-      // rows in the spectral / natural layouts and the tensor: the one-CTA
-      // kernels (faster there); everything that reads tiled keys: GC
-      if (op == 0 || op == 1) return launch_with<NttGeom<LOGN>>(op, a);
-      return launch_with<GC>(op, a);
+      // everything that reads tiled keys: GC; rows in the spectral / natural
+      // layouts and the tensor: the one-CTA dispatch below (faster there)
+      if (op != 0 && op != 1) return launch_with<GC>(op, a);
     }
   }
   if constexpr (LOGN >= 10) {
@@ -899,7 +898,7 @@ int mont_of(int v) { return relin_acc64<G>((v & RELIN_SINGLE) != 0) ? 0 : 1; }
 // does variant v use Montgomery-form rlk?
 template <int LOGN>
 int ntt_variant_mont(int v) {
-  if constexpr (LOGN == 15) {
+  if constexpr (LOGN == 15 || LOGN == 14) {
     if (v & CLUSTER_ROWS) return 1;  // k_relin_cl: Montgomery-form keys
   }
   if constexpr (LOGN >= 10) {
