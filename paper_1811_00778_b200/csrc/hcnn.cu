@@ -802,11 +802,11 @@ void layout_key(hcnn_ctx* c, const uint32_t* raw, int domain, size_t rows, uint3
 }
 
 void prepare_keys(hcnn_ctx* c) {
-  if (c->keys_variant == (c->variant & ~(32 | 1024 | 2048 | 4096))) return;
+  if (c->keys_variant == (c->variant & ~(32 | 1024 | 2048 | 4096 | 8192))) return;
   if (c->d_rlk_raw)
     layout_key(c, c->d_rlk_raw, c->rlk_domain, (size_t)c->D * 2 * c->K, &c->d_rlk, variant_mont(c, c->variant));
   if (c->d_pk_raw) layout_key(c, c->d_pk_raw, c->pk_domain, 2 * (size_t)c->K, &c->d_pk, 0);
-  c->keys_variant = c->variant & ~(32 | 1024 | 2048 | 4096);
+  c->keys_variant = c->variant & ~(32 | 1024 | 2048 | 4096 | 8192);
 }
 
 }  // namespace
@@ -907,7 +907,7 @@ int hcnn_ctx_create(hcnn_ctx** out, uint32_t n, uint32_t k, const uint64_t* prim
     // default geometry per ring degree (profiles/r1_micro_sweep.jsonl): the
     // shuffle-tail radix-16 kernels up to 2^13, mixed-width passes at 2^14,
     // 2-CTA cluster relinearisation at 2^15
-    c->variant = c->logN == 14 ? (64 | 1024 | 4096) : c->logN == 15 ? (512 | 2048) : 0;
+    c->variant = c->logN == 13 ? 8192 : c->logN == 14 ? (64 | 1024 | 4096) : c->logN == 15 ? (512 | 2048) : 0;
     build_tables(c.get(), q, t);
     *out = c.release();
   });
@@ -986,8 +986,8 @@ int hcnn_ctx_set_option(hcnn_ctx* c, int key, int64_t value) {
       // geometry flags of the fused kernels (ntt_kernels.cuh): +16 one-row
       // relinearisation transforms, +32 square tensors on the radix-32 mixed
       // geometry, +64 mixed-width passes instead of a warp-shuffle tail
-      if (value & ~(int64_t)(16 | 32 | 64 | 512 | 1024 | 2048 | 4096))
-        fail(HCNN_ERR_PARAM, "NTT variant flags are 16, 32, 64, 512, 1024, 2048 and 4096");
+      if (value & ~(int64_t)(16 | 32 | 64 | 512 | 1024 | 2048 | 4096 | 8192))
+        fail(HCNN_ERR_PARAM, "NTT variant flags are 16, 32, 64, 512, 1024, 2048, 4096 and 8192");
       if ((value & (32 | 64)) && c->logN < 10) fail(HCNN_ERR_UNSUPPORTED, "mixed geometries need N >= 1024");
       if ((value & 512) && c->logN != 15 && c->logN != 14)
         fail(HCNN_ERR_UNSUPPORTED, "cluster kernels are for N = 2^14 and 2^15");

@@ -307,6 +307,83 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
   }  // !TM
 }
 
+// Persistent square tensor (flag TENSOR_PERSIST): one CTA per SM walks the
+// (ct, prime) items; the two input rows of the NEXT item stream into shared
+// memory by TMA bulk copies while the current item computes, so no CTA starts
+// with an exposed HBM load.  Same arithmetic as k_tensor's square path.
+template <class G>
+constexpr int tensor_pf_smem_words() { return G::ntt_smem_words(pair_nr<G>()) + 2 * G::N; }
+
+template <class G>
+__global__ void __launch_bounds__(G::T, 1)
+    k_tensor_sq_pf(const uint32_t* __restrict__ a, const uint32_t* __restrict__ a_ext,
+                   uint32_t* __restrict__ d, int K, int KP, int n_items, NttTabs nt) {
+  extern __shared__ __align__(16) uint32_t s[];
+  __shared__ __align__(8) uint64_t bar;
+  constexpr int E = G::E;
+  const int tid = threadIdx.x;
+  const int L = K + KP;
+  uint32_t* stage = s + G::ntt_smem_words(pair_nr<G>());
+  auto row_of = [&](int item, int part) -> const uint32_t* {
+    const size_t ct = item / L;
+    const int j = item % L;
+    return j < K ? a + ((ct * 2 + part) * K + j) * G::N : a_ext + ((ct * 2 + part) * KP + (j - K)) * G::N;
+  };
+  auto fetch = [&](int item) {
+    fence_proxy_async();
+    mbar_expect_tx(&bar, 2 * G::N * 4);
+    bulk_g2s(stage, row_of(item, 0), G::N * 4, &bar);
+    bulk_g2s(stage + G::N, row_of(item, 1), G::N * 4, &bar);
+  };
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  int item = blockIdx.x;
+  if (tid == 0 && item < n_items) fetch(item);
+  uint32_t phase = 0;
+#pragma unroll 1
+  for (; item < n_items; item += gridDim.x) {
+    const size_t ct = item / L;
+    const int j = item % L;
+    const uint32_t p = nt.prime[j];
+    const uint32_t pinv = nt.pinv[j];
+    const uint32_t p2 = 2 * p;
+    const uint2* tw = nt.tw + (size_t)j * G::N;
+    const uint2* itw = nt.itw + (size_t)j * G::N;
+    const InvScale ninv = inv_scale(nt, j, true);
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    uint32_t x[2 * E], y[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      x[e] = stage[natural_index<G>(tid, e)];
+      x[E + e] = stage[G::N + natural_index<G>(tid, e)];
+    }
+    __syncthreads();  // every thread has read the stage
+    if (tid == 0 && item + (int)gridDim.x < n_items) fetch(item + gridDim.x);
+    ntt_fwd_pair<G, false>(x, s, tw, p, tid);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t a0 = x[e], a1 = x[E + e];
+      const uint32_t c = mont_mul(a0, a1, p, pinv);
+      x[e] = mont_mul(a0, a0, p, pinv);
+      x[E + e] = umin32(2 * c, 2 * c - p2);
+      y[e] = mont_mul(a1, a1, p, pinv);
+    }
+    ntt_inv_pair<G>(x, s, itw, p, ninv, tid);
+    uint32_t* o0 = d + ((ct * 3 + 0) * L + j) * G::N;
+    uint32_t* o1 = d + ((ct * 3 + 1) * L + j) * G::N;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      o0[natural_index<G>(tid, e)] = x[e];
+      o1[natural_index<G>(tid, e)] = x[E + e];
+    }
+    inv_store<G>(y, s, itw, p, ninv, tid, d + ((ct * 3 + 2) * L + j) * G::N);
+  }
+}
+
 // Plaintext-polynomial product (bfv.py:301-318, NTT path): one CTA per (ct,
 // prime of q); a: [B][2][K][N]; pt: [K][N] NTT domain, tiled layout (plain
 // form; the Montgomery 2^-32 is undone by the N^-1 2^32 of the inverse).
@@ -759,6 +836,8 @@ constexpr int RELIN_TMEM = 1024;
 constexpr int TENSOR_TMEM = 2048;
 // square tensor with the pair transforms kept and only d2 parked in TMEM
 constexpr int TENSOR_TMEM_PAIR = 4096;
+// persistent square tensor with TMA prefetch of the next item's rows
+constexpr int TENSOR_PERSIST = 8192;
 
 template <class G, bool SINGLE>
 cudaError_t launch_relin(const NttLaunch& a) {
@@ -792,6 +871,25 @@ cudaError_t launch_with(int op, const NttLaunch& a) {
       k_ntt_rows<G><<<a.grid, G::T, smem, a.stream>>>(a.rows, a.limbs, a.prime_off, a.inverse, a.nt);
       break;
     case 1:
+      if constexpr (tensor_pf_smem_words<G>() * 4 <= 220 * 1024 && G::N >= 1024) {
+        if ((a.variant & TENSOR_PERSIST) && a.square) {
+          static std::atomic<uint64_t> cfg{0};
+          static int sms = 0;
+          per_device_once(cfg, [] {
+            cudaFuncSetAttribute(k_tensor_sq_pf<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tensor_pf_smem_words<G>() * 4);
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+          });
+          const int n = (int)(a.grid.x * a.grid.y);
+          const int blocks = n < sms ? n : sms;
+          if (n > 0)
+            k_tensor_sq_pf<G><<<blocks, G::T, tensor_pf_smem_words<G>() * 4, a.stream>>>(a.a, a.ae, a.d, a.K, a.KP,
+                                                                                         n, a.nt);
+          break;
+        }
+      }
       if constexpr (G::E % 16 == 0 && G::E * (G::T / 128) <= 256) {
         if ((a.variant & TENSOR_TMEM_PAIR) && a.square) {
           k_tensor<G, 2><<<a.grid, G::T, G::ntt_smem_words(pair_nr<G>()) * sizeof(uint32_t), a.stream>>>(

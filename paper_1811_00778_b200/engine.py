@@ -147,7 +147,8 @@ class GpuContext:
         """Geometry flags of the fused kernels (include/hcnn_b200.h: 16 one-row
         relinearisation, 32 radix-32 square tensor, 64 mixed-width passes, 512
         2-CTA cluster rows at 2^15, 1024 relinearisation sums in TMEM, 2048 /
-        4096 square tensor with rows parked in TMEM)."""
+        4096 square tensor with rows parked in TMEM, 8192 persistent square
+        tensor with TMA prefetch)."""
         _lib.check(_lib.lib().hcnn_ctx_set_option(self.handle, 1, int(variant)), "ntt variant")
 
     def variant(self) -> int:
