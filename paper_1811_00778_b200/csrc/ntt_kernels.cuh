@@ -551,6 +551,17 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
     mbar_expect_tx(bar, bytes);
     bulk_g2s(stage0 + (g % NS) * SM::STAGE_WORDS, dig_ct + (size_t)i * G::N, bytes, bar);
   };
+  // y0, y1 (added after the inverse) follow the last digit group into the
+  // stage it frees, so the epilogue does not wait on HBM
+  constexpr bool Y3PF = SM::STAGES == 2 && NR == 2;
+  auto issue_y3 = [&](int g) {
+    uint64_t* bar = &bars[g % 2];
+    uint32_t* dst = stage0 + (g % 2) * SM::STAGE_WORDS;
+    fence_proxy_async();
+    mbar_expect_tx(bar, 2 * G::N * 4);
+    bulk_g2s(dst, y3 + ((ct * 3 + 0) * K + j) * G::N, G::N * 4, bar);
+    bulk_g2s(dst + G::N, y3 + ((ct * 3 + 1) * K + j) * G::N, G::N * 4, bar);
+  };
   if constexpr (SM::STAGES > 0) {
     if (tid == 0) {
       for (int st = 0; st < SM::STAGES; ++st) mbar_init(&bars[st], 1);
@@ -568,7 +579,10 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
       // with two stages, group g+1 streams in while group g is transformed;
       // its buffer was last read before this thread's previous-group barriers
       if constexpr (SM::STAGES == 2) {
-        if (tid == 0 && i + R < D) issue(i + R, g + 1);
+        if (tid == 0) {
+          if (i + R < D) issue(i + R, g + 1);
+          else if constexpr (Y3PF) issue_y3(g + 1);  // the free stage takes y0, y1
+        }
       }
       const uint32_t* row = stage0 + (g % SM::STAGES) * SM::STAGE_WORDS;
       mbar_wait(&bars[g % SM::STAGES], (uint32_t)(g / SM::STAGES) & 1);
@@ -664,12 +678,13 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
       }
     }
   };
-  for (int i = 0, g = 0; i < D; ++g) {
+  int ngroups = 0;
+  for (int i = 0; i < D; ++ngroups) {
     const int R = group_rows(i);
     if (NR == 2 && R == 2) {
-      step(std::integral_constant<int, NR>(), i, g);
+      step(std::integral_constant<int, NR>(), i, ngroups);
     } else {
-      step(std::integral_constant<int, 1>(), i, g);
+      step(std::integral_constant<int, 1>(), i, ngroups);
       // a one-row transform's last exchange buffer overlaps the two-row one's first
       if constexpr (NR == 2) __syncthreads();
     }
@@ -700,6 +715,22 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
   } else {
     ntt_inv<G>(x, s, itw, p, ninv, tid);
     ntt_inv<G>(x + E, s, itw, p, ninv, tid);
+  }
+  if constexpr (Y3PF) {
+    if (ngroups > 0) {
+      mbar_wait(&bars[ngroups % 2], (uint32_t)(ngroups / 2) & 1);
+      const uint32_t* yst = stage0 + (ngroups % 2) * SM::STAGE_WORDS;
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        uint32_t* o = out + ((ct * 2 + part) * K + j) * G::N;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int idx = natural_index<G>(tid, e);
+          o[idx] = add_mod(x[part * E + e], yst[part * G::N + idx], p);
+        }
+      }
+      return;
+    }
   }
 #pragma unroll
   for (int part = 0; part < 2; ++part) {
