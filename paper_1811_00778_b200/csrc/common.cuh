@@ -161,19 +161,40 @@ DI uint32_t exact_v(const uint32_t (&xt)[K], const ConvTabs& tb) {
   return V;
 }
 
-// sum_{i<K} x_i c_i (+ v c_v), c's in Montgomery form mod m, reduced:
-// one REDC per <= 11 products (3 * 2^62 headroom)
+// Montgomery reduction by subtraction: acc * 2^-32 mod m for any acc < 2^64
+// with (acc >> 32) < 4m.  mpos = m^-1 mod 2^32 (minus the REDC constant):
+// u = lo(acc) mpos makes acc - u m a multiple of 2^32, so
+// (acc - u m) / 2^32 = hi(acc) - umulhi(u, m) exactly, in (-m, 4m).
+DI uint32_t redc_sub(uint64_t acc, uint32_t m, uint32_t minv) {
+  const uint32_t u = (uint32_t)acc * (0u - minv);
+  const uint32_t ah = (uint32_t)(acc >> 32), mh = __umulhi(u, m);
+  uint32_t r = ah - mh;
+  if (ah < mh) r += m;
+  r = umin_u32(r, r - 2 * m);
+  return umin_u32(r, r - m);
+}
+
+// sum_{i<K} x_i c_i (+ v c_v), x_i < 2^30, c's in Montgomery form mod m (< m),
+// v c_v < 2^60, reduced.  Up to 11 products: one REDC (3 * 2^62 headroom).
+// 12-15 products: the sum still stays below 2^64 with its high word below
+// 16 * 2^30 m / 2^32 = 4m, so one subtractive REDC (measured cheaper than two
+// REDCs; the additive one stays cheaper where it suffices).  Larger K: two
+// halves of <= 11.
 template <int K, class Getc>
 DI uint32_t mont_dot(const uint32_t* x, Getc c, uint32_t v, uint32_t cv, uint32_t m, uint32_t minv) {
-  constexpr int H = K <= 11 ? K : (K + 1) / 2;
+  constexpr int H = K <= 15 ? K : (K + 1) / 2;
   uint64_t a0 = (uint64_t)v * cv, a1 = 0;
 #pragma unroll
   for (int i = 0; i < H; ++i) a0 += (uint64_t)x[i] * c(i);
 #pragma unroll
   for (int i = H; i < K; ++i) a1 += (uint64_t)x[i] * c(i);
-  uint32_t r = redc(a0, m, minv);
-  if constexpr (H < K) r = add_mod(r, redc(a1, m, minv), m);
-  return r;
+  if constexpr (K <= 11) {
+    return redc(a0, m, minv);
+  } else if constexpr (K <= 15) {
+    return redc_sub(a0, m, minv);
+  } else {
+    return add_mod(redc(a0, m, minv), redc(a1, m, minv), m);
+  }
 }
 
 // x_j = (sum_i xt_i (q/q_i) - v q) mod p_j
