@@ -18,6 +18,7 @@ u = W["units"][0]
 h = torch.empty(u["gin"].data.shape, dtype=torch.int32, pin_memory=True)
 h.copy_(u["gin"].data)
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 10
+bands = int(sys.argv[2]) if len(sys.argv) > 2 else 6
 n_out = W["spec"].layers[-1].filters
 ho = [torch.empty((n_out,) + tuple(h.shape[1:]), dtype=torch.int32, pin_memory=True) for _ in range(steps)]
 stream = torch.cuda.current_stream()
@@ -31,7 +32,7 @@ def run(k, marks=None):
             ev.record(stream)
             marks.append((name, ev))
     E.eval_network_stream([h] * k, u["model"], u["rlk"], u["params"], u["gin"].shape, u["gin"].delta,
-                          E.OpCounter(), outputs=ho, layer_hook=hook)
+                          E.OpCounter(), outputs=ho, layer_hook=hook, bands=bands)
 
 
 run(3)
