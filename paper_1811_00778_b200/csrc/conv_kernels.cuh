@@ -233,10 +233,11 @@ cudaError_t conv_launch(int op, const ConvLaunch& a, const ConvTabs& tb) {
       k_extend<K, KP><<<a.grid, a.block, 0, a.stream>>>(a.in, a.out, a.N, tb);
       break;
     case 1: {
-      // V = 2 coefficients per thread: faster at K = 6 (0.95 vs 1.01 us per
-      // ciphertext), slower from K = 11 (2.47 vs 2.19 us: registers); the
-      // kernel is fmaheavy-bound (profiles/r1_micro_scale_v2.jsonl)
-      if (K <= 8 && a.N % (2 * a.block.x) == 0) {
+      // V = 2 coefficients per thread: faster up to K = 7 (K = 6: 0.95 vs
+      // 1.01 us per ciphertext), level at 8, slower above (K = 10: 1.96 vs
+      // 1.88; K = 11: 2.47 vs 2.19 us: registers); the kernel is
+      // fmaheavy-bound (profiles/r1_micro_scale_v2.jsonl)
+      if (K <= 7 && a.N % (2 * a.block.x) == 0) {
         dim3 g2(a.grid.x / 2 > 0 ? a.grid.x / 2 : 1, a.grid.y);
         k_scale<K, KP, 2><<<g2, a.block, 0, a.stream>>>(a.in, a.out, a.dig, a.N, tb);
       } else {
