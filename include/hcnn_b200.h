@@ -178,6 +178,15 @@ int hcnn_hadd(hcnn_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out
 int hcnn_ntt(hcnn_ctx* ctx, uint32_t* rows, size_t n_rows, uint32_t limbs, uint32_t prime_offset,
              int inverse);
 
+/* Host-side staging of the reference's residue arrays (no device work):
+ * dst[i * len + j] = (uint32_t)src[i][j] for count HOST int64 arrays of len
+ * residues each (RingElem.residues, ring.py:98-112: canonical [0, p), p <
+ * 2^30) into one HOST buffer (normally pinned, for the upload), split over
+ * `threads` host threads (<= 0: all cores).  HCNN_ERR_PARAM if a value lies
+ * outside [0, 2^32).  This is what engine.upload / eval_network do to a
+ * host CipherTensor before it crosses PCIe (engine.py:42-58 objects in). */
+int hcnn_host_narrow(const int64_t* const* src, size_t count, size_t len, uint32_t* dst, int threads);
+
 /* Per-kernel CUDA-event timing on the context's stream.  hcnn_profile(ctx, 1)
  * resets and starts recording; hcnn_profile_dump writes "name count total_ms"
  * lines (returns the text length, or -status). */

@@ -34,8 +34,26 @@ def _newest_source() -> float:
     return max(os.path.getmtime(p) for p in _sources())
 
 
+def _deps(src: str, seen=None) -> set:
+    """src plus every file it #includes with quotes, transitively."""
+    import re
+
+    seen = set() if seen is None else seen
+    src = os.path.normpath(src)
+    if src in seen or not os.path.exists(src):
+        return seen
+    seen.add(src)
+    with open(src) as fh:
+        for inc in re.findall(r'^\s*#\s*include\s+"([^"]+)"', fh.read(), re.M):
+            _deps(os.path.join(os.path.dirname(src), inc), seen)
+    return seen
+
+
 def _compile(args):
     src, obj, defs = args
+    if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in _deps(src)) \
+            and os.path.getmtime(obj) >= os.path.getmtime(__file__):
+        return obj  # up to date
     cmd = [NVCC, *FLAGS, *defs, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -3,6 +3,8 @@
 
 #include <cstring>
 #include <memory>
+#include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -44,6 +46,37 @@ int guarded(F&& f) {
 }
 
 void fail(int code, const std::string& m) { throw Error{code, m}; }
+
+// The library's own stream-ordered memory pool per device: workspaces and
+// temporaries stay pooled across synchronisations (release threshold = max)
+// without changing the device's default pool, which other cudaMallocAsync
+// users in the process (e.g. PyTorch's async allocator) share.
+std::mutex g_pool_mu;
+cudaMemPool_t g_pools[64] = {};
+
+cudaMemPool_t lib_pool(int device) {
+  if (device < 0 || device >= 64) fail(HCNN_ERR_PARAM, "device index out of range");
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!g_pools[device]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t pool;
+    CK(cudaMemPoolCreate(&pool, &props));
+    uint64_t keep = ~0ull;
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    g_pools[device] = pool;
+  }
+  return g_pools[device];
+}
+
+// cudaMallocAsync from the library pool of `device`
+template <class T>
+void pool_malloc(T** ptr, size_t bytes, cudaStream_t stream, int device) {
+  CK(cudaMallocFromPoolAsync((void**)ptr, bytes, lib_pool(device), stream));
+}
 
 }  // namespace
 
@@ -97,13 +130,14 @@ struct hcnn_ctx {
   size_t ws_bytes = 0;
   size_t ws_limit = size_t(6) << 30;  // whole MNIST layers (800 cts at set 1) in one chunk
   int64_t launches = 0;
+  cudaEvent_t switch_ev = nullptr;  // orders the old stream before the new one (hcnn_ctx_set_stream)
 
   uint8_t* workspace(size_t bytes) {
     if (bytes > ws_bytes) {
       if (ws) CK(cudaFreeAsync(ws, stream));
       ws = nullptr;
       ws_bytes = 0;
-      CK(cudaMallocAsync((void**)&ws, bytes, stream));
+      pool_malloc(&ws, bytes, stream, device);
       ws_bytes = bytes;
     }
     return ws;
@@ -759,7 +793,7 @@ __global__ void k_int_peak(uint32_t* out, uint32_t a, uint32_t b, int iters) {
 void upload_raw_key(hcnn_ctx* c, const uint64_t* host, size_t rows, uint32_t** raw) {
   const size_t count = rows * c->N;
   uint64_t* stage = nullptr;
-  CK(cudaMallocAsync((void**)&stage, count * sizeof(uint64_t), c->stream));
+  pool_malloc(&stage, count * sizeof(uint64_t), c->stream, c->device);
   if (!*raw) CK(cudaMalloc((void**)raw, count * sizeof(uint32_t)));
   CK(cudaMemcpyAsync(stage, host, count * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
   k_narrow<<<cdiv(count, 256), 256, 0, c->stream>>>(stage, *raw, count);
@@ -815,6 +849,46 @@ void prepare_keys(hcnn_ctx* c) {
 extern "C" {
 
 const char* hcnn_last_error(void) { return g_err.c_str(); }
+namespace {
+// one thread's share of hcnn_host_narrow; returns the OR of all inputs' high
+// words (non-zero: a value outside [0, 2^32))
+__attribute__((optimize("O3"))) uint64_t narrow_rows(const int64_t* const* src, size_t a, size_t b,
+                                                      size_t len, uint32_t* dst) {
+  uint64_t hi = 0;
+  for (size_t i = a; i < b; ++i) {
+    const uint64_t* __restrict__ s = reinterpret_cast<const uint64_t*>(src[i]);
+    uint32_t* __restrict__ d = dst + i * len;
+    for (size_t j = 0; j < len; ++j) {
+      const uint64_t v = s[j];
+      hi |= v;
+      d[j] = (uint32_t)v;
+    }
+  }
+  return hi >> 32;
+}
+}  // namespace
+
+int hcnn_host_narrow(const int64_t* const* src, size_t count, size_t len, uint32_t* dst, int threads) {
+  return guarded([&] {
+    if (!count || !len) return;
+    if (!src || !dst) fail(HCNN_ERR_PARAM, "null argument");
+    for (size_t i = 0; i < count; ++i)
+      if (!src[i]) fail(HCNN_ERR_PARAM, "null source array");
+    size_t nt = threads > 0 ? (size_t)threads : (size_t)std::thread::hardware_concurrency();
+    if (nt < 1) nt = 1;
+    if (nt > 64) nt = 64;
+    if (nt > count) nt = count;
+    std::vector<uint64_t> bad(nt, 0);
+    std::vector<std::thread> pool;
+    for (size_t k = 1; k < nt; ++k)
+      pool.emplace_back([&, k] { bad[k] = narrow_rows(src, count * k / nt, count * (k + 1) / nt, len, dst); });
+    bad[0] = narrow_rows(src, 0, count / nt, len, dst);
+    for (auto& t : pool) t.join();
+    for (uint64_t b : bad)
+      if (b) fail(HCNN_ERR_PARAM, "residue outside [0, 2^32): not a canonical RNS residue");
+  });
+}
+
 int hcnn_int_peak(int device, int kind, double* ops_per_s) {
   return guarded([&] {
     CK(cudaSetDevice(device));
@@ -888,14 +962,8 @@ int hcnn_ctx_create(hcnn_ctx** out, uint32_t n, uint32_t k, const uint64_t* prim
     auto c = std::make_unique<hcnn_ctx>();
     c->device = device;
     CK(cudaSetDevice(device));
-    {
-      // keep stream-ordered allocations (workspace, temporaries) in the pool
-      // across synchronisations instead of returning them to the driver
-      cudaMemPool_t pool;
-      CK(cudaDeviceGetDefaultMemPool(&pool, device));
-      uint64_t keep = ~0ull;
-      CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-    }
+    lib_pool(device);  // the library's own pool (stream-ordered workspace and temporaries)
+    CK(cudaEventCreateWithFlags(&c->switch_ev, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
     c->stream = c->own_stream;
     c->N = n;
@@ -932,6 +1000,7 @@ int hcnn_ctx_destroy(hcnn_ctx* c) {
     if (c->d_sk) cudaFree(c->d_sk);
     if (c->d_delta) cudaFree(c->d_delta);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    if (c->switch_ev) cudaEventDestroy(c->switch_ev);
     delete c;
   });
 }
@@ -977,7 +1046,16 @@ int64_t hcnn_profile_dump(hcnn_ctx* c, char* buf, size_t len) {
 }
 
 int hcnn_ctx_set_stream(hcnn_ctx* c, void* stream) {
-  return guarded([&] { c->stream = (cudaStream_t)stream; });
+  return guarded([&] {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (s == c->stream) return;
+    // everything already queued for this context (including the workspace
+    // it shares across calls, and any stream-ordered free of it) is ordered
+    // before the new stream's work
+    CK(cudaEventRecord(c->switch_ev, c->stream));
+    CK(cudaStreamWaitEvent(s, c->switch_ev, 0));
+    c->stream = s;
+  });
 }
 
 int hcnn_ctx_set_option(hcnn_ctx* c, int key, int64_t value) {
@@ -1098,7 +1176,7 @@ static int hcnn_encrypt_impl(hcnn_ctx* c, const int8_t* u, const int8_t* e1, con
     const size_t ch = n < 4096 ? n : 4096;
     uint8_t* stage = nullptr;
     const size_t bytes = ch * N * (3 + sizeof(int64_t));
-    CK(cudaMallocAsync((void**)&stage, bytes, c->stream));
+    pool_malloc(&stage, bytes, c->stream, c->device);
     for (size_t s0 = 0; s0 < n; s0 += ch) {
       const size_t m = n - s0 < ch ? n - s0 : ch;
       int8_t* du = (int8_t*)stage;
@@ -1202,7 +1280,7 @@ int hcnn_codec_decode(hcnn_codec* c, const uint64_t* polys, uint64_t* slots, siz
     if (smem > 200 * 1024) fail(HCNN_ERR_UNSUPPORTED, "slot count too large for the u64 NTT");
     CK(cudaFuncSetAttribute(k_ntt64<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     uint64_t* tmp = nullptr;
-    CK(cudaMallocAsync((void**)&tmp, rows * c->n * sizeof(uint64_t), st));
+    pool_malloc(&tmp, rows * c->n * sizeof(uint64_t), st, c->device);
     CK(cudaMemcpyAsync(tmp, polys, rows * c->n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
     k_ntt64<false><<<(unsigned)rows, 512, smem, st>>>(tmp, (int)c->logn, c->t, c->d_tw, c->ninv);
     CK(cudaGetLastError());
@@ -1218,7 +1296,7 @@ int hcnn_set_secret_key(hcnn_ctx* c, const uint8_t* s_bits) {
     CK(cudaSetDevice(c->device));
     const size_t N = c->N, K = c->K;
     uint8_t* ds = nullptr;
-    CK(cudaMallocAsync((void**)&ds, N, c->stream));
+    pool_malloc(&ds, N, c->stream, c->device);
     CK(cudaMemcpyAsync(ds, s_bits, N, cudaMemcpyHostToDevice, c->stream));
     if (!c->d_sk) CK(cudaMalloc((void**)&c->d_sk, K * N * sizeof(uint32_t)));
     k_sk_rows<<<cdiv(N, 256), 256, 0, c->stream>>>(ds, c->d_sk, (int)K, (int)N);
@@ -1238,7 +1316,7 @@ int hcnn_keygen(hcnn_ctx* c, const uint8_t* s_bits, const uint64_t* a_ref, const
     const unsigned logn = c->logN;
     // secret key rows in the device NTT order (also the decryption key)
     uint8_t* ds = nullptr;
-    CK(cudaMallocAsync((void**)&ds, N, c->stream));
+    pool_malloc(&ds, N, c->stream, c->device);
     CK(cudaMemcpyAsync(ds, s_bits, N, cudaMemcpyHostToDevice, c->stream));
     if (!c->d_sk) CK(cudaMalloc((void**)&c->d_sk, K * N * sizeof(uint32_t)));
     k_sk_rows<<<cdiv(N, 256), 256, 0, c->stream>>>(ds, c->d_sk, (int)K, (int)N);
@@ -1249,13 +1327,13 @@ int hcnn_keygen(hcnn_ctx* c, const uint8_t* s_bits, const uint64_t* a_ref, const
     uint64_t* stage = nullptr;
     uint32_t *da = nullptr, *adev = nullptr, *erow = nullptr, *out = nullptr, *dw = nullptr;
     int8_t* de = nullptr;
-    CK(cudaMallocAsync((void**)&stage, count * sizeof(uint64_t), c->stream));
-    CK(cudaMallocAsync((void**)&da, count * sizeof(uint32_t), c->stream));
-    CK(cudaMallocAsync((void**)&adev, count * sizeof(uint32_t), c->stream));
-    CK(cudaMallocAsync((void**)&erow, count * sizeof(uint32_t), c->stream));
-    CK(cudaMallocAsync((void**)&out, count * sizeof(uint32_t), c->stream));
-    CK(cudaMallocAsync((void**)&de, R * N, c->stream));
-    CK(cudaMallocAsync((void**)&dw, rows * sizeof(uint32_t), c->stream));
+    pool_malloc(&stage, count * sizeof(uint64_t), c->stream, c->device);
+    pool_malloc(&da, count * sizeof(uint32_t), c->stream, c->device);
+    pool_malloc(&adev, count * sizeof(uint32_t), c->stream, c->device);
+    pool_malloc(&erow, count * sizeof(uint32_t), c->stream, c->device);
+    pool_malloc(&out, count * sizeof(uint32_t), c->stream, c->device);
+    pool_malloc(&de, R * N, c->stream, c->device);
+    pool_malloc(&dw, rows * sizeof(uint32_t), c->stream, c->device);
     CK(cudaMemcpyAsync(stage, a_ref, count * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
     k_narrow<<<cdiv(count, 256), 256, 0, c->stream>>>(stage, da, count);
     c->launched("k_narrow");
@@ -1312,7 +1390,7 @@ int hcnn_decrypt(hcnn_ctx* c, const uint32_t* cts, uint64_t* m, size_t n) {
     c->mark();
     const size_t N = c->N, K = c->K, kn = K * N;
     uint32_t* tmp = nullptr;
-    CK(cudaMallocAsync((void**)&tmp, n * kn * sizeof(uint32_t), c->stream));
+    pool_malloc(&tmp, n * kn * sizeof(uint32_t), c->stream, c->device);
     // c1 of every ciphertext -> tmp, then c1 * s in the NTT domain
     CK(cudaMemcpy2DAsync(tmp, kn * sizeof(uint32_t), cts + kn, 2 * kn * sizeof(uint32_t),
                          kn * sizeof(uint32_t), n, cudaMemcpyDeviceToDevice, c->stream));
@@ -1336,7 +1414,7 @@ int hcnn_decrypt(hcnn_ctx* c, const uint32_t* cts, uint64_t* m, size_t n) {
 int hcnn_alloc(hcnn_ctx* c, size_t bytes, void** out) {
   return guarded([&] {
     CK(cudaSetDevice(c->device));
-    CK(cudaMallocAsync(out, bytes, c->stream));
+    pool_malloc(out, bytes, c->stream, c->device);
   });
 }
 
@@ -1351,7 +1429,7 @@ int hcnn_upload_u64(hcnn_ctx* c, uint32_t* dst, const uint64_t* src, size_t coun
   return guarded([&] {
     CK(cudaSetDevice(c->device));
     uint64_t* stage = nullptr;
-    CK(cudaMallocAsync((void**)&stage, count * sizeof(uint64_t), c->stream));
+    pool_malloc(&stage, count * sizeof(uint64_t), c->stream, c->device);
     CK(cudaMemcpyAsync(stage, src, count * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
     k_narrow<<<cdiv(count, 256), 256, 0, c->stream>>>(stage, dst, count);
     c->launched("k_narrow");
@@ -1364,7 +1442,7 @@ int hcnn_download_u64(hcnn_ctx* c, uint64_t* dst, const uint32_t* src, size_t co
   return guarded([&] {
     CK(cudaSetDevice(c->device));
     uint64_t* stage = nullptr;
-    CK(cudaMallocAsync((void**)&stage, count * sizeof(uint64_t), c->stream));
+    pool_malloc(&stage, count * sizeof(uint64_t), c->stream, c->device);
     k_widen<<<cdiv(count, 256), 256, 0, c->stream>>>(src, stage, count);
     c->launched("k_widen");
     CK(cudaMemcpyAsync(dst, stage, count * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
@@ -1403,7 +1481,7 @@ int hcnn_weights_create(hcnn_ctx* c, const int64_t* w, size_t count, hcnn_weight
     }
     if (count) {
       int64_t* stage = nullptr;
-      CK(cudaMallocAsync((void**)&stage, count * sizeof(int64_t), c->stream));
+      pool_malloc(&stage, count * sizeof(int64_t), c->stream, c->device);
       CK(cudaMemcpyAsync(stage, w, count * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
       if (h->small) {
         CK(cudaMalloc((void**)&h->wb, count * sizeof(uint16_t)));
@@ -1469,12 +1547,19 @@ int hcnn_conv(hcnn_ctx* c, const uint32_t* in, uint32_t* out, int h, int w, int 
         break;
       }
     const size_t zdim = (size_t)g.oh * g.ow * (f / fb);
-    if (zdim > 65535) fail(HCNN_ERR_CAPACITY, "conv: too many output blocks for one launch");
-    dim3 grid(cdiv(c->N / 4, tpb), 2 * c->K, (unsigned)zdim);
+    if (zdim > (size_t)INT32_MAX) fail(HCNN_ERR_CAPACITY, "conv: output too large");
     const size_t smem_d = (size_t)fb * kh * kw * g.cg * sizeof(double) + (size_t)kh * kw * g.cg * sizeof(int);
-    if (wt->wd && wt->flush >= 16 && smem_d <= 96 * 1024) {
-      const dim3 gridp(cdiv(c->N / 4, tpb), 2, (unsigned)zdim);
-      switch (fb) {
+    const size_t smem = (size_t)fb * kh * kw * g.cg * sizeof(uint16_t);
+    const int path = (wt->wd && wt->flush >= 16 && smem_d <= 96 * 1024) ? 0 : (wt->small && smem <= 48 * 1024) ? 1 : 2;
+    if (path == 2 && !wt->wred) fail(HCNN_ERR_CAPACITY, "conv: filter too large for the small-weight kernel");
+    // grid z holds at most 65535 blocks: tile the output blocks over launches
+    for (size_t z0 = 0; z0 < zdim; z0 += 65535) {
+      const unsigned zn = (unsigned)(zdim - z0 < 65535 ? zdim - z0 : 65535);
+      g.z0 = (int)z0;
+      const dim3 grid(cdiv(c->N / 4, tpb), 2 * c->K, zn);
+      if (path == 0) {
+        const dim3 gridp(cdiv(c->N / 4, tpb), 2, zn);
+        switch (fb) {
 #define X(FB)                                                                                           \
   case FB: {                                                                                            \
     static std::atomic<uint64_t> cfg{0};                                                                \
@@ -1484,35 +1569,30 @@ int hcnn_conv(hcnn_ctx* c, const uint32_t* in, uint32_t* out, int h, int w, int 
     k_conv_f64<FB><<<gridp, tpb, smem_d, c->stream>>>(in, out, wt->wd, g, (int)c->K, (int)c->N, wt->flush, c->d_prime); \
     break;                                                                                              \
   }
-        X(1) X(2) X(4) X(5) X(8)
+          X(1) X(2) X(4) X(5) X(8)
 #undef X
-      }
-      c->launched("k_conv");
-      return;
-    }
-    const size_t smem = (size_t)fb * kh * kw * g.cg * sizeof(uint16_t);
-    if (wt->small && smem <= 48 * 1024) {
-      switch (fb) {
+        }
+      } else if (path == 1) {
+        switch (fb) {
 #define X(FB)                                                                                          \
   case FB:                                                                                             \
     k_conv_sw<FB><<<grid, tpb, smem, c->stream>>>(in, out, wt->wb, g, (int)c->K, (int)c->N, c->d_prime, c->d_mu); \
     break;
-        X(1) X(2) X(4) X(5) X(8)
+          X(1) X(2) X(4) X(5) X(8)
 #undef X
-      }
-      c->launched("k_conv");
-      return;
-    }
-    if (!wt->wred) fail(HCNN_ERR_CAPACITY, "conv: filter too large for the small-weight kernel");
-    switch (fb) {
+        }
+      } else {
+        switch (fb) {
 #define X(FB)                                                                                       \
   case FB:                                                                                          \
     k_conv<FB><<<grid, tpb, 0, c->stream>>>(in, out, wt->wred, g, (int)c->K, (int)c->N, c->d_prime, c->d_mu); \
     break;
-      X(1) X(2) X(4) X(5) X(8)
+          X(1) X(2) X(4) X(5) X(8)
 #undef X
+        }
+      }
+      c->launched("k_conv");
     }
-    c->launched("k_conv");
   });
 }
 
@@ -1592,11 +1672,15 @@ int hcnn_pool(hcnn_ctx* c, const uint32_t* in, uint32_t* out, int h, int w, int 
     const int oh = (h - e) / sh + 1, ow = (w - e) / sw + 1;
     if (oh <= 0 || ow <= 0) fail(HCNN_ERR_PARAM, "pool: empty output");
     const size_t nout = (size_t)oh * ow * ch;
-    if (nout > 65535) fail(HCNN_ERR_CAPACITY, "pool: too many outputs for one launch");
+    if (nout > (size_t)INT32_MAX) fail(HCNN_ERR_CAPACITY, "pool: output too large");
     const unsigned tpb = c->N >= 512 ? 128 : (c->N / 4 >= 32 ? c->N / 4 : 32);
-    dim3 grid(cdiv(c->N / 4, tpb), 2 * c->K, (unsigned)nout);
-    k_pool<<<grid, tpb, 0, c->stream>>>(in, out, h, w, ch, e, sh, sw, ow, (int)c->K, (int)c->N, c->d_prime, c->d_mu);
-    c->launched("k_pool");
+    for (size_t o0 = 0; o0 < nout; o0 += 65535) {  // grid z <= 65535 blocks per launch
+      const unsigned zn = (unsigned)(nout - o0 < 65535 ? nout - o0 : 65535);
+      dim3 grid(cdiv(c->N / 4, tpb), 2 * c->K, zn);
+      k_pool<<<grid, tpb, 0, c->stream>>>(in, out, h, w, ch, e, sh, sw, ow, (int)c->K, (int)c->N, c->d_prime,
+                                          c->d_mu, (int)o0);
+      c->launched("k_pool");
+    }
   });
 }
 
@@ -1670,7 +1754,7 @@ int hcnn_hfir_unpack(hcnn_ctx* c, const uint64_t* hfir, size_t rows, uint32_t* r
     const size_t total = rows * c->N;
     if (!total) return;
     int* bad = nullptr;
-    CK(cudaMallocAsync((void**)&bad, sizeof(int), c->stream));
+    pool_malloc(&bad, sizeof(int), c->stream, c->device);
     CK(cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
     k_hfir_unpack<<<cdiv(total, 256), 256, 0, c->stream>>>(hfir, rows_out, (int)c->K, (int)c->N, rows,
                                                             c->d_prime, bad);
@@ -1699,7 +1783,7 @@ int hcnn_mul_plain(hcnn_ctx* c, const uint32_t* cts, const int64_t* pt, uint32_t
         sres[i] = (uint32_t)(r < 0 ? r + p : r);
       }
       uint32_t* d_s = nullptr;
-      CK(cudaMallocAsync((void**)&d_s, K * sizeof(uint32_t), c->stream));
+      pool_malloc(&d_s, K * sizeof(uint32_t), c->stream, c->device);
       CK(cudaMemcpyAsync(d_s, sres.data(), K * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
       const size_t total = n * 2 * K * N;
       k_mul_scalar<<<cdiv(total, 256), 256, 0, c->stream>>>(cts, out, d_s, (int)K, (int)N, total, c->d_prime,
@@ -1710,8 +1794,8 @@ int hcnn_mul_plain(hcnn_ctx* c, const uint32_t* cts, const int64_t* pt, uint32_t
     }
     int64_t* d_pt = nullptr;
     uint32_t* rows = nullptr;
-    CK(cudaMallocAsync((void**)&d_pt, N * sizeof(int64_t), c->stream));
-    CK(cudaMallocAsync((void**)&rows, K * N * sizeof(uint32_t), c->stream));
+    pool_malloc(&d_pt, N * sizeof(int64_t), c->stream, c->device);
+    pool_malloc(&rows, K * N * sizeof(uint32_t), c->stream, c->device);
     const std::vector<int64_t> hpt(pt, pt + N);  // pageable copy: staged before the call returns
     CK(cudaMemcpyAsync(d_pt, hpt.data(), N * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
     k_lift_plain<<<cdiv(N, 256), 256, 0, c->stream>>>(d_pt, rows, (int)N, (int)K, c->d_prime);

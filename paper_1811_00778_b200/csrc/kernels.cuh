@@ -9,6 +9,7 @@ namespace hcnn {
 // fit before a reduction (15 * (2^30-1)^2 + 2^30 < 2^64).
 struct ConvGeom {
   int h, w, c, f, kh, kw, cg, sh, sw, ph, pw, oh, ow, per_group;
+  int z0;  // first output block of this launch (launches are tiled by 65535 blocks in z)
 };
 
 DI void mac4(uint64_t* a, uint32_t wv, uint4 x) {
@@ -28,7 +29,8 @@ __global__ void k_conv(const uint32_t* __restrict__ in, uint32_t* __restrict__ o
   if (quad * 4 >= N) return;
   const int limb = blockIdx.y % K, part = blockIdx.y / K;
   const int nfb = g.f / FB;
-  const int pos = blockIdx.z / nfb, fbk = blockIdx.z % nfb;
+  const int zb = blockIdx.z + g.z0;
+  const int pos = zb / nfb, fbk = zb % nfb;
   const int oy = pos / g.ow, ox = pos % g.ow;
   const int f0 = fbk * FB;
   const int grp = f0 / g.per_group;
@@ -132,7 +134,8 @@ __global__ void __launch_bounds__(128)
   extern __shared__ uint16_t wsm[];
   const int taps = g.kh * g.kw * g.cg;
   const int nfb = g.f / FB;
-  const int pos = blockIdx.z / nfb, fbk = blockIdx.z % nfb;
+  const int zb = blockIdx.z + g.z0;
+  const int pos = zb / nfb, fbk = zb % nfb;
   const int f0 = fbk * FB;
   for (int idx = threadIdx.x; idx < FB * taps; idx += blockDim.x) wsm[idx] = wb[(size_t)f0 * taps + idx];
   __syncthreads();
@@ -263,7 +266,8 @@ __global__ void __launch_bounds__(128)
   const int taps = g.kh * g.kw * g.cg;
   int* tct = reinterpret_cast<int*>(wsd + FB * taps);
   const int nfb = g.f / FB;
-  const int pos = blockIdx.z / nfb, fbk = blockIdx.z % nfb;
+  const int zb = blockIdx.z + g.z0;
+  const int pos = zb / nfb, fbk = zb % nfb;
   const int f0 = fbk * FB;
   const int oy = pos / g.ow, ox = pos % g.ow;
   const int grp = f0 / g.per_group;
@@ -510,14 +514,14 @@ __global__ void k_bias_weights(const int64_t* __restrict__ w, size_t n, uint16_t
   if (t < n) out[t] = (uint16_t)(w[t] + (int64_t)WBIAS);
 }
 
-// sum-pool: grid x = quads, y = part*K + limb, z = output ct
+// sum-pool: grid x = quads, y = part*K + limb, z = output ct - o0
 __global__ void k_pool(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int h, int w,
                        int c, int e, int sh, int sw, int ow, int K, int N,
-                       const uint32_t* __restrict__ primes, const uint64_t* __restrict__ mus) {
+                       const uint32_t* __restrict__ primes, const uint64_t* __restrict__ mus, int o0) {
   const int quad = blockIdx.x * blockDim.x + threadIdx.x;
   if (quad * 4 >= N) return;
   const int limb = blockIdx.y % K, part = blockIdx.y / K;
-  const int o = blockIdx.z;
+  const int o = blockIdx.z + o0;
   const int ch = o % c, pos = o / c;
   const int oy = pos / ow, ox = pos % ow;
   uint64_t a[4] = {0, 0, 0, 0};

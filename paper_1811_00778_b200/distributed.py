@@ -34,18 +34,28 @@ def shard_plan(n_batches: int, n_channels: int, world: int) -> list:
     return [units[r::world] for r in range(world)]
 
 
-def gather_units(local: list, plan: list, rank: int, world: int, dst: int = 0, group=None):
+def gather_units(local: list, plan: list, rank: int, world: int, dst: int = 0, group=None,
+                 template: torch.Tensor | None = None):
     """Gather per-unit result tensors (all of one shape/dtype) to `dst`.
 
     local: tensors for plan[rank], in order.  Returns {Unit: tensor} on dst,
-    None elsewhere.  Ranks with fewer units send zero padding.
+    None elsewhere.  Ranks with fewer units send zero padding; a rank with
+    no units needs `template` (a tensor of the unit shape/dtype/device).
+    The plan is identical on every rank, so a plan this call cannot serve is
+    rejected on every rank before any collective starts (no rank is left
+    waiting inside the gather).
     """
+    if len(plan) != world:
+        raise ValueError(f"plan has {len(plan)} ranks, world is {world}")
+    if len(local) != len(plan[rank]):
+        raise ValueError(f"rank {rank}: {len(local)} results for {len(plan[rank])} units")
     if world == 1:
         return {u: t for u, t in zip(plan[0], local)}
     max_units = max(len(p) for p in plan)
-    if not local:
-        raise ValueError("every rank needs at least one unit (use fewer ranks)")
-    shape, dtype, device = local[0].shape, local[0].dtype, local[0].device
+    if min(len(p) for p in plan) == 0 and template is None:
+        raise ValueError("a rank of the plan has no units: pass `template` (or use fewer ranks)")
+    like = local[0] if local else template
+    shape, dtype, device = like.shape, like.dtype, like.device
     send = torch.zeros((max_units,) + tuple(shape), dtype=dtype, device=device)
     for i, t in enumerate(local):
         send[i].copy_(t)

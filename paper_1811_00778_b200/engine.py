@@ -321,22 +321,103 @@ def _to_host_cts(res: np.ndarray, params, host_types) -> list:
     return out
 
 
+class _HostStager:
+    """Pinned u32 staging buffer for host CipherTensors, one per context and
+    reused across calls (a fresh pin_memory() per call costs more than the
+    copy).  The reference's residues are int64 numpy arrays, one per part
+    and ciphertext; they are narrowed to u32 straight into the pinned buffer
+    by a thread pool (numpy's casting copy releases the GIL), in row ranges
+    so that uploads can start on the first rows while later ones are filled."""
+
+    _pool = None
+
+    def __init__(self):
+        self.buf = None
+        self.free = None  # event after the last upload out of `buf`
+
+    @classmethod
+    def pool(cls):
+        if cls._pool is None:
+            import concurrent.futures
+
+            cls._pool = concurrent.futures.ThreadPoolExecutor(
+                max_workers=max(1, min(16, os.cpu_count() or 1)), thread_name_prefix="hcnn-stage")
+        return cls._pool
+
+    def get(self, n: int, K: int, N: int) -> torch.Tensor:
+        if self.buf is None or self.buf.shape[0] < n or tuple(self.buf.shape[1:]) != (2, K, N):
+            self.buf = torch.empty((max(n, 1), 2, K, N), dtype=torch.int32, pin_memory=True)
+            self.free = None
+        if self.free is not None:
+            self.free.synchronize()  # the previous call's uploads have left the buffer
+        return self.buf[:n]
+
+    def fill(self, stage: torch.Tensor, cts, lo: int, hi: int):
+        """stage[lo:hi] <- cts[lo:hi] (int64 residues narrowed to u32): one
+        multi-threaded native call (hcnn_host_narrow) when every part is a
+        C-contiguous int64 [K][N] array, numpy casting copies otherwise."""
+        if hi <= lo:
+            return
+        K, N = stage.shape[2], stage.shape[3]
+        ptrs = np.empty(2 * (hi - lo), dtype=np.uintp)
+        k = 0
+        for ct in cts[lo:hi]:
+            for part in ct.parts:
+                r = part.residues
+                if r.dtype != np.int64 or r.shape != (K, N) or not r.flags.c_contiguous:
+                    return self._fill_numpy(stage, cts, lo, hi)
+                ptrs[k] = r.ctypes.data
+                k += 1
+        dst = stage.data_ptr() + lo * 2 * K * N * 4
+        _lib.check(_lib.lib().hcnn_host_narrow(ptrs.ctypes.data, 2 * (hi - lo), K * N, _lib.C.c_void_p(dst),
+                                               min(32, os.cpu_count() or 1)), "hcnn_host_narrow")
+
+    def _fill_numpy(self, stage, cts, lo, hi):
+        arr = stage.numpy().view(np.uint32)
+
+        def job(a, b):
+            for i in range(a, b):
+                p0, p1 = cts[i].parts
+                np.copyto(arr[i, 0], p0.residues, casting="unsafe")
+                np.copyto(arr[i, 1], p1.residues, casting="unsafe")
+
+        pool = self.pool()
+        nw = pool._max_workers
+        cuts = np.linspace(lo, hi, min(hi - lo, 4 * nw) + 1).astype(np.int64)
+        for f in [pool.submit(job, int(a), int(b)) for a, b in zip(cuts[:-1], cuts[1:])]:
+            f.result()
+
+
+def _stager(g) -> _HostStager:
+    st = getattr(g, "_stager", None)
+    if st is None:
+        st = g._stager = _HostStager()
+    return st
+
+
+def _check_host_cts(tensor, params):
+    fp = params.fingerprint
+    for ct in tensor.cts:
+        if ct.fingerprint != fp:
+            raise ParameterMismatchError("ciphertext does not match parameter set")
+        if len(ct.parts) != 2:
+            raise ParameterMismatchError("evaluator expects 2-part ciphertexts")
+
+
 def upload(tensor, params, device=None) -> GpuCipherTensor:
     """Host CipherTensor -> GpuCipherTensor (u64 residues narrowed to u32)."""
     if isinstance(tensor, GpuCipherTensor):
         return tensor
     g = context_for(params, device)
-    for ct in tensor.cts:
-        if ct.fingerprint != params.fingerprint:
-            raise ParameterMismatchError("ciphertext does not match parameter set")
-        if len(ct.parts) != 2:
-            raise ParameterMismatchError("evaluator expects 2-part ciphertexts")
+    _check_host_cts(tensor, params)
     n = len(tensor.cts)
-    host = np.empty((n, 2, g.K, g.N), dtype=np.uint32)
-    for i, ct in enumerate(tensor.cts):
-        host[i, 0] = ct.parts[0].residues
-        host[i, 1] = ct.parts[1].residues
-    data = torch.from_numpy(host.view(np.int32)).pin_memory().to(f"cuda:{g.device}", non_blocking=True)
+    st = _stager(g)
+    stage = st.get(n, g.K, g.N)
+    st.fill(stage, tensor.cts, 0, n)
+    data = g.empty(n)
+    data.copy_(stage, non_blocking=True)
+    st.free = torch.cuda.Event()
+    st.free.record(torch.cuda.current_stream(data.device))
     return GpuCipherTensor(tensor.shape, data, tensor.delta, tensor.channel_modulus, params,
                            _host_types_of(tensor, params))
 
@@ -497,9 +578,45 @@ def eval_network(tensor, model, rlk, params, counter=None, workers: int = 1, cap
     (engine.py:400-423).  Host input -> host output; GPU input -> GPU output;
     layer_hook receives GpuCipherTensors (their .cts download on demand)."""
     counter = counter if counter is not None else OpCounter()
+    if not isinstance(tensor, GpuCipherTensor) and _bandable(model, tensor.shape) and len(tensor.cts) > 1:
+        return _eval_network_host(tensor, model, rlk, params, counter, capacity, layer_hook)
     x, was_host = _as_gpu(tensor, params)
     x = _eval_layers(x, model, 0, rlk, params, counter, workers, capacity, layer_hook)
     return _ret(x, was_host)
+
+
+def _eval_network_host(tensor, model, rlk, params, counter, capacity=None, layer_hook=None, bands: int = 6):
+    """eval_network of a host CipherTensor (the reference's own objects): its
+    int64 residues are narrowed into a reused pinned buffer by row bands, each
+    band is uploaded on a copy stream as soon as it is filled, and conv1 +
+    square1 of a band start as soon as its input rows are on the device, so
+    the host-side narrowing and the upload overlap the evaluation.  Same
+    kernels, results and counters as the device path (engine.py:400-423)."""
+    if tensor.channel_modulus != params.t:
+        raise ParameterMismatchError("tensor channel does not match params")
+    _, kh, kw, _ = np.asarray(model.weights[0]).shape
+    if capacity is not None and capacity < kh * kw:
+        raise CapacityError(f"capacity {capacity} below filter size {kh * kw}")
+    _check_host_cts(tensor, params)
+    g = context_for(params)
+    dev = torch.device("cuda", g.device)
+    compute = torch.cuda.current_stream(dev)
+    up_stream, _ = _copy_streams(dev)
+    up_stream.wait_stream(compute)
+    st = _stager(g)
+    n = len(tensor.cts)
+    stage = st.get(n, g.K, g.N)
+    buf = g.empty(n)
+    buf.record_stream(up_stream)
+    x, released = _banded_head(stage, buf, tuple(tensor.shape), tensor.delta, model, rlk, params, counter,
+                               up_stream, compute, bands, layer_hook,
+                               prepare=lambda lo, hi: st.fill(stage, tensor.cts, lo, hi),
+                               host_types=_host_types_of(tensor, params))
+    st.free = torch.cuda.Event()
+    st.free.record(up_stream)
+    compute.wait_stream(up_stream)
+    x = _eval_layers(x, model, 2, rlk, params, counter, layer_hook=layer_hook)
+    return x.to_host()
 
 
 def _eval_layers(x, model, start, rlk, params, counter, workers=1, capacity=None, layer_hook=None):
@@ -539,12 +656,17 @@ def _bandable(model, shape) -> bool:
             and kind_of(layers[1]) == "square" and shape[0] >= 2)
 
 
-def _banded_head(hb, buf, shape, delta, model, rlk, params, counter, up_stream, compute, bands, layer_hook):
+def _banded_head(hb, buf, shape, delta, model, rlk, params, counter, up_stream, compute, bands, layer_hook,
+                 prepare=None, host_types=None):
     """conv1 + square1 of one batch by output-row bands, each band starting as
     soon as the input rows it reads are uploaded (the upload of the next band
     overlaps the square of this one).  Same kernels, same results and counters
     as eval_conv + eval_square on the whole tensor (engine.py:237-364).
-    Returns (square output tensor, event after the last read of `buf`)."""
+    `prepare(lo, hi)`, when given, fills host ciphertexts [lo, hi) of `hb`
+    before they are uploaded (the drop-in path narrows the caller's residues
+    there).  Returns (square output tensor, event after the last read of `buf`)."""
+    if hb.shape[0] != shape[0] * shape[1] * shape[2]:
+        raise ParameterMismatchError("ciphertext count != h*w*c")
     conv, weights = model.spec.layers[0], np.asarray(model.weights[0])
     h, w, c = shape
     f, kh, kw, cg = weights.shape
@@ -567,6 +689,8 @@ def _banded_head(hb, buf, shape, delta, model, rlk, params, counter, up_stream, 
             continue
         hi = (y1 - 1) * sh + kh
         if hi > uploaded:
+            if prepare is not None:
+                prepare(uploaded * row, hi * row)
             with torch.cuda.stream(up_stream):
                 buf[uploaded * row:hi * row].copy_(hb[uploaded * row:hi * row], non_blocking=True)
                 ready = torch.cuda.Event()
@@ -584,8 +708,8 @@ def _banded_head(hb, buf, shape, delta, model, rlk, params, counter, up_stream, 
     _count(counter, *_conv_counts(h, w, conv, weights))
     counter.hsquare += oh * ow * f
     d1 = delta * conv.weight_scale
-    x1 = GpuCipherTensor((oh, ow, f), cout, d1, params.t, params)
-    x2 = GpuCipherTensor((oh, ow, f), sq, d1 * d1, params.t, params)
+    x1 = GpuCipherTensor((oh, ow, f), cout, d1, params.t, params, host_types)
+    x2 = GpuCipherTensor((oh, ow, f), sq, d1 * d1, params.t, params, host_types)
     if layer_hook is not None:
         layer_hook(conv.name, x1)
         layer_hook(model.spec.layers[1].name, x2)
@@ -623,6 +747,9 @@ def eval_network_stream(batches, model, rlk, params, shape, delta, counter=None,
         slot = i % 2
         if tuple(hb.shape[1:]) != (2, len(params.ctx.primes), int(params.ctx.ring_degree)):
             raise ParameterMismatchError("batch layout does not match params")
+        if hb.shape[0] != shape[0] * shape[1] * shape[2]:
+            raise ParameterMismatchError(f"batch {i} holds {hb.shape[0]} ciphertexts, shape {tuple(shape)} "
+                                         f"needs {shape[0] * shape[1] * shape[2]}")
         if bufs[slot] is None or bufs[slot].shape != hb.shape:
             # allocated on the compute stream (which reads it), written by the
             # copy stream: record_stream keeps the block until both are done
@@ -747,6 +874,9 @@ def keygen_device(params, rng, device=None):
     rlk = _b.RelinKey([(el(rlk_out[i, 0]), el(rlk_out[i, 1])) for i in range(d)], params.w, params.fingerprint)
     g._pk_ref = weakref.ref(pk)
     g._rlk_ref = weakref.ref(rlk)
+    # hcnn_keygen installed this secret key on the device: keep the
+    # decrypt-side cache (decrypt_device) in step with it
+    g._sk_key = hashlib.blake2b(s8.tobytes(), digest_size=16).digest()
     return sk, pk, rlk
 
 
@@ -814,7 +944,7 @@ def decrypt_device(tensor: GpuCipherTensor, sk, params) -> torch.Tensor:
     """bfv.decrypt (bfv.py:239-250) of every ciphertext on the GPU: [n][N]
     plaintext polys in [0, t) (int64, device).  Requires t < 2^48."""
     g = context_for(params, tensor.data.device)
-    s = np.ascontiguousarray(np.asarray(sk.s_bits, dtype=np.uint8))
+    s = np.ascontiguousarray(np.asarray(sk.s_bits).astype(np.uint8))
     key = hashlib.blake2b(s.tobytes(), digest_size=16).digest()
     if getattr(g, "_sk_key", None) != key:
         g.bind_stream()

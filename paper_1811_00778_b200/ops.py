@@ -143,9 +143,10 @@ def hsquare(c, rlk, params):
     if rlk is None:
         raise MissingKeyError("relinearization key required for hsquare")
     g = context_for(params)
+    like = c  # results come back in the caller's Ciphertext / RingElem classes
     if len(c.parts) == 3:
         c = relinearize(c.parts, rlk, params)
-    return _unstack(square_device(g, _stack([c], g, 2), rlk), c, params)[0]
+    return _unstack(square_device(g, _stack([c], g, 2), rlk), like, params)[0]
 
 
 def hmult_raw(c1, c2, params):
@@ -176,26 +177,44 @@ def hmult(c1, c2, rlk, params):
     return _unstack(hmult_device(g, a, b, rlk), c1, params)[0]
 
 
+class _Parts:
+    """A bare holder of ciphertext parts (what _stack reads)."""
+
+    def __init__(self, parts):
+        self.parts = tuple(parts)
+
+
+def _ciphertext_class_for(elem):
+    """The Ciphertext class that goes with the caller's RingElem class: the
+    reference's bfv.Ciphertext when the parts are hefir RingElems (hefir.ring ->
+    hefir.bfv), else this package's mirror."""
+    import importlib
+    import sys
+
+    mod = type(elem).__module__
+    pkg = mod.rsplit(".", 1)[0] if "." in mod else ""
+    if pkg and (pkg + ".bfv" in sys.modules or mod == pkg + ".ring"):
+        try:
+            cls = getattr(importlib.import_module(pkg + ".bfv"), "Ciphertext", None)
+            if cls is not None:
+                return cls
+        except ImportError:
+            pass
+    from .bfv import Ciphertext
+
+    return Ciphertext
+
+
 def relinearize(parts3, rlk, params):
+    """bfv.relinearize (bfv.py:368-404): 3 parts -> a 2-part ciphertext in the
+    caller's classes."""
     if rlk is None:
         raise MissingKeyError("relinearization key required")
     _check(params, rlk.fingerprint)
     g = context_for(params)
-
-    class _C:
-        pass
-
-    holder = _C()
-    holder.parts = tuple(parts3)
-    x3 = _stack([holder], g, 3)
-    out = relinearize_device(g, x3, rlk)
-    like_ct = type("Ct", (), {})
-    # build outputs with the caller's RingElem class and our Ciphertext mirror
-    from .bfv import Ciphertext
-
+    out = relinearize_device(g, _stack([_Parts(parts3)], g, 3), rlk)
     el = parts3[0]
     torch.cuda.current_stream(out.device).synchronize()
     res = out.cpu().numpy().view(np.uint32).astype(np.int64)
     parts = tuple(type(el)(el.ctx, np.ascontiguousarray(res[0, p]), el.domain) for p in range(2))
-    del like_ct
-    return Ciphertext(parts=parts, fingerprint=params.fingerprint)
+    return _ciphertext_class_for(el)(parts=parts, fingerprint=params.fingerprint)

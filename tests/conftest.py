@@ -57,3 +57,24 @@ def import_reference():
     import hefir  # noqa: F401
 
     return hefir
+
+
+INSTALLED_REF = os.path.join(ROOT, "baseline", "_ref")
+
+
+def import_installed_reference():
+    """The reference package as installed (unmodified) into baseline/_ref by
+    `pip install --target` (it travels to the GPU box, /root/reference does
+    not), imported through the gmpy2 shim (tests/_shim: mpz = int)."""
+    if not os.path.isdir(os.path.join(INSTALLED_REF, "hefir")):
+        pytest.skip("baseline/_ref (installed reference) not present")
+    shim = os.path.join(ROOT, "tests", "_shim")
+    for p in (shim, INSTALLED_REF):
+        if p not in sys.path:
+            sys.path.insert(0, p)
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_tests")
+    import hefir
+
+    if not os.path.abspath(hefir.__file__).startswith(os.path.abspath(INSTALLED_REF)) and not HAVE_REF:
+        pytest.skip("a different hefir is importable")
+    return hefir

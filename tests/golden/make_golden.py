@@ -20,6 +20,12 @@ Outputs (committed; small):
                                sha256 digests, op counters, decrypted logits.
   set1.json                    N=8192 set 1: digests of keys, one ciphertext,
                                its hmult_raw and hsquare (full-size pin).
+  set1net.json / set1net.npz   The bench workload itself (bench.py, seed 2024):
+                               MNIST HCNN at set 1, dense random 4-bit weights,
+                               one 8192-image slot-batch, evaluated by the
+                               reference's eval_network; every layer's sha256
+                               (all limbs of all ciphertexts), the counters and
+                               the decrypted logits of all 8192 images.
   plain.npz / plain.json       hmult_plain, scalar and NTT paths, 2- and 3-part
                                ciphertexts (N=64 arrays, N=1024 digests).
   hfir.npz / hfir.json         HFIR bytes of a cipher tensor, a 3-part
@@ -358,6 +364,78 @@ def make_set1():
         seconds=dict(hmult_raw=t1 - t0, hsquare=t2 - t1),
     )
     with open(os.path.join(HERE, "set1.json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
+
+
+_SQ = {}
+
+
+def _sq_worker(i):
+    return bfv.hsquare(_SQ["cts"][i], _SQ["rlk"], _SQ["params"])
+
+
+def _pool_eval_square(tensor, rlk, params, counter, workers=1):
+    """engine.eval_square (engine.py:337-364) with the per-ciphertext
+    bfv.hsquare calls fanned over forked processes instead of GIL-bound
+    threads: same calls, same outputs, same counter and delta updates."""
+    import multiprocessing as mp
+
+    _SQ.update(cts=tensor.cts, rlk=rlk, params=params)
+    with mp.get_context("fork").Pool(os.cpu_count()) as pool:
+        out = pool.map(_sq_worker, range(len(tensor.cts)), chunksize=1)
+    counter.hsquare += len(out)
+    return engine.CipherTensor(shape=tensor.shape, cts=out, delta=tensor.delta * tensor.delta,
+                               channel_modulus=tensor.channel_modulus)
+
+
+def make_set1net(seed: int = 2024):
+    """bench.py's MNIST step (build_workload, seed 2024) run by the reference.
+
+    Same derivations as bench.build_workload: weights nn.random_model(spec,
+    default_rng(seed+1)), keys bfv.keygen(default_rng(seed)), images
+    default_rng(seed+100).integers(0, 5, (8192, 28, 28, 1)), packing rng
+    default_rng(seed+200), delta 4."""
+    sys.path.insert(0, REPO)
+    from paper_1811_00778_b200 import nn as mynn
+
+    p = presets.load_preset("1")
+    params = presets.build_context(p)
+    n = params.ring_degree
+    spec = nn_oracle.mnist_hcnn()
+    mine = mynn.random_model(mynn.mnist_hcnn(), np.random.default_rng(seed + 1))
+    model = nn_oracle.QuantizedModel(spec=spec, bit_width=4, weights=mine.weights)
+    t0 = time.time()
+    sk, pk, rlk = bfv.keygen(params, np.random.default_rng(seed))
+    images = list(np.random.default_rng(seed + 100).integers(0, 5, (n, 28, 28, 1)))
+    enc = SlotEncoder(MNIST_T, n)
+    tin = engine.pack_images(images, engine.PackingLayout(n, n), enc, pk, params,
+                             np.random.default_rng(seed + 200), delta=4)
+    print(f"set1net keys+pack: {time.time() - t0:.1f}s", flush=True)
+    digests = {"input": digest_cts(tin.cts)}
+    times = {}
+    last = [time.time()]
+
+    def hook(name, t):
+        digests[name] = digest_cts(t.cts)
+        times[name] = time.time() - last[0]
+        last[0] = time.time()
+        print(f"  {name}: {times[name]:.1f}s {digests[name][:16]}", flush=True)
+
+    counter = engine.OpCounter()
+    engine.eval_square = _pool_eval_square  # eval_network resolves it at call time
+    tout = engine.eval_network(tin, engine.reduce_model(model, MNIST_T), rlk, params, counter,
+                               workers=8, layer_hook=hook)
+    vals = engine.unpack_tensor(tout, sk, enc, params, n)  # (batch, 10) in [0, t)
+    np.savez_compressed(os.path.join(HERE, "set1net.npz"), decrypted=vals.astype(np.int64))
+    meta = dict(
+        n=n, primes=list(p.rns_primes), t=MNIST_T, seed=seed, keys_seed=seed, image_seed=seed + 100,
+        pack_seed=seed + 200, weights_seed=seed + 1, digests=digests, counter=counter_dict(counter),
+        delta=tout.delta, layer_seconds=times, cpu_count=os.cpu_count(),
+        rlk=hashlib.sha256(rlk_arr(rlk).astype("<u8").tobytes()).hexdigest(),
+        logits_sha=hashlib.sha256(vals.astype("<i8").tobytes()).hexdigest(),
+        note="square layers: bfv.hsquare per ciphertext over a fork pool (same calls as engine.eval_square)",
+    )
+    with open(os.path.join(HERE, "set1net.json"), "w") as fh:
         json.dump(meta, fh, indent=1)
 
 

@@ -245,3 +245,25 @@ def test_plain_c_program_links_and_fails_loudly_without_a_gpu(tmp_path):
         fh.write(struct.pack("<Q", 1073643521))
     r = subprocess.run([exe, str(src), str(tmp_path / "out.bin")], capture_output=True, text=True)
     assert r.returncode == 5, (r.returncode, r.stderr)
+
+
+def test_host_narrow_is_exact_and_rejects_out_of_range():
+    """hcnn_host_narrow (host-only, no device): int64 residue arrays -> one
+    u32 buffer, every thread count; values outside [0, 2^32) are refused."""
+    import ctypes
+
+    from paper_1811_00778_b200 import _lib
+    from paper_1811_00778_b200.errors import ParameterMismatchError
+
+    rng = np.random.default_rng(3)
+    arrs = [rng.integers(0, 1 << 30, (3, 257)).astype(np.int64) for _ in range(11)]
+    ptrs = np.array([a.ctypes.data for a in arrs], dtype=np.uintp)
+    for threads in (1, 3, 0, 64):
+        dst = np.zeros((11, 3, 257), dtype=np.uint32)
+        _lib.check(_lib.lib().hcnn_host_narrow(ptrs.ctypes.data, 11, 3 * 257, dst.ctypes.data, threads))
+        assert np.array_equal(dst.astype(np.int64), np.stack(arrs))
+    arrs[7][2, 5] = -1
+    dst = np.zeros((11, 3, 257), dtype=np.uint32)
+    with pytest.raises(ParameterMismatchError):
+        _lib.check(_lib.lib().hcnn_host_narrow(ptrs.ctypes.data, 11, 3 * 257, dst.ctypes.data, 4))
+    _ = ctypes
