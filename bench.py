@@ -410,7 +410,7 @@ def run_ours(args):
                   "d2h_bytes_per_step": int(len(last.cts) * 2 * g0_bytes(units)),
                   "path": "engine.eval_network(host CipherTensor of int64 RingElems) -> host CipherTensor: "
                           "residues narrowed to u32 by a thread pool into a reused pinned buffer, by row bands, "
-                          "each band uploaded and its conv1 + square1 started while the next band is narrowed",
+                          "each band uploaded and the conv1/square1/conv2/square2 wavefront advanced on it while the next band is narrowed",
                   "steps": e2e_steps}
         del host_cts
 
@@ -545,7 +545,7 @@ def run_ours(args):
                          "pinned host logits on rank 0") if groups else
                         "pinned host u32 ciphertexts -> engine.eval_network_stream (upload of step s+1 overlaps "
                         "evaluation of step s; two device input buffers; the first batch streamed by row bands into "
-                        "conv1 + square1) -> pinned host logits", "steps": e2e_steps},
+                        "a conv1/square1/conv2/square2 wavefront) -> pinned host logits", "steps": e2e_steps},
         "e2e_dropin": dropin,
         "gpu_launches": int(launches),
         "kernels": kernels,

@@ -368,9 +368,12 @@ class _HostStager:
                     return self._fill_numpy(stage, cts, lo, hi)
                 ptrs[k] = r.ctypes.data
                 k += 1
+        # one native call, split over host threads inside (measured on the
+        # 16-core GPU host: 14.7 ms for the 784-ciphertext MNIST input alone,
+        # about 20 ms while the uploads run; tools/host_bw_probe.py)
         dst = stage.data_ptr() + lo * 2 * K * N * 4
         _lib.check(_lib.lib().hcnn_host_narrow(ptrs.ctypes.data, 2 * (hi - lo), K * N, _lib.C.c_void_p(dst),
-                                               min(32, os.cpu_count() or 1)), "hcnn_host_narrow")
+                                               min(16, os.cpu_count() or 1)), "hcnn_host_narrow")
 
     def _fill_numpy(self, stage, cts, lo, hi):
         arr = stage.numpy().view(np.uint32)
@@ -588,9 +591,10 @@ def eval_network(tensor, model, rlk, params, counter=None, workers: int = 1, cap
 def _eval_network_host(tensor, model, rlk, params, counter, capacity=None, layer_hook=None, bands: int = 6):
     """eval_network of a host CipherTensor (the reference's own objects): its
     int64 residues are narrowed into a reused pinned buffer by row bands, each
-    band is uploaded on a copy stream as soon as it is filled, and conv1 +
-    square1 of a band start as soon as its input rows are on the device, so
-    the host-side narrowing and the upload overlap the evaluation.  Same
+    band is uploaded on a copy stream as soon as it is filled, and the leading
+    row-local layers (conv1, square1, conv2, square2) run as a wavefront on
+    the rows already on the device, so the host-side narrowing and the upload
+    overlap the evaluation.  Same
     kernels, results and counters as the device path (engine.py:400-423)."""
     if tensor.channel_modulus != params.t:
         raise ParameterMismatchError("tensor channel does not match params")
@@ -608,14 +612,14 @@ def _eval_network_host(tensor, model, rlk, params, counter, capacity=None, layer
     stage = st.get(n, g.K, g.N)
     buf = g.empty(n)
     buf.record_stream(up_stream)
-    x, released = _banded_head(stage, buf, tuple(tensor.shape), tensor.delta, model, rlk, params, counter,
+    x, released, m = _banded_head(stage, buf, tuple(tensor.shape), tensor.delta, model, rlk, params, counter,
                                up_stream, compute, bands, layer_hook,
                                prepare=lambda lo, hi: st.fill(stage, tensor.cts, lo, hi),
                                host_types=_host_types_of(tensor, params))
     st.free = torch.cuda.Event()
     st.free.record(up_stream)
     compute.wait_stream(up_stream)
-    x = _eval_layers(x, model, 2, rlk, params, counter, layer_hook=layer_hook)
+    x = _eval_layers(x, model, m, rlk, params, counter, layer_hook=layer_hook)
     return x.to_host()
 
 
@@ -648,72 +652,154 @@ def _copy_streams(dev):
     return _COPY_STREAMS[key]
 
 
+def _row_local_prefix(model) -> int:
+    """Number of leading layers whose output rows each depend on a contiguous
+    band of input rows (unpadded convolutions, squares, pools): those layers
+    can run as a wavefront behind a row-by-row upload."""
+    m = 0
+    for layer in model.spec.layers:
+        k = kind_of(layer)
+        if k == "square" or k == "pool" or (k == "conv" and not layer.padded):
+            m += 1
+        else:
+            break
+    return m
+
+
 def _bandable(model, shape) -> bool:
-    """First layers are an unpadded convolution followed by a square: the
-    convolution's output rows depend on a contiguous band of input rows."""
+    """The network starts with an unpadded convolution followed by a square:
+    its first layers can start on the first uploaded input rows."""
     layers = model.spec.layers
-    return (len(layers) >= 2 and kind_of(layers[0]) == "conv" and not layers[0].padded
-            and kind_of(layers[1]) == "square" and shape[0] >= 2)
+    return (_row_local_prefix(model) >= 2 and kind_of(layers[0]) == "conv" and kind_of(layers[1]) == "square"
+            and shape[0] >= 2)
+
+
+class _Stage:
+    """One row-local layer of the wavefront: output buffer and rows done."""
+
+    def __init__(self, layer, weights, shape, g):
+        self.layer, self.kind = layer, kind_of(layer)
+        self.ishape = shape
+        h, w, c = shape
+        if self.kind == "conv":
+            weights = np.asarray(weights)
+            f, kh, kw, cg = weights.shape
+            if c != cg * layer.groups:
+                raise ParameterMismatchError(f"{layer.name}: channel mismatch")
+            self.weights, self.wt = weights, g.weights(weights)
+            self.k, self.kw, self.s, self.sw = kh, kw, layer.stride[0], layer.stride[1]
+            self.oshape = ((h - kh) // self.s + 1, (w - kw) // self.sw + 1, f)
+        elif self.kind == "pool":
+            self.k = self.kw = layer.extent
+            self.s, self.sw = layer.stride
+            self.oshape = ((h - self.k) // self.s + 1, (w - self.kw) // self.sw + 1, c)
+        else:
+            self.oshape = shape
+        if self.oshape[0] <= 0 or self.oshape[1] <= 0:
+            raise ParameterMismatchError(f"{layer.name}: empty output")
+        self.out = g.empty(self.oshape[0] * self.oshape[1] * self.oshape[2])
+        self.done = 0
+
+    def ready_rows(self, rows_in: int) -> int:
+        if self.kind == "square":
+            return rows_in
+        if rows_in < self.k:
+            return 0
+        return min(self.oshape[0], (rows_in - self.k) // self.s + 1)
+
+    def run(self, g, src, rows_in: int) -> bool:
+        """Launch this layer on the output rows its ready input rows allow."""
+        L = _lib.lib()
+        upto = self.ready_rows(rows_in)
+        if upto <= self.done:
+            return False
+        lo, (h, w, c), (oh, ow, oc) = self.done, self.ishape, self.oshape
+        if self.kind == "square":
+            _lib.check(L.hcnn_square(g.handle, _ptr(src[lo * w * c:]), _ptr(self.out[lo * w * c:]),
+                                     (upto - lo) * w * c), "square")
+        else:
+            y0, y1 = lo * self.s, (upto - 1) * self.s + self.k  # input rows read
+            if self.kind == "conv":
+                _lib.check(L.hcnn_conv(g.handle, _ptr(src[y0 * w * c:]), _ptr(self.out[lo * ow * oc:]), y1 - y0, w,
+                                       c, self.wt, oc, self.k, self.kw, self.s, self.sw, 0, self.layer.groups),
+                           self.layer.name)
+            else:
+                _lib.check(L.hcnn_pool(g.handle, _ptr(src[y0 * w * c:]), _ptr(self.out[lo * ow * oc:]), y1 - y0, w,
+                                       c, self.k, self.s, self.sw), self.layer.name)
+        self.done = upto
+        return True
 
 
 def _banded_head(hb, buf, shape, delta, model, rlk, params, counter, up_stream, compute, bands, layer_hook,
                  prepare=None, host_types=None):
-    """conv1 + square1 of one batch by output-row bands, each band starting as
-    soon as the input rows it reads are uploaded (the upload of the next band
-    overlaps the square of this one).  Same kernels, same results and counters
-    as eval_conv + eval_square on the whole tensor (engine.py:237-364).
-    `prepare(lo, hi)`, when given, fills host ciphertexts [lo, hi) of `hb`
-    before they are uploaded (the drop-in path narrows the caller's residues
-    there).  Returns (square output tensor, event after the last read of `buf`)."""
+    """The network's leading row-local layers (unpadded convolutions, squares,
+    pools: MNIST conv1, square1, conv2, square2) evaluated as a wavefront
+    behind a row-band upload of the input: input rows go up in `bands`
+    bands (by conv1 output rows), and after each band every layer is launched
+    on the output rows its now-available input rows determine, so conv2 +
+    square2 of the top rows run while later input rows are still uploading.
+    Same kernels, same results and counters as the layer-by-layer path
+    (engine.py:237-397).  `prepare(lo, hi)`, when given, fills host
+    ciphertexts [lo, hi) of `hb` before they are uploaded (the drop-in path
+    narrows the caller's residues there).  Returns (output tensor of the
+    prefix, event after the last read of `buf`, number of layers done)."""
     if hb.shape[0] != shape[0] * shape[1] * shape[2]:
         raise ParameterMismatchError("ciphertext count != h*w*c")
-    conv, weights = model.spec.layers[0], np.asarray(model.weights[0])
-    h, w, c = shape
-    f, kh, kw, cg = weights.shape
-    if c != cg * conv.groups:
-        raise ParameterMismatchError(f"{conv.name}: channel mismatch")
-    sh, sw = conv.stride
-    oh, ow = (h - kh) // sh + 1, (w - kw) // sw + 1
     g = context_for(params, buf.device)
-    if rlk is None:
-        raise MissingKeyError("relinearization key required for hsquare")
-    g.set_relin_key(rlk)
-    wt = g.weights(weights)
-    cout, sq = g.empty(oh * ow * f), g.empty(oh * ow * f)
-    L = _lib.lib()
+    m = _row_local_prefix(model)
+    layers, weights = model.spec.layers[:m], model.weights[:m]
+    if any(kind_of(la) == "square" for la in layers):
+        if rlk is None:
+            raise MissingKeyError("relinearization key required for hsquare")
+        g.set_relin_key(rlk)
+    stages, cur = [], tuple(shape)
+    for la, wt in zip(layers, weights):
+        stages.append(_Stage(la, wt, cur, g))
+        cur = stages[-1].oshape
+    h, w, c = shape
     row = w * c  # ciphertexts per input row
-    cuts = [round(b * oh / bands) for b in range(bands + 1)]
+    first = stages[0]
+    oh0 = first.oshape[0]
+    cuts = [round(b * oh0 / bands) for b in range(bands + 1)]
     uploaded = 0
-    for y0, y1 in zip(cuts, cuts[1:]):
-        if y1 == y0:
+    g.bind_stream()
+    for y1 in cuts[1:]:
+        hi = h if y1 >= oh0 else min(h, (y1 - 1) * first.s + first.k) if first.kind != "square" else y1
+        if hi <= uploaded:
             continue
-        hi = (y1 - 1) * sh + kh
-        if hi > uploaded:
-            if prepare is not None:
-                prepare(uploaded * row, hi * row)
-            with torch.cuda.stream(up_stream):
-                buf[uploaded * row:hi * row].copy_(hb[uploaded * row:hi * row], non_blocking=True)
-                ready = torch.cuda.Event()
-                ready.record(up_stream)
-            compute.wait_event(ready)
-            uploaded = hi
+        if prepare is not None:
+            prepare(uploaded * row, hi * row)
+        with torch.cuda.stream(up_stream):
+            buf[uploaded * row:hi * row].copy_(hb[uploaded * row:hi * row], non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(up_stream)
+        compute.wait_event(ready)
+        uploaded = hi
         g.bind_stream()
-        lo = y0 * sh
-        _lib.check(L.hcnn_conv(g.handle, _ptr(buf[lo * row:]), _ptr(cout[y0 * ow * f:]), hi - lo, w, c, wt, f,
-                               kh, kw, sh, sw, 0, conv.groups), conv.name)
-        n = (y1 - y0) * ow * f
-        _lib.check(L.hcnn_square(g.handle, _ptr(cout[y0 * ow * f:]), _ptr(sq[y0 * ow * f:]), n), "square")
+        src, rows = buf, uploaded
+        for st in stages:
+            st.run(g, src, rows)
+            src, rows = st.out, st.done
     released = torch.cuda.Event()
     released.record(compute)
-    _count(counter, *_conv_counts(h, w, conv, weights))
-    counter.hsquare += oh * ow * f
-    d1 = delta * conv.weight_scale
-    x1 = GpuCipherTensor((oh, ow, f), cout, d1, params.t, params, host_types)
-    x2 = GpuCipherTensor((oh, ow, f), sq, d1 * d1, params.t, params, host_types)
-    if layer_hook is not None:
-        layer_hook(conv.name, x1)
-        layer_hook(model.spec.layers[1].name, x2)
-    return x2, released
+    # counters, scales and hooks layer by layer, as the reference's loop has them
+    x = None
+    d = delta
+    for st in stages:
+        if st.kind == "conv":
+            _count(counter, *_conv_counts(st.ishape[0], st.ishape[1], st.layer, st.weights))
+            d = d * st.layer.weight_scale
+        elif st.kind == "square":
+            counter.hsquare += st.oshape[0] * st.oshape[1] * st.oshape[2]
+            d = d * d
+        else:
+            e = st.layer.extent
+            counter.hadd += st.oshape[0] * st.oshape[1] * st.oshape[2] * (e * e - 1)
+            d = d * e * e
+        x = GpuCipherTensor(st.oshape, st.out, d, params.t, params, host_types)
+        if layer_hook is not None:
+            layer_hook(st.layer.name, x)
+    return x, released, m
 
 
 def eval_network_stream(batches, model, rlk, params, shape, delta, counter=None, device=None,
@@ -730,8 +816,10 @@ def eval_network_stream(batches, model, rlk, params, shape, delta, counter=None,
     (y, x, c) row-major like CipherTensor.cts), all of `shape`.
     The first batch has no evaluation to hide its upload behind: when the
     network starts with an unpadded convolution and a square, its upload is
-    split into `bands` output-row bands and each band's conv1 + square1 starts
-    as soon as its input rows are on the device (bands=1 turns this off).
+    split into `bands` output-row bands and the leading row-local layers
+    (conv1, square1, conv2, square2 for MNIST) run as a wavefront behind it,
+    each launched on the rows its uploaded input rows allow (bands=1 turns
+    this off).
     Returns the list of host int32 logit tensors [n_out][2][K][N] (written
     into `outputs[i]` when given, else freshly pinned); they are complete when
     the call returns.
@@ -757,10 +845,10 @@ def eval_network_stream(batches, model, rlk, params, shape, delta, counter=None,
             bufs[slot].record_stream(up_stream)
         if i == 0 and bands > 1 and _bandable(model, shape):
             # nothing to overlap the first upload with: stream it by row bands
-            # into conv1 + square1 instead
-            x, free[slot] = _banded_head(hb, bufs[slot], shape, delta, model, rlk, params, counter, up_stream,
-                                         compute, bands, layer_hook)
-            out = _eval_layers(x, model, 2, rlk, params, counter, layer_hook=layer_hook)
+            # into the leading row-local layers instead
+            x, free[slot], m = _banded_head(hb, bufs[slot], shape, delta, model, rlk, params, counter, up_stream,
+                                            compute, bands, layer_hook)
+            out = _eval_layers(x, model, m, rlk, params, counter, layer_hook=layer_hook)
         else:
             with torch.cuda.stream(up_stream):
                 if free[slot] is not None:

@@ -31,7 +31,8 @@ Outputs (committed; small):
   hfir.npz / hfir.json         HFIR bytes of a cipher tensor, a 3-part
                                ciphertext and a relinearisation key.
 
-Usage: python tests/golden/make_golden.py [small n1024 cifar64 mnist1024 set1 plain hfir]
+Usage: python tests/golden/make_golden.py [small n1024 cifar64 mnist1024 set1 plain hfir set1net]
+(set1net is not in the default list: ~25 minutes on 8 cores.)
 """
 
 from __future__ import annotations
