@@ -187,6 +187,18 @@ int hcnn_ntt(hcnn_ctx* ctx, uint32_t* rows, size_t n_rows, uint32_t limbs, uint3
  * host CipherTensor before it crosses PCIe (engine.py:42-58 objects in). */
 int hcnn_host_narrow(const int64_t* const* src, size_t count, size_t len, uint32_t* dst, int threads);
 
+/* Plaintext-CRT recombination on the device (engine.reconstruct_logits,
+ * engine.py:494-506 / CrtSystem.reconstruct_centered, codec.py:79-89):
+ * res: DEVICE u64 [n_moduli][count], residue of value m mod moduli[i] at
+ * [i][m], each in [0, moduli[i]); moduli: HOST, pairwise coprime, in
+ * [2, 2^62), at most 16.  out: DEVICE u32 [count][words], the centred value
+ * (X - T when X > floor(T/2), T = prod moduli) as little-endian two's
+ * complement words; words must exceed the word length of T.  Runs on
+ * `stream` of `device` and synchronises it (HCNN_ERR_PARAM for a residue
+ * outside its range, which the reference raises as HefirError). */
+int hcnn_crt_combine(const uint64_t* res, const uint64_t* moduli, int n_moduli, size_t count, uint32_t* out,
+                     int words, int device, void* stream);
+
 /* Per-kernel CUDA-event timing on the context's stream.  hcnn_profile(ctx, 1)
  * resets and starts recording; hcnn_profile_dump writes "name count total_ms"
  * lines (returns the text length, or -status). */

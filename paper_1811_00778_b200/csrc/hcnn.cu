@@ -10,6 +10,7 @@
 
 #include "../../include/hcnn_b200.h"
 #include "conv_kernels.cuh"
+#include "crt.cuh"
 #include "kernels.cuh"
 #include "ntt_kernels.cuh"
 #include "ntt64.cuh"
@@ -886,6 +887,67 @@ int hcnn_host_narrow(const int64_t* const* src, size_t count, size_t len, uint32
     for (auto& t : pool) t.join();
     for (uint64_t b : bad)
       if (b) fail(HCNN_ERR_PARAM, "residue outside [0, 2^32): not a canonical RNS residue");
+  });
+}
+
+namespace {
+uint64_t inv_mod_u64(uint64_t a, uint64_t m) {  // a^-1 mod m (gcd 1), extended Euclid in signed 128-bit
+  __int128 t0 = 0, t1 = 1, r0 = m, r1 = a % m;
+  while (r1) {
+    const __int128 q = r0 / r1, r2 = r0 - q * r1, t2 = t0 - q * t1;
+    r0 = r1;
+    r1 = r2;
+    t0 = t1;
+    t1 = t2;
+  }
+  if (r0 != 1) fail(HCNN_ERR_PARAM, "CRT moduli are not pairwise coprime");
+  if (t0 < 0) t0 += m;
+  return (uint64_t)t0;
+}
+}  // namespace
+
+int hcnn_crt_combine(const uint64_t* res, const uint64_t* moduli, int n_moduli, size_t count, uint32_t* out,
+                     int words, int device, void* stream) {
+  return guarded([&] {
+    if (!moduli || n_moduli < 1 || n_moduli > CRT_MAXC) fail(HCNN_ERR_PARAM, "1..16 CRT moduli supported");
+    if (words < 1 || words > CRT_MAXW) fail(HCNN_ERR_PARAM, "output words out of range");
+    CrtTabs tb{};
+    tb.C = n_moduli;
+    tb.W = words;
+    std::vector<uint32_t> T(CRT_MAXW + 4, 0);
+    T[0] = 1;
+    for (int i = 0; i < n_moduli; ++i) {
+      if (moduli[i] < 2 || moduli[i] >= (1ull << 62)) fail(HCNN_ERR_PARAM, "CRT moduli must lie in [2, 2^62)");
+      tb.t[i] = moduli[i];
+      unsigned __int128 carry = 0;
+      for (auto& w : T) {
+        const unsigned __int128 acc = (unsigned __int128)w * moduli[i] + carry;
+        w = (uint32_t)acc;
+        carry = acc >> 32;
+      }
+      for (int j = 0; j < i; ++j) tb.inv[j][i] = inv_mod_u64(moduli[j], moduli[i]);
+    }
+    int used = (int)T.size();
+    while (used > 0 && T[used - 1] == 0) --used;
+    if (used + 1 > words) fail(HCNN_ERR_PARAM, "output words too few for the product of the moduli plus a sign");
+    for (int k = 0; k < words; ++k) {
+      tb.T[k] = T[k];
+      tb.half[k] = (T[k] >> 1) | (k + 1 < (int)T.size() ? T[k + 1] << 31 : 0u);
+    }
+    if (!count) return;
+    if (!res || !out) fail(HCNN_ERR_PARAM, "null argument");
+    CK(cudaSetDevice(device));
+    cudaStream_t st = (cudaStream_t)stream;
+    int* bad = nullptr;
+    pool_malloc(&bad, sizeof(int), st, device);
+    CK(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    k_crt_combine<<<(unsigned)((count + 127) / 128), 128, 0, st>>>(res, count, tb, out, bad);
+    CK(cudaGetLastError());
+    int h_bad = 0;
+    CK(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(bad, st));
+    CK(cudaStreamSynchronize(st));
+    if (h_bad) fail(HCNN_ERR_PARAM, "CRT residue outside [0, t_i)");
   });
 }
 

@@ -210,3 +210,241 @@ def output_delta(spec, delta: int) -> int:
         elif k == "pool":
             delta *= layer.extent * layer.extent
     return delta
+
+
+# ---------------------------------------------------------------- CRT channels + output-channel split
+#
+# BASELINE config 5: CIFAR-10's 10 plaintext-CRT channels on 8 GPUs.  Dealing
+# whole channels round-robin runs 2 waves (the second keeps 2 GPUs busy).
+# channel_plan gives every rank floor(C / W) whole channels and splits each
+# of the C mod W remaining channels over a subgroup of W // (C mod W) ranks BY
+# OUTPUT CHANNEL: every rank of the subgroup computes its slice of each
+# convolution's filters (then square and pool on that slice); before the next
+# convolution the slices are all-gathered (NCCL over NVLink) into the full
+# feature map; the dense layer on a sliced map is a partial sum over the
+# rank's columns, and the partials are gathered to the subgroup root and added
+# there (exact mod p; the root counts the adds like the reference's weighted
+# sum).  For 10 channels on 8 GPUs every rank does 1 + 2/8 channel of work.
+
+
+def channel_plan(n_channels: int, world: int):
+    """-> (whole, splits): whole[r] = channels rank r evaluates alone;
+    splits = [(channel, [ranks])] evaluated by output-channel slices."""
+    base, rem = divmod(n_channels, world)
+    whole = [[c for c in range(base * world) if c % world == r] for r in range(world)]
+    splits = []
+    if rem:
+        size = world // rem
+        for j in range(rem):
+            ranks = list(range(j * size, (j + 1) * size))
+            if len(ranks) == 1:
+                whole[ranks[0]].append(base * world + j)
+            else:
+                splits.append((base * world + j, ranks))
+    return whole, splits
+
+
+def slices(n: int, parts: int) -> list:
+    """n items in `parts` contiguous, near-equal ranges."""
+    return [range(n * i // parts, n * (i + 1) // parts) for i in range(parts)]
+
+
+class GpuSplitBackend:
+    """Layer operations of the split program on the GPU engine."""
+
+    def __init__(self, params, rlk):
+        from . import engine as E
+
+        self.E, self.params, self.rlk = E, params, rlk
+
+    def conv(self, x, layer, w, counter):
+        return self.E.eval_conv(x, layer, w, self.params, counter)
+
+    def square(self, x, counter):
+        return self.E.eval_square(x, self.rlk, self.params, counter)
+
+    def pool(self, x, layer, counter):
+        return self.E.eval_pool(x, layer, self.params, counter)
+
+    def fc(self, x, layer, w, counter):
+        return self.E.eval_fc(x, layer, w, self.params, counter)
+
+    def wrap(self, shape, data, delta):
+        return self.E.GpuCipherTensor(shape, data, delta, self.params.t, self.params)
+
+    def add(self, a, b):
+        from . import ops
+
+        return ops.hadd_device(self.E.context_for(self.params, a.device), a, b)
+
+
+def _split_program(x, model, backend, S: int, me: int, counter):
+    """One CRT channel's network, rank `me` of an S-rank subgroup (a
+    generator: it yields ("all_gather", tensor) / ("gather", tensor) at the
+    collectives and receives the list of every rank's tensor, or None on
+    non-root ranks for "gather").  Returns the logits on rank 0 of the
+    subgroup, None elsewhere."""
+    from dataclasses import replace
+
+    from .nn import kind_of
+
+    layers = list(zip(model.spec.layers, model.weights))
+    if not layers or kind_of(layers[0][0]) != "conv":
+        raise ValueError("the output-channel split starts at a convolution")
+    cut = None  # channel slices of every rank while x holds only this rank's slice
+
+    def join(x):
+        h, w, c = x.shape
+        cmax = max(len(s) for s in cut)
+        d = x.data.reshape((h * w, c) + tuple(x.data.shape[1:]))
+        if c < cmax:
+            d = torch.cat([d, d.new_zeros((h * w, cmax - c) + tuple(d.shape[2:]))], dim=1)
+        chunks = yield ("all_gather", d.contiguous())
+        full = torch.cat([ch[:, :len(s)] for ch, s in zip(chunks, cut)], dim=1)
+        C = sum(len(s) for s in cut)
+        return backend.wrap((h, w, C), full.reshape((h * w * C,) + tuple(d.shape[2:])).contiguous(), x.delta)
+
+    for layer, wts in layers:
+        k = kind_of(layer)
+        if k == "conv":
+            if layer.groups != 1:
+                raise ValueError("the output-channel split needs dense convolutions")
+            if cut is not None:
+                x = yield from join(x)
+            cut = slices(layer.filters, S)
+            mine = cut[me]
+            x = backend.conv(x, replace(layer, filters=len(mine)), np.asarray(wts)[mine.start:mine.stop], counter)
+        elif k == "square":
+            x = backend.square(x, counter)
+        elif k == "pool":
+            x = backend.pool(x, layer, counter)
+        elif k == "fc" and cut is not None:
+            h, w, _ = x.shape
+            C = sum(len(s) for s in cut)
+            W = np.asarray(wts)
+            cols = [np.array([(y * w + xx) * C + ch for y in range(h) for xx in range(w) for ch in s], dtype=np.int64)
+                    for s in cut]
+            part = backend.fc(x, layer, W[:, cols[me]], counter)
+            parts = yield ("gather", part.data)
+            if me != 0:
+                return None
+            acc = parts[0]
+            for p in parts[1:]:
+                acc = backend.add(acc, p)
+            # the adds of the partials, counted as the reference counts a weighted
+            # sum's adds (engine.py:206-223): one per extra non-empty partial
+            nz = np.stack([(W[:, c] != 0).any(axis=1) for c in cols]).sum(axis=0)
+            counter.hadd += int(np.maximum(nz - 1, 0).sum())
+            x = backend.wrap((1, 1, W.shape[0]), acc, part.delta)
+            cut = None
+        elif k == "fc":
+            if me != 0:
+                return None
+            x = backend.fc(x, layer, wts, counter)
+    if cut is not None:
+        x = yield from join(x)
+        if me != 0:
+            return None
+    return x
+
+
+def run_split_emulated(x, model, backend, S: int, counters=None):
+    """Run all S ranks of a split program in lockstep in ONE process (one
+    GPU): the collectives are resolved in memory.  Returns rank 0's logits."""
+    counters = counters if counters is not None else [None] * S
+    from .engine import OpCounter
+
+    counters = [c if c is not None else OpCounter() for c in counters]
+    gens = [_split_program(x, model, backend, S, r, counters[r]) for r in range(S)]
+    msgs = [None] * S
+    results = [None] * S
+    alive = list(range(S))
+    while alive:
+        ops_ = {}
+        for r in alive:
+            try:
+                ops_[r] = gens[r].send(msgs[r])
+            except StopIteration as stop:
+                results[r] = stop.value
+        alive = [r for r in alive if r in ops_]
+        if not alive:
+            break
+        kinds = {ops_[r][0] for r in alive}
+        if len(kinds) != 1 or len(alive) != S:
+            raise RuntimeError("split ranks diverged")
+        data = [ops_[r][1] for r in range(S)]
+        kind = kinds.pop()
+        for r in range(S):
+            msgs[r] = list(data) if kind == "all_gather" or r == 0 else None
+    return results[0]
+
+
+def run_split(x, model, backend, ranks: list, rank: int, group=None, counter=None):
+    """Run this rank's part of a split program with torch.distributed
+    collectives over `group` (the subgroup of `ranks`).  Returns the logits
+    on ranks[0], None elsewhere."""
+    S, me = len(ranks), ranks.index(rank)
+    gen = _split_program(x, model, backend, S, me, counter)
+    msg = None
+    while True:
+        try:
+            kind, data = gen.send(msg)
+        except StopIteration as stop:
+            return stop.value
+        if kind == "all_gather":
+            lst = [torch.empty_like(data) for _ in range(S)]
+            dist.all_gather(lst, data, group=group)
+            msg = lst
+        else:
+            lst = [torch.empty_like(data) for _ in range(S)] if me == 0 else None
+            dist.gather(data, lst, dst=ranks[0], group=group)
+            msg = lst
+
+
+def split_groups(splits):
+    """torch.distributed subgroups of a channel_plan's splits (every rank must
+    call this, in the same order)."""
+    return [dist.new_group(ranks) for _, ranks in splits]
+
+
+# ---------------------------------------------------------------- decrypt, gather, recombine (SURVEY 8(f) 1)
+
+
+def decrypt_residues(logits, sk, params, batch_size: int) -> torch.Tensor:
+    """Decrypt + slot-decode a logits GpuCipherTensor on its own GPU:
+    DEVICE int64 (outputs, batch) residues mod t (engine.py:178-192)."""
+    from . import engine as E
+
+    polys = E.decrypt_device(logits, sk, params)
+    slots = E.codec_for(params.t, params.ring_degree, logits.data.device).decode(polys)
+    return slots[:, :batch_size].contiguous()
+
+
+def gather_recombine(local: dict, owners: dict, moduli, n_batches: int, rank: int, world: int, shape, device,
+                     dst: int = 0, group=None):
+    """The pipeline's one exchange: every rank holds the decrypted residues
+    (DEVICE int64 (outputs, batch)) of the (batch, channel) units it owns
+    (`local`: {Unit: tensor}); `owners` maps every Unit to its rank (identical
+    on all ranks).  The residue matrices are gathered to dst (NCCL; 8 x 10 x
+    8192 x 8 B per CIFAR batch instead of the 66 MB of logit ciphertexts) and
+    CRT-recombined there on the GPU.  `shape` = (outputs, batch) of one
+    matrix and `device` this rank's device (ranks that own no unit still take
+    part in the gather).  Returns the signed logits [(batch, outputs) object
+    array per slot-batch] on dst, None elsewhere."""
+    from .engine import ChannelResult, reconstruct_logits
+
+    units = sorted(owners, key=lambda u: (u.batch, u.channel))
+    plan = [[u for u in units if owners[u] == r] for r in range(world)]
+    mine = [local[u] for u in plan[rank]]
+    template = torch.empty(tuple(shape), dtype=torch.int64, device=device)
+    res = gather_units(mine, plan, rank, world, dst, group, template=template)
+    if rank != dst:
+        return None
+    moduli = tuple(int(m) for m in moduli)
+    out = []
+    for b in range(n_batches):
+        cr = ChannelResult(moduli=moduli, batch_size=int(res[Unit(b, 0)].shape[1]))
+        for c, t in enumerate(moduli):
+            cr.add(t, res[Unit(b, c)])
+        out.append(reconstruct_logits(cr, moduli))
+    return out

@@ -1144,27 +1144,95 @@ def run_channels(images, model, crt_system, params_for_channel, keys_for_channel
     return result
 
 
+def _words_to_ints(words: np.ndarray) -> np.ndarray:
+    """[M][W] u32 little-endian two's complement -> object array of Python ints
+    (int64 fast path when every value fits)."""
+    M, W = words.shape
+    if M == 0:
+        return np.zeros(0, dtype=object)
+    lo = words[:, 0].astype(np.uint64) | (words[:, 1].astype(np.uint64) << np.uint64(32)) if W > 1 else \
+        words[:, 0].astype(np.uint64)
+    v64 = lo.view(np.int64)
+    ext = np.where(v64 < 0, np.uint32(0xFFFFFFFF), np.uint32(0))
+    if W <= 2 or (words[:, 2:] == ext[:, None]).all():
+        return v64.astype(object)
+    raw = np.ascontiguousarray(words).tobytes()
+    step = 4 * W
+    return np.array([int.from_bytes(raw[i:i + step], "little", signed=True) for i in range(0, len(raw), step)],
+                    dtype=object)
+
+
+def crt_combine_device(res: torch.Tensor, moduli) -> np.ndarray:
+    """Centred CRT recombination on the GPU: res DEVICE int64 [C][M] (residue of
+    value m mod moduli[i] at [i][m]) -> object array [M] of signed Python ints
+    equal to CrtSystem.reconstruct_centered (codec.py:79-89) of each column."""
+    moduli = [int(t) for t in moduli]
+    if res.dim() != 2 or res.shape[0] != len(moduli):
+        raise ParameterMismatchError("residue rows != modulus count")
+    total = 1
+    for t in moduli:
+        total *= t
+    words = total.bit_length() // 32 + 2
+    res = res.to(dtype=torch.int64).contiguous()
+    dev = res.device
+    out = torch.empty((res.shape[1], words), dtype=torch.int32, device=dev)
+    arr = (_lib.C.c_uint64 * len(moduli))(*moduli)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    try:
+        _lib.check(_lib.lib().hcnn_crt_combine(_ptr(res), arr, len(moduli), res.shape[1], _ptr(out), words,
+                                               dev.index or 0, _lib.C.c_void_p(stream)), "hcnn_crt_combine")
+    except ParameterMismatchError as e:  # out-of-range residue / non-coprime moduli, as the reference raises
+        raise HefirError(str(e)) from None
+    return _words_to_ints(out.cpu().numpy().view(np.uint32))
+
+
 def reconstruct_logits(result, crt_moduli) -> np.ndarray:
-    """Signed logits from per-channel residues (engine.py:494-506)."""
+    """Signed logits (batch, outputs) from per-channel residues
+    (engine.py:494-506), recombined on the GPU (crt_combine_device).  The
+    per-channel matrices may be host arrays or device tensors (outputs, batch)."""
     moduli = tuple(getattr(crt_moduli, "moduli", crt_moduli))
     for t in moduli:
         if t not in result.residues:
             raise IncompleteResultError(f"missing CRT channel t={t}")
+    if not torch.cuda.is_available():
+        return reconstruct_logits_host(result, moduli)
+    mats = [result.residues[t] for t in moduli]
+    dev = next((m.device for m in mats if isinstance(m, torch.Tensor) and m.is_cuda),
+               torch.device("cuda", torch.cuda.current_device()))
+    stack = torch.stack([m.to(dev, dtype=torch.int64) if isinstance(m, torch.Tensor)
+                         else torch.from_numpy(np.ascontiguousarray(np.asarray(m, dtype=np.int64))).to(dev)
+                         for m in mats])
+    C, outputs, batch = stack.shape
+    vals = crt_combine_device(stack.reshape(C, -1), moduli)
+    return vals.reshape(outputs, batch).T.copy()
+
+
+def reconstruct_logits_host(result, crt_moduli) -> np.ndarray:
+    """The client-side host form of reconstruct_logits (engine.py:494-506) for
+    a process without a GPU (the gloo tests of the gather): Garner mixed-radix
+    digits vectorised over all values, Python ints only for the final sum."""
+    moduli = tuple(int(t) for t in getattr(crt_moduli, "moduli", crt_moduli))
+    for t in moduli:
+        if t not in result.residues:
+            raise IncompleteResultError(f"missing CRT channel t={t}")
+    mats = []
+    for t in moduli:
+        m = np.asarray(result.residues[t], dtype=np.int64)
+        if (m < 0).any() or (m >= t).any():
+            raise HefirError(f"residue outside [0, {t})")
+        mats.append(m.astype(object))
+    outputs, batch = mats[0].shape
     total = 1
     for t in moduli:
         total *= t
-    any_mat = next(iter(result.residues.values()))
-    outputs, batch = any_mat.shape
-    logit = np.zeros((batch, outputs), dtype=object)
-    for o in range(outputs):
-        for b in range(batch):
-            acc = 0
-            for t in moduli:
-                big = total // t
-                acc += int(result.residues[t][o, b]) * big * pow(big % t, -1, t)
-            v = acc % total
-            logit[b, o] = v if v <= total // 2 else v - total
-    return logit
+    acc = np.zeros((outputs, batch), dtype=object)
+    radix = 1
+    for m, t in zip(mats, moduli):  # next mixed-radix digit: (r_i - X) * (prod t_<i)^-1 mod t_i
+        acc = acc + ((m - acc) % t) * pow(radix % t, -1, t) % t * radix
+        radix *= t
+    half = total // 2
+    out = np.where(acc > half, acc - total, acc)
+    return out.T.copy()
 
 
 def classify_logits(logits) -> list:

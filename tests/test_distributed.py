@@ -174,3 +174,207 @@ def test_group_partials_gather_world2():
     for pr in procs:
         pr.join(timeout=60)
     assert ok
+
+
+# ---------------------------------------------------------------- CRT channels + output-channel split
+
+
+def test_channel_plan_balances_cifar_on_1_2_4_8_ranks():
+    for world, per_rank in ((1, 10), (2, 5), (4, 2.5), (8, 1.25), (3, 10 / 3)):
+        whole, splits = D.channel_plan(10, world)
+        load = [len(w) for w in whole]
+        covered = [c for w in whole for c in w] + [c for c, _ in splits]
+        assert sorted(covered) == list(range(10))
+        for c, ranks in splits:
+            for r in ranks:
+                load[r] += 1 / len(ranks)
+        assert max(load) == pytest.approx(per_rank), (world, load)
+    whole, splits = D.channel_plan(10, 8)
+    assert whole == [[r] for r in range(8)] and splits == [(8, [0, 1, 2, 3]), (9, [4, 5, 6, 7])]
+
+
+class _OTensor:
+    """CPU stand-in for a GpuCipherTensor: int64 [n][2][K][N] residues."""
+
+    def __init__(self, shape, data, delta):
+        self.shape, self.data, self.delta = tuple(shape), data, delta
+
+    def __len__(self):
+        return self.data.shape[0]
+
+
+class _OracleBackend:
+    """The split program's layer operations on the pinned oracle (CPU)."""
+
+    def __init__(self, op, rlk):
+        self.op, self.rlk = op, rlk
+
+    def _ot(self, x):
+        import hcnn_oracle as O
+
+        d = x.data.numpy()
+        return O.Tensor(x.shape, [(c[0], c[1]) for c in d], x.delta)
+
+    def _back(self, ot):
+        return _OTensor(ot.shape, torch.from_numpy(np.stack([np.stack(c) for c in ot.cts]).astype(np.int64)),
+                        ot.delta)
+
+    def conv(self, x, layer, w, counter):
+        import hcnn_oracle as O
+
+        return self._back(O.conv(self.op, self._ot(x), layer.kernel, layer.stride, layer.padded, layer.groups,
+                                 layer.weight_scale, w, counter))
+
+    def square(self, x, counter):
+        import hcnn_oracle as O
+
+        return self._back(O.square(self.op, self._ot(x), self.rlk, counter))
+
+    def pool(self, x, layer, counter):
+        import hcnn_oracle as O
+
+        return self._back(O.pool(self.op, self._ot(x), layer.extent, layer.stride, counter))
+
+    def fc(self, x, layer, w, counter):
+        import hcnn_oracle as O
+
+        return self._back(O.fc(self.op, self._ot(x), w, layer.weight_scale, counter))
+
+    def wrap(self, shape, data, delta):
+        return _OTensor(shape, data, delta)
+
+    def add(self, a, b):
+        mods = torch.from_numpy(self.op.ctx.mods.reshape(1, 1, -1, 1))
+        return (a + b) % mods
+
+
+def _split_world():
+    """Tiny CIFAR-shaped network (padded dense convs, squares, pools, two
+    dense layers) at N=64 with 4 pool primes, t = 257, and its inputs."""
+    import hcnn_oracle as O
+
+    from paper_1811_00778_b200 import nn
+
+    n, primes, t = 64, [1073643521, 1073479681, 1073184769, 1073053697], 257
+    op = O.Params(O.Context(n, primes), t)
+    rng = np.random.default_rng(90)
+    _, _, rlk = O.keygen(op, rng)
+    spec = nn.NetworkSpec("mini_cifar", (6, 6, 2), 255, (
+        nn.conv_layer("conv1", 5, (3, 3), (1, 1), True, 10),
+        nn.square_layer_spec("square1"),
+        nn.pool_layer("pool1", 2, 2),
+        nn.conv_layer("conv2", 7, (3, 3), (1, 1), True, 10),
+        nn.square_layer_spec("square2"),
+        nn.pool_layer("pool2", 2, 1),
+        nn.fc_layer("fc1", 4, 5),
+        nn.fc_layer("fc2", 3, 5),
+    ))
+    model = nn.random_model(spec, np.random.default_rng(91))
+    mods = op.ctx.mods.reshape(1, 1, -1, 1)
+    x = np.random.default_rng(92).integers(0, 1 << 30, (72, 2, 4, n)) % mods
+    return op, rlk, model, x
+
+
+def _full_network(op, rlk, model, x):
+    import hcnn_oracle as O
+    from helpers import layer_dicts
+
+    c = O.Counter()
+    out = O.network(op, O.Tensor((6, 6, 2), [(d[0], d[1]) for d in x], 255), layer_dicts(model.spec, model.weights),
+                    rlk, c)
+    return np.stack([np.stack(ct) for ct in out.cts]), c
+
+
+def test_split_program_emulated_equals_the_full_network():
+    """All S ranks of one channel's output-channel split run in lockstep in
+    one process (the single-GPU emulation driver), on the oracle: the
+    reassembled logits equal the unsplit network bit for bit, and the ranks'
+    counters add up to the unsplit counter."""
+    import hcnn_oracle as O
+
+    op, rlk, model, x = _split_world()
+    exp, ec = _full_network(op, rlk, model, x)
+    be = _OracleBackend(op, rlk)
+    for S in (2, 3):
+        counters = [O.Counter() for _ in range(S)]
+        out = D.run_split_emulated(_OTensor((6, 6, 2), torch.from_numpy(x), 255), model, be, S, counters)
+        assert np.array_equal(out.data.numpy(), exp), S
+        tot = {k: sum(getattr(c, k) for c in counters) for k in ec.__dict__}
+        assert tot == ec.__dict__, S
+
+
+def _split_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import hcnn_oracle as O
+
+        op, rlk, model, x = _split_world()
+        c = O.Counter()
+        out = D.run_split(_OTensor((6, 6, 2), torch.from_numpy(x), 255), model, _OracleBackend(op, rlk),
+                          list(range(world)), rank, None, c)
+        cs = [None] * world
+        dist.all_gather_object(cs, c.__dict__)
+        if rank == 0:
+            exp, ec = _full_network(op, rlk, model, x)
+            tot = {k: sum(d[k] for d in cs) for k in ec.__dict__}
+            q.put(bool(np.array_equal(out.data.numpy(), exp)) and tot == ec.__dict__)
+        else:
+            assert out is None
+    finally:
+        dist.destroy_process_group()
+
+
+def test_split_program_over_two_gloo_ranks():
+    """The same split with real torch.distributed collectives (gloo, world
+    size 2): all-gather of the channel slices before conv2, gather of the fc
+    partial sums to rank 0."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_split_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    assert q.get(timeout=10) is True
+
+
+def _recombine_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        moduli = (2424833, 2654209, 2752513, 2819073)
+        signed = np.array([[123456789012345, -9876543210987], [-1, 0], [5, -5]], dtype=object)  # (outputs, batch)
+        owners = {D.Unit(0, c): c % world for c in range(len(moduli))}
+        local = {u: torch.from_numpy(np.vectorize(lambda v, t=moduli[u.channel]: int(v) % t)(signed).astype(np.int64))
+                 for u, r in owners.items() if r == rank}
+        out = D.gather_recombine(local, owners, moduli, 1, rank, world, signed.shape, torch.device("cpu"))
+        if rank == 0:
+            q.put(bool((out[0] == signed.T).all()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gather_recombine_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_recombine_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert q.get(timeout=10) is True
+
+
+def test_gather_units_rejects_an_unservable_plan_on_every_rank():
+    plan = [[D.Unit(0, 0)], []]
+    with pytest.raises(ValueError):
+        D.gather_units([], plan, 1, 2)  # rank 1: no units and no template -> raises before any collective
+    with pytest.raises(ValueError):
+        D.gather_units([torch.zeros(2)], plan, 0, 2)  # rank 0 raises too (same plan)
