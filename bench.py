@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=2024)
     ap.add_argument("--profile-only", action="store_true", help="one step, no timing (for ncu)")
     ap.add_argument("--workload", default="mnist", choices=["mnist", "mnist3", "cifar"])
+    ap.add_argument("--channels", type=int, default=None,
+                    help="use only the first K plaintext-CRT channels (tests; the metric uses all)")
     ap.add_argument("--shard", default="units", choices=["units", "groups"],
                     help="units: one slot-batch (x CRT channel) per rank, weak scaling; groups: one MNIST "
                          "slot-batch split over the ranks by output-channel group, strong scaling")
@@ -71,10 +73,12 @@ WORKLOADS = {
 }
 
 
-def build_workload(name: str, rank: int, world: int, seed: int):
+def build_workload(name: str, rank: int, world: int, seed: int, channels: int | None = None):
     """This rank's units of one step: (params, rlk, model, device input) per
     (slot-batch, CRT channel).  MNIST: one batch per rank (replicas);
-    CIFAR: the 10 channels of one batch shared by the ranks."""
+    CIFAR: the 10 channels of one batch, distributed.channel_plan: whole
+    channels per rank plus the leftover channels split by output channel
+    over subgroups (10 on 8 GPUs: 1 whole + 1/4 of a split channel each)."""
     from paper_1811_00778_b200 import bfv as B
     from paper_1811_00778_b200 import distributed as D
     from paper_1811_00778_b200 import engine as E
@@ -85,15 +89,22 @@ def build_workload(name: str, rank: int, world: int, seed: int):
     n = preset.ring_degree
     spec = nn.NETWORKS[w["net"]]()
     model = nn.random_model(spec, np.random.default_rng(seed + 1))
-    if preset.channels == 1:
-        plan = [[D.Unit(r, 0)] for r in range(world)]
+    splits = []
+    n_ch = min(preset.channels, channels or preset.channels)
+    if n_ch == 1 and preset.channels == 1:
+        whole = [[D.Unit(r, 0)] for r in range(world)]
         n_batches = world
     else:
-        plan = D.shard_plan(1, preset.channels, world)
+        wc, sp = D.channel_plan(n_ch, world)
+        whole = [[D.Unit(0, c) for c in wc[r]] for r in range(world)]
+        splits = [(D.Unit(0, c), ranks) for c, ranks in sp]
         n_batches = 1
+    owners = {u: r for r in range(world) for u in whole[r]}
+    owners.update({u: ranks[0] for u, ranks in splits})
+    mine = list(whole[rank]) + [u for u, ranks in splits if rank in ranks]
     units = []
     t0 = time.time()
-    for u in plan[rank]:
+    for u in mine:
         params = presets.build_context(preset, u.channel)
         sk, pk, rlk = B.keygen(params, np.random.default_rng(seed + 10 * u.channel))
         irng = np.random.default_rng(seed + 100 + u.batch)
@@ -102,9 +113,11 @@ def build_workload(name: str, rank: int, world: int, seed: int):
         gin = E.pack_images_device(images, E.PackingLayout(n, n), enc, pk, params,
                                    np.random.default_rng(seed + 200 + 31 * u.batch + u.channel),
                                    delta=w["delta"])
-        units.append(dict(unit=u, params=params, sk=sk, rlk=rlk, gin=gin, enc=enc,
+        split = next((ranks for v, ranks in splits if v == u), None)
+        units.append(dict(unit=u, params=params, sk=sk, rlk=rlk, gin=gin, enc=enc, split=split,
                           model=E.reduce_model(model, params.t), images=images))
-    return dict(units=units, plan=plan, n_batches=n_batches, images_per_step=n * n_batches,
+    return dict(units=units, owners=owners, splits=splits, n_batches=n_batches, images_per_step=n * n_batches,
+                moduli=tuple(int(t) for t in preset.plaintext_moduli[:n_ch]),
                 setup_s=time.time() - t0, desc=w["desc"], spec=spec, preset=preset)
 
 
@@ -259,35 +272,61 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())  # (oversubscribed tests)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        backend = os.environ.get("HCNN_DIST_BACKEND", "nccl")  # gloo: multi-rank logic on one GPU (tests)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     groups = args.shard == "groups"
     if groups and args.workload not in ("mnist", "mnist3"):
         raise SystemExit("--shard groups needs a grouped network (mnist, mnist3)")
     # groups: every rank holds the same slot-batch and evaluates its share of it
-    W = build_workload(args.workload, 0 if groups else rank, 1 if groups else world, args.seed)
+    W = build_workload(args.workload, 0 if groups else rank, 1 if groups else world, args.seed, args.channels)
     units = W["units"]
     ctxs = [E.context_for(u["params"]) for u in units]
     counters = []
+    split_pgs = D.split_groups([(u.channel, ranks) for u, ranks in W["splits"]]) if world > 1 and not groups else []
+    split_pg = {u: pg for (u, _), pg in zip(W["splits"], split_pgs)}
+    n_img = W["preset"].ring_degree
+    n_out = W["spec"].layers[-1].filters
+    dev = torch.device("cuda", local)
 
     def evaluate(u, x=None):
         counter = E.OpCounter()
         x = x if x is not None else u["gin"]
         if groups:
             out = D.eval_network_groups(x, u["model"], u["rlk"], u["params"], rank, world, counter)
+        elif u["split"] is not None:
+            out = D.run_split(x, u["model"], D.GpuSplitBackend(u["params"], u["rlk"]), u["split"], rank,
+                              split_pg.get(u["unit"]), counter)
         else:
             out = E.eval_network(x, u["model"], u["rlk"], u["params"], counter)
         counters.append(counter)
         return out
 
+    def finish(outs):
+        """The pipeline's last step: decrypt each logits tensor on the GPU that
+        owns it, gather the plaintext residues to rank 0 (NCCL), CRT-recombine
+        there on the GPU."""
+        local = {}
+        for u, o in zip(units, outs):
+            if o is not None:
+                local[u["unit"]] = D.decrypt_residues(o, u["sk"], u["params"], n_img)
+        if groups:
+            if rank != 0:
+                return None
+            owners = {D.Unit(0, 0): 0}
+            return D.gather_recombine(local, owners, W["moduli"], 1, 0, 1, (n_out, n_img), dev, lazy=True)
+        return D.gather_recombine(local, W["owners"], W["moduli"], W["n_batches"], rank, world, (n_out, n_img), dev,
+                                  lazy=True)
+
     def step(inputs=None):
         counters.clear()
         outs = [evaluate(u, None if inputs is None else inputs[i]) for i, u in enumerate(units)]
-        if world > 1 and not groups:
-            D.gather_units([o.data for o in outs], W["plan"], rank, world)
-        return outs
+        return finish(outs)
 
     if args.profile_only:
         step()
@@ -319,6 +358,8 @@ def run_ours(args):
         dist.barrier()
     launches = sum(g.launches() for g in ctxs) - launches0
     step_counters = list(counters[-len(units):])  # the last timed step's counters (one per unit)
+    # the last step's signed logits, read on the host after the timed region
+    result_shape = list(outs[0].values().T.shape) if (rank == 0 and outs) else None
     ms = ev0.elapsed_time(ev1) / args.steps
     prof = {}
     for g in ctxs:
@@ -344,7 +385,7 @@ def run_ours(args):
                  for _ in range(e2e_steps)] for u in units]
     def e2e_run(k):
         for u, h, ho in zip(units, host_in, host_out):
-            if groups:  # upload, sharded evaluation, logits back on rank 0
+            if groups or u["split"] is not None:  # upload, sharded evaluation, logits back on the root
                 for i in range(k):
                     x = E.GpuCipherTensor(u["gin"].shape, h.to("cuda", non_blocking=True), u["gin"].delta,
                                           u["gin"].channel_modulus, u["params"])
@@ -530,8 +571,15 @@ def run_ours(args):
             "model": f"{W['spec'].name}, dense random 4-bit weights (every tap executes)",
             "global_batch": images,
             "parallelism": ("single" if world == 1 else f"output-channel-groups/{world}" if groups
-                            else f"replicas{world}" if W["preset"].channels == 1 else f"crt-channels/{world}"),
+                            else f"replicas{world}" if W["preset"].channels == 1
+                            else f"crt-channels/{world}" + (f" + output-channel split of channels "
+                                                            f"{[u.channel for u, _ in W['splits']]} over "
+                                                            f"{[len(r) for _, r in W['splits']]} ranks"
+                                                            if W["splits"] else "")),
+            "step": "evaluation of every unit + GPU decryption of the logits on the owning GPU + NCCL gather of "
+                    "the plaintext residues to rank 0 + GPU CRT recombination there",
             "units_on_rank0": len(units),
+            "crt_channels": len(W["moduli"]),
             **({"groups_on_rank0": D.group_plan(D.groupable(W["spec"]), world)[0]} if groups else {}),
             "hsquare_per_unit": c0.hsquare,
             "mult_plain_per_unit": c0.mult_plain_scheduled,
@@ -547,6 +595,7 @@ def run_ours(args):
                         "evaluation of step s; two device input buffers; the first batch streamed by row bands into "
                         "a conv1/square1/conv2/square2 wavefront) -> pinned host logits", "steps": e2e_steps},
         "e2e_dropin": dropin,
+        "logits_shape_per_batch": result_shape,
         "gpu_launches": int(launches),
         "kernels": kernels,
         "roofline": roof,

@@ -194,10 +194,13 @@ int hcnn_host_narrow(const int64_t* const* src, size_t count, size_t len, uint32
  * [2, 2^62), at most 16.  out: DEVICE u32 [count][words], the centred value
  * (X - T when X > floor(T/2), T = prod moduli) as little-endian two's
  * complement words; words must exceed the word length of T.  Runs on
- * `stream` of `device` and synchronises it (HCNN_ERR_PARAM for a residue
- * outside its range, which the reference raises as HefirError). */
+ * `stream` of `device`.  flag: NULL = the range check is done here (the
+ * call synchronises the stream and returns HCNN_ERR_PARAM for a residue
+ * outside its range, which the reference raises as HefirError); else a
+ * DEVICE int (zeroed by the caller) that the kernel sets non-zero on a bad
+ * residue, and the call stays asynchronous. */
 int hcnn_crt_combine(const uint64_t* res, const uint64_t* moduli, int n_moduli, size_t count, uint32_t* out,
-                     int words, int device, void* stream);
+                     int words, int* flag, int device, void* stream);
 
 /* Per-kernel CUDA-event timing on the context's stream.  hcnn_profile(ctx, 1)
  * resets and starts recording; hcnn_profile_dump writes "name count total_ms"

@@ -907,7 +907,7 @@ uint64_t inv_mod_u64(uint64_t a, uint64_t m) {  // a^-1 mod m (gcd 1), extended 
 }  // namespace
 
 int hcnn_crt_combine(const uint64_t* res, const uint64_t* moduli, int n_moduli, size_t count, uint32_t* out,
-                     int words, int device, void* stream) {
+                     int words, int* flag, int device, void* stream) {
   return guarded([&] {
     if (!moduli || n_moduli < 1 || n_moduli > CRT_MAXC) fail(HCNN_ERR_PARAM, "1..16 CRT moduli supported");
     if (words < 1 || words > CRT_MAXW) fail(HCNN_ERR_PARAM, "output words out of range");
@@ -938,16 +938,20 @@ int hcnn_crt_combine(const uint64_t* res, const uint64_t* moduli, int n_moduli, 
     if (!res || !out) fail(HCNN_ERR_PARAM, "null argument");
     CK(cudaSetDevice(device));
     cudaStream_t st = (cudaStream_t)stream;
-    int* bad = nullptr;
-    pool_malloc(&bad, sizeof(int), st, device);
-    CK(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    int* bad = flag;
+    if (!bad) {
+      pool_malloc(&bad, sizeof(int), st, device);
+      CK(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    }
     k_crt_combine<<<(unsigned)((count + 127) / 128), 128, 0, st>>>(res, count, tb, out, bad);
     CK(cudaGetLastError());
-    int h_bad = 0;
-    CK(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaFreeAsync(bad, st));
-    CK(cudaStreamSynchronize(st));
-    if (h_bad) fail(HCNN_ERR_PARAM, "CRT residue outside [0, t_i)");
+    if (!flag) {  // checked here: synchronous
+      int h_bad = 0;
+      CK(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaFreeAsync(bad, st));
+      CK(cudaStreamSynchronize(st));
+      if (h_bad) fail(HCNN_ERR_PARAM, "CRT residue outside [0, t_i)");
+    }
   });
 }
 

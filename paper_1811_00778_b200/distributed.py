@@ -21,6 +21,15 @@ import torch
 import torch.distributed as dist
 
 
+def _comm_device(t: torch.Tensor, group=None) -> torch.device:
+    """Where a collective's buffers live: the tensor's own device, except
+    CUDA tensors under gloo (which has no CUDA gather), staged through host
+    memory; on B200 boxes the backend is NCCL and nothing is staged."""
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        return torch.device("cpu")
+    return t.device
+
+
 @dataclass(frozen=True)
 class Unit:
     batch: int    # slot-batch index
@@ -56,7 +65,8 @@ def gather_units(local: list, plan: list, rank: int, world: int, dst: int = 0, g
         raise ValueError("a rank of the plan has no units: pass `template` (or use fewer ranks)")
     like = local[0] if local else template
     shape, dtype, device = like.shape, like.dtype, like.device
-    send = torch.zeros((max_units,) + tuple(shape), dtype=dtype, device=device)
+    cdev = _comm_device(like, group)
+    send = torch.zeros((max_units,) + tuple(shape), dtype=dtype, device=cdev)
     for i, t in enumerate(local):
         send[i].copy_(t)
     bufs = [torch.empty_like(send) for _ in range(world)] if rank == dst else None
@@ -66,7 +76,7 @@ def gather_units(local: list, plan: list, rank: int, world: int, dst: int = 0, g
     out = {}
     for r in range(world):
         for i, u in enumerate(plan[r]):
-            out[u] = bufs[r][i]
+            out[u] = bufs[r][i].to(device)
     return out
 
 
@@ -182,10 +192,13 @@ def eval_network_groups(tensor, model, rlk, params, rank: int, world: int, count
     send = part.data if part is not None else g.empty(n_out)
     if part is None:
         send.zero_()
+    home = send.device
+    send = send.to(_comm_device(send, group))
     bufs = [torch.empty_like(send) for _ in range(world)] if rank == dst else None
     dist.gather(send, bufs, dst=dst, group=group)
     if rank != dst:
         return None
+    bufs = [b.to(home) for b in bufs]
     from . import ops
 
     acc = bufs[active[0]]
@@ -391,14 +404,15 @@ def run_split(x, model, backend, ranks: list, rank: int, group=None, counter=Non
             kind, data = gen.send(msg)
         except StopIteration as stop:
             return stop.value
+        home = data.device
+        data = data.to(_comm_device(data, group))
         if kind == "all_gather":
             lst = [torch.empty_like(data) for _ in range(S)]
             dist.all_gather(lst, data, group=group)
-            msg = lst
         else:
             lst = [torch.empty_like(data) for _ in range(S)] if me == 0 else None
             dist.gather(data, lst, dst=ranks[0], group=group)
-            msg = lst
+        msg = [t.to(home) for t in lst] if lst is not None else None
 
 
 def split_groups(splits):
@@ -421,7 +435,7 @@ def decrypt_residues(logits, sk, params, batch_size: int) -> torch.Tensor:
 
 
 def gather_recombine(local: dict, owners: dict, moduli, n_batches: int, rank: int, world: int, shape, device,
-                     dst: int = 0, group=None):
+                     dst: int = 0, group=None, lazy: bool = False):
     """The pipeline's one exchange: every rank holds the decrypted residues
     (DEVICE int64 (outputs, batch)) of the (batch, channel) units it owns
     (`local`: {Unit: tensor}); `owners` maps every Unit to its rank (identical
@@ -430,8 +444,10 @@ def gather_recombine(local: dict, owners: dict, moduli, n_batches: int, rank: in
     CRT-recombined there on the GPU.  `shape` = (outputs, batch) of one
     matrix and `device` this rank's device (ranks that own no unit still take
     part in the gather).  Returns the signed logits [(batch, outputs) object
-    array per slot-batch] on dst, None elsewhere."""
-    from .engine import ChannelResult, reconstruct_logits
+    array per slot-batch] on dst, None elsewhere; lazy=True returns the
+    engine.DeviceCrtValues instead (no host synchronisation; .values().T is
+    the (batch, outputs) array)."""
+    from .engine import ChannelResult, reconstruct_logits, reconstruct_logits_device
 
     units = sorted(owners, key=lambda u: (u.batch, u.channel))
     plan = [[u for u in units if owners[u] == r] for r in range(world)]
@@ -443,6 +459,9 @@ def gather_recombine(local: dict, owners: dict, moduli, n_batches: int, rank: in
     moduli = tuple(int(m) for m in moduli)
     out = []
     for b in range(n_batches):
+        if lazy and res[Unit(b, 0)].is_cuda:
+            out.append(reconstruct_logits_device([res[Unit(b, c)] for c in range(len(moduli))], moduli))
+            continue
         cr = ChannelResult(moduli=moduli, batch_size=int(res[Unit(b, 0)].shape[1]))
         for c, t in enumerate(moduli):
             cr.add(t, res[Unit(b, c)])

@@ -1162,10 +1162,26 @@ def _words_to_ints(words: np.ndarray) -> np.ndarray:
                     dtype=object)
 
 
-def crt_combine_device(res: torch.Tensor, moduli) -> np.ndarray:
+class DeviceCrtValues:
+    """Result of an asynchronous GPU CRT recombination: the signed values as
+    DEVICE u32 words plus the kernel's range-check flag; nothing waits on the
+    GPU until .values() (the client's host read)."""
+
+    def __init__(self, words: torch.Tensor, flag: torch.Tensor, shape):
+        self.words, self.flag, self.shape = words, flag, tuple(shape)
+
+    def values(self) -> np.ndarray:
+        """object array of signed Python ints, reshaped to `shape`"""
+        if int(self.flag.item()):
+            raise HefirError("CRT residue outside [0, t_i)")
+        return _words_to_ints(self.words.cpu().numpy().view(np.uint32)).reshape(self.shape)
+
+
+def crt_combine_device(res: torch.Tensor, moduli, sync: bool = True):
     """Centred CRT recombination on the GPU: res DEVICE int64 [C][M] (residue of
     value m mod moduli[i] at [i][m]) -> object array [M] of signed Python ints
-    equal to CrtSystem.reconstruct_centered (codec.py:79-89) of each column."""
+    equal to CrtSystem.reconstruct_centered (codec.py:79-89) of each column.
+    sync=False returns a DeviceCrtValues (no host synchronisation)."""
     moduli = [int(t) for t in moduli]
     if res.dim() != 2 or res.shape[0] != len(moduli):
         raise ParameterMismatchError("residue rows != modulus count")
@@ -1176,14 +1192,17 @@ def crt_combine_device(res: torch.Tensor, moduli) -> np.ndarray:
     res = res.to(dtype=torch.int64).contiguous()
     dev = res.device
     out = torch.empty((res.shape[1], words), dtype=torch.int32, device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
     arr = (_lib.C.c_uint64 * len(moduli))(*moduli)
     stream = torch.cuda.current_stream(dev).cuda_stream
     try:
         _lib.check(_lib.lib().hcnn_crt_combine(_ptr(res), arr, len(moduli), res.shape[1], _ptr(out), words,
-                                               dev.index or 0, _lib.C.c_void_p(stream)), "hcnn_crt_combine")
-    except ParameterMismatchError as e:  # out-of-range residue / non-coprime moduli, as the reference raises
+                                               _ptr(flag), dev.index or 0, _lib.C.c_void_p(stream)),
+                   "hcnn_crt_combine")
+    except ParameterMismatchError as e:  # non-coprime / out-of-range moduli, as the reference raises
         raise HefirError(str(e)) from None
-    return _words_to_ints(out.cpu().numpy().view(np.uint32))
+    lazy = DeviceCrtValues(out, flag, (res.shape[1],))
+    return lazy if not sync else lazy.values()
 
 
 def reconstruct_logits(result, crt_moduli) -> np.ndarray:
@@ -1205,6 +1224,18 @@ def reconstruct_logits(result, crt_moduli) -> np.ndarray:
     C, outputs, batch = stack.shape
     vals = crt_combine_device(stack.reshape(C, -1), moduli)
     return vals.reshape(outputs, batch).T.copy()
+
+
+def reconstruct_logits_device(mats, moduli) -> "DeviceCrtValues":
+    """reconstruct_logits without a host synchronisation: mats = per-channel
+    DEVICE int64 (outputs, batch) residues in `moduli` order; returns a
+    DeviceCrtValues whose .values() is the (outputs, batch) object array
+    (transpose for the reference's (batch, outputs))."""
+    stack = torch.stack([m.to(dtype=torch.int64) for m in mats])
+    C, outputs, batch = stack.shape
+    lazy = crt_combine_device(stack.reshape(C, -1), moduli, sync=False)
+    lazy.shape = (outputs, batch)
+    return lazy
 
 
 def reconstruct_logits_host(result, crt_moduli) -> np.ndarray:
