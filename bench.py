@@ -602,62 +602,137 @@ def run_ours(args):
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline and args.workload == "mnist":
-        line["cpu_baseline"] = cpu_baseline_sample(units[0], threads=1)
+        line["cpu_baseline"] = cpu_baseline_sample(units[0], args.seed, threads=1)
     print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------- CPU arms
+#
+# The reference itself (hefir, installed unmodified into baseline/_ref with
+# `pip install --target`; gmpy2 is absent from this image and is replaced by
+# tests/_shim/gmpy2.py, `mpz = int`: the same exact integers, slower big-int
+# multiplies) is timed on the host cores through its own public API on a
+# bounded sample of the MNIST set-1 step, and extrapolated to the full batch:
+#   conv     engine.eval_conv on a 7x7 crop of the input -> 2x2x5 = 20 outputs
+#            (25 taps each, the dense random weights of the workload); conv1
+#            has 720 and conv2 800 such 25-tap outputs (x 1520 / 20)
+#   square   engine.eval_square of one ciphertext per host process, `cores`
+#            processes at once (x 1520 / cores)
+#   fc       engine.eval_fc of one 800-tap output (x 10)
+# When baseline/_ref is absent, the pinned oracle port (oracle/) is timed
+# the same way instead (kind "port").
+
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+_REF = {}
 
 
-def _oracle_inputs(W):
-    """one ciphertext + rlk of the workload as numpy, for the oracle port"""
+def _import_hefir():
+    if not os.path.isdir(os.path.join(REF_DIR, "hefir")):
+        return None
+    for p in (os.path.join(ROOT, "tests", "_shim"), REF_DIR):
+        if p not in sys.path:
+            sys.path.insert(0, p)
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_bench")
+    try:
+        from hefir import bfv, engine, nn_oracle, presets, ring  # noqa: F401
+    except Exception:
+        return None
+    import hefir
+
+    return hefir
+
+
+def _ref_setup(seed: int):
+    """hefir params / keys / one encrypted ciphertext at set 1, and the
+    workload's dense random weights (bench.build_workload's seeds)."""
+    from hefir import bfv, engine, nn_oracle, presets
+    from paper_1811_00778_b200 import nn
+
+    params = presets.build_context(presets.load_preset("1"))
+    n = params.ring_degree
+    sk, pk, rlk = bfv.keygen(params, np.random.default_rng(seed))
+    erng = np.random.default_rng(seed + 5)
+    c = bfv.encrypt(pk, bfv.Plaintext(erng.integers(0, MNIST_T, n), MNIST_T), params, erng)
+    model = nn.random_model(nn.mnist_hcnn(), np.random.default_rng(seed + 1))
+    spec = nn_oracle.mnist_hcnn()
+    crop = engine.CipherTensor(shape=(7, 7, 1), cts=[c] * 49, delta=4, channel_modulus=MNIST_T)
+    flat = engine.CipherTensor(shape=(1, 1, 800), cts=[c] * 800, delta=4, channel_modulus=MNIST_T)
+    one = engine.CipherTensor(shape=(1, 1, 1), cts=[c], delta=4, channel_modulus=MNIST_T)
+    _REF.update(params=params, rlk=rlk, crop=crop, flat=flat, one=one, conv1=spec.layers[0], fc=spec.layers[4],
+                w_conv=np.asarray(model.weights[0]), w_fc=np.asarray(model.weights[4])[:1], engine=engine)
+
+
+def _ref_square_worker(_):
+    e = _REF["engine"]
+    t0 = time.perf_counter()
+    e.eval_square(_REF["one"], _REF["rlk"], _REF["params"], e.OpCounter())
+    return time.perf_counter() - t0
+
+
+def _ref_step(cores: int, pool):
+    """One bounded sample; returns (seconds of each part)."""
+    e, params = _REF["engine"], _REF["params"]
+    t0 = time.perf_counter()
+    out = e.eval_conv(_REF["crop"], _REF["conv1"], _REF["w_conv"], params, e.OpCounter(), workers=cores)
+    t1 = time.perf_counter()
+    assert len(out.cts) == 20
+    if pool is None:
+        _ref_square_worker(0)
+    else:
+        pool.map(_ref_square_worker, range(cores), chunksize=1)
+    t2 = time.perf_counter()
+    e.eval_fc(_REF["flat"], _REF["fc"], _REF["w_fc"], params, e.OpCounter(), workers=cores)
+    t3 = time.perf_counter()
+    return t1 - t0, t2 - t1, t3 - t2
+
+
+def _extrapolate(t_conv20, t_sq_wall, t_fc1, cores):
+    # MNIST step: 720 + 800 25-tap conv outputs, 1520 HSquares, 10 x 800-tap fc outputs
+    return (720 + 800) / 20 * t_conv20 + 1520 / cores * t_sq_wall + 10 * t_fc1
+
+
+def _sample_desc(cores, parts, kind):
+    c, q, f = parts
+    what = ("hefir (the reference, baseline/_ref, unmodified; gmpy2 shimmed by mpz = int: exact, slower "
+            "big-int multiplies than real gmpy2)") if kind == "reference" else "oracle port (oracle/hcnn_oracle.py)"
+    return (f"{what} at N=8192/set 1, its public engine API: eval_conv of 20 conv1 outputs ({c:.2f}s), "
+            f"eval_square of {cores} ciphertexts on {cores} processes ({q:.2f}s wall), eval_fc of one 800-tap "
+            f"output ({f:.2f}s); extrapolated x76 conv, x{1520 / cores:.0f} square, x10 fc to the 8192-image batch")
+
+
+def _port_step(W, cores):
+    """oracle-port fallback: same sample shape"""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import hcnn_oracle as O
 
     params = W["params"]
     op = O.Params(O.Context(params.ring_degree, [pm.value for pm in params.ctx.primes]), params.t)
     rlk = [(k0.residues, k1.residues) for k0, k1 in W["rlk"].components]
     x = W["gin"].data[:1].cpu().numpy().view(np.uint32).astype(np.int64)[0]
-    return op, rlk, (x[0], x[1])
-
-
-def _hsq_time(op, rlk, ct):
-    import hcnn_oracle as O
-
+    ct = (x[0], x[1])
     t0 = time.perf_counter()
+    for _ in range(20):
+        O.weighted_sum(op, [(ct, 3)] * 25, O.Counter())
+    t1 = time.perf_counter()
     O.hsquare(op, ct, rlk)
-    return time.perf_counter() - t0
+    t2 = time.perf_counter()
+    O.weighted_sum(op, [(ct, 3)] * 800, O.Counter())
+    t3 = time.perf_counter()
+    return t1 - t0, t2 - t1, t3 - t2
 
 
-def _ws_time(op, ct, taps):
-    import hcnn_oracle as O
-
-    t0 = time.perf_counter()
-    O.weighted_sum(op, [(ct, 3)] * taps, O.Counter())
-    return time.perf_counter() - t0
-
-
-def _extrapolate(t_hsq, t_ws25, t_ws800):
-    # MNIST: conv1 720 outputs x 25 taps, 720 HSquare, conv2 800 x 25, 800 HSquare, fc 10 x 800
-    return 1520 * t_hsq + 1520 * t_ws25 + 10 * t_ws800
-
-
-def cpu_baseline_sample(W, threads: int = 1):
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    op, rlk, ct = _oracle_inputs(W)
-    t_hsq = _hsq_time(op, rlk, ct)
-    t_ws25 = _ws_time(op, ct, 25)
-    t_ws800 = _ws_time(op, ct, 800)
-    T = _extrapolate(t_hsq, t_ws25, t_ws800)
-    return {"value": round(8192 / T, 4), "unit": "images/s", "cores": threads, "kind": "port",
-            "latency_s_extrapolated": round(T, 1),
-            "sample": f"oracle port (oracle/hcnn_oracle.py, same algorithm as hefir: exact CRT lift + "
-                      f"Kronecker big-int tensor) at N=8192/set 1: 1 HSquare ({t_hsq:.2f}s) + one 25-tap and "
-                      f"one 800-tap weighted sum, extrapolated x1520 HSquare / 1520 25-tap / 10 800-tap"}
-
-
-def _worker_hsq(args):
-    op, rlk, ct = args
-    return _hsq_time(op, rlk, ct)
+def cpu_baseline_sample(W, seed: int, threads: int = 1):
+    """Our arm's cpu_baseline: one bounded sample of the reference on 1 core."""
+    if _import_hefir() is not None:
+        _ref_setup(seed)
+        parts = _ref_step(1, None)
+        kind = "reference"
+    else:
+        parts = _port_step(W, 1)
+        kind = "port"
+    T = _extrapolate(*parts, 1)
+    return {"value": round(8192 / T, 4), "unit": "images/s", "cores": threads, "kind": kind,
+            "latency_s_extrapolated": round(T, 1), "sample": _sample_desc(1, parts, kind)}
 
 
 def run_reference(args):
@@ -667,33 +742,20 @@ def run_reference(args):
         return
     import multiprocessing as mp
 
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import hcnn_oracle as O
-    from paper_1811_00778_b200 import bfv as B
-
-    n = 8192
-    params = B.BfvParams(B.RnsContext(n, SET1_PRIMES), MNIST_T)
-    sk, pk, rlk = B.keygen(params, np.random.default_rng(args.seed))
-    erng = np.random.default_rng(args.seed + 5)
-    c = B.encrypt(pk, B.Plaintext(erng.integers(0, MNIST_T, n), MNIST_T), params, erng)
-    op = O.Params(O.Context(n, SET1_PRIMES), MNIST_T)
-    orlk = [(k0.residues, k1.residues) for k0, k1 in rlk.components]
-    ct = (c.parts[0].residues, c.parts[1].residues)
     cores = os.cpu_count() or 1
-    t_ws25 = _ws_time(op, ct, 25)
-    t_ws800 = _ws_time(op, ct, 800)
-    ctxm = mp.get_context("fork")
+    if _import_hefir() is None:
+        print(json.dumps({"impl": "reference", "unavailable": "baseline/_ref (pip install --target of the reference) "
+                                                             "is missing or does not import"}), flush=True)
+        return
+    _ref_setup(args.seed)
     vals = []
-    with ctxm.Pool(cores) as pool:
+    with mp.get_context("fork").Pool(cores) as pool:
         for i in range(args.warmup + args.steps):
-            t0 = time.perf_counter()
-            pool.map(_worker_hsq, [(op, orlk, ct)] * cores)
-            wall = time.perf_counter() - t0
+            parts = _ref_step(cores, pool)
             if i >= args.warmup:
-                vals.append(wall)
-    wall = float(np.mean(vals))
-    # `cores` HSquares per `wall` seconds; MACs parallelise the same way
-    T = (1520 * wall / cores) + (1520 * t_ws25 + 10 * t_ws800) / cores
+                vals.append(parts)
+    parts = tuple(float(np.mean([v[k] for v in vals])) for k in range(3))
+    T = _extrapolate(*parts, cores)
     value = 8192 / T
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": "images/s", "n_gpus": world,
@@ -701,13 +763,14 @@ def run_reference(args):
         "latency_s": round(T, 2), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int (Python big int / int64)", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": "MNIST HCNN, preset 1 (N=8192, 11 primes, t=5522259017729), one 8192-image slot-batch",
-                   "parallelism": f"{cores} host processes"},
-        "cpu_baseline": {"value": round(value, 4), "unit": "images/s", "cores": cores, "kind": "port",
-                         "sample": f"per step: {cores} HSquares in parallel (one per core, oracle port of "
-                                   f"hefir's exact Kronecker path) at N=8192/set 1, mean wall {wall:.2f}s; plus "
-                                   f"25/800-tap weighted sums; extrapolated to 1520 HSquare + 46,000 MACs"},
+        "config": {"workload": "MNIST HCNN, preset 1 (N=8192, 11 primes, t=5522259017729), one 8192-image slot-batch, "
+                               "dense random 4-bit weights",
+                   "parallelism": f"{cores} host processes (squares) / eval_conv and eval_fc with workers={cores}"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "images/s", "cores": cores, "kind": "reference",
+                         "sample": _sample_desc(cores, parts, "reference") + "; per step, mean of the timed steps"},
         "e2e": {"value": round(value, 4), "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "the reference with real gmpy2 would multiply faster (its README quotes ~0.29 s per HSquare); "
+                "gmpy2 is not installable here",
     }
     print(json.dumps(line), flush=True)
 

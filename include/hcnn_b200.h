@@ -187,6 +187,11 @@ int hcnn_ntt(hcnn_ctx* ctx, uint32_t* rows, size_t n_rows, uint32_t limbs, uint3
  * host CipherTensor before it crosses PCIe (engine.py:42-58 objects in). */
 int hcnn_host_narrow(const int64_t* const* src, size_t count, size_t len, uint32_t* dst, int threads);
 
+/* Return the library pool's free memory on `device` to the driver (the pool
+ * keeps freed blocks across synchronisations otherwise).  Synchronises the
+ * device; workspaces owned by live contexts are not freed. */
+int hcnn_release_memory(int device);
+
 /* Plaintext-CRT recombination on the device (engine.reconstruct_logits,
  * engine.py:494-506 / CrtSystem.reconstruct_centered, codec.py:79-89):
  * res: DEVICE u64 [n_moduli][count], residue of value m mod moduli[i] at

@@ -906,6 +906,14 @@ uint64_t inv_mod_u64(uint64_t a, uint64_t m) {  // a^-1 mod m (gcd 1), extended 
 }
 }  // namespace
 
+int hcnn_release_memory(int device) {
+  return guarded([&] {
+    CK(cudaSetDevice(device));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemPoolTrimTo(lib_pool(device), 0));
+  });
+}
+
 int hcnn_crt_combine(const uint64_t* res, const uint64_t* moduli, int n_moduli, size_t count, uint32_t* out,
                      int words, int* flag, int device, void* stream) {
   return guarded([&] {

@@ -245,6 +245,22 @@ class GpuContext:
 _CTXS: dict = {}
 
 
+def release_memory(device=None):
+    """Drop every cached context (their workspaces and keys) and codec on
+    `device`, and return the library pool's and torch's cached free memory
+    to the driver."""
+    import gc
+
+    dev = _device_index(device)
+    for cache in (_CTXS, _CODECS):
+        for k in [k for k in cache if k[-1] == dev]:
+            del cache[k]
+    gc.collect()
+    torch.cuda.synchronize(dev)
+    _lib.check(_lib.lib().hcnn_release_memory(dev), "hcnn_release_memory")
+    torch.cuda.empty_cache()
+
+
 def context_for(params, device=None) -> GpuContext:
     key = (params.fingerprint, _device_index(device))
     c = _CTXS.get(key)

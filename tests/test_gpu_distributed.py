@@ -126,6 +126,7 @@ def test_bench_two_ranks_on_one_gpu_gloo(workload, tmp_path):
     MNIST: 2 replicas, logits recombined on rank 0; CIFAR with its first 3
     CRT channels (--channels 3, to fit two processes on one GPU): one whole
     channel per rank and channel 2 split by output channel over both."""
+    E.release_memory()  # this process's cached device memory: the two ranks need the GPU
     env = dict(os.environ, HCNN_DIST_BACKEND="gloo")
     extra = ["--workload", "mnist"] if workload == "mnist" else ["--workload", "cifar", "--channels", "3"]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
