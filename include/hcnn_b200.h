@@ -70,8 +70,11 @@ enum {
  * relinearisation sums in TMEM, 2048 square tensor with one-row transforms
  * and rows parked in TMEM, 4096 square tensor with pair transforms and d2
  * parked in TMEM, 8192 persistent square tensor (one CTA per SM, TMA
- * prefetch of the next item's rows).  Default per N: 8192 at 2^13,
- * 64|1024|4096 at 2^14, 512|2048 at 2^15, 0 otherwise.  Results are identical for every setting. */
+ * prefetch of the next item's rows), 16384 relinearisation over a shared
+ * three-prime basis R (digit NTTs mod 3 primes instead of mod every q_j, exact
+ * CRT back; N = 2^12 and 2^13, at most 23 digits).  Default per N:
+ * 8192|16384 at 2^13, 64|1024|4096 at 2^14, 512|2048 at 2^15, 0 otherwise.
+ * Results are identical for every setting. */
 enum { HCNN_OPT_NTT_VARIANT = 1 };
 int hcnn_ctx_set_option(hcnn_ctx* ctx, int key, int64_t value);
 int64_t hcnn_ctx_query(hcnn_ctx* ctx, int what);

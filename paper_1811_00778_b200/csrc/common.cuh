@@ -72,6 +72,25 @@ struct NttTabs {
   const uint2* ninv_mw;   // [K+KP]        psi^-N/2 N^-1 2^32
 };
 
+// Relinearisation through a shared three-prime basis R = r0 r1 r2
+// (flag RELIN_RBASIS).  The key-switching sums Z = sum_i d_i k_i over
+// Z[X]/(X^N+1), with digits d_i in [0, w) and key rows k_i centred mod q_j,
+// satisfy |Z| < D N w q_j / 2 < R / 2, so the NTTs of the digits are taken
+// once over R (3 per digit instead of K) and Z mod q_j is recovered exactly
+// from Z mod r0, r1, r2 (Garner, centred).  Table index of r_a: roff + a.
+constexpr int RB_A = 3;
+struct RbTabs {
+  int roff;
+  uint32_t r[RB_A];
+  uint2 t32[RB_A];     // 2^32 mod r_a (Shoup): folds the high word of a 64-bit sum
+  uint32_t one[RB_A];  // floor(2^32 / r_a): the Shoup word of 1 (low word)
+  uint2 isc_n[RB_A], isc_nw[RB_A];  // inverse scaling N^-1 g_a, psi^-N/2 N^-1 g_a with
+                                    // g_a = (R/r_a)^-1 mod r_a: the inverse leaves x~_a
+  float rinv[RB_A];    // 1 / r_a: v = rint(sum_a x~_a / r_a) (|Z| / R < 2^-25)
+  uint32_t crt_q[KMAX][RB_A];  // (R/r_a) 2^32 mod q_j (Montgomery form)
+  uint32_t negR_q[KMAX];       // -R 2^32 mod q_j (Montgomery form)
+};
+
 // Output scaling of an inverse transform, folded into its last stage (whose
 // butterflies all share the twiddle psi^-N/2): n for the sum, nw for the
 // difference.

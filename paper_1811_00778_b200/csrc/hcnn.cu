@@ -14,6 +14,7 @@
 #include "kernels.cuh"
 #include "ntt_kernels.cuh"
 #include "ntt64.cuh"
+#include "relin_rb.cuh"
 #include "tables.hpp"
 
 using namespace hcnn;
@@ -125,6 +126,12 @@ struct hcnn_ctx {
   int pk_domain = 0;
   int variant = 0;       // NTT radix variant of the fused kernels (0 = default)
   int keys_variant = -1; // variant the tiled keys were laid out for
+  // relinearisation over R (RELIN_RBASIS): usable when D <= RB_DMAX and
+  // R > 2 (D N (w-1) max q_j / 2 + r0 r1)
+  bool rb_ok = false;
+  RbTabs rb{};
+  uint32_t* d_rlk_rb = nullptr;  // [RB_A][D][2K][N] NTT domain mod r_a, tiled
+  bool rb_keys = false;
   uint2* d_delta = nullptr;
   bool rlk_reduce = false;
   uint8_t* ws = nullptr;
@@ -242,7 +249,18 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
   c->KP = (uint32_t)P.size();
   c->primes = q;
   c->primes.insert(c->primes.end(), P.begin(), P.end());
-  const uint32_t L = c->K + c->KP;
+  // R: three primes = 1 mod 2^17 with D (r - 1)^2 < 2^64 for D <= RB_DMAX
+  std::vector<u64> R;
+  {
+    const u64 rmax = 895562590ull;  // 23 (rmax - 1)^2 < 2^64
+    for (u64 k = rmax >> 17; R.size() < (size_t)RB_A && k > 1; --k) {
+      const u64 r = (k << 17) + 1;
+      if (r > rmax || std::find(c->primes.begin(), c->primes.end(), r) != c->primes.end()) continue;
+      if (is_prime64(r)) R.push_back(r);
+    }
+    c->primes.insert(c->primes.end(), R.begin(), R.end());
+  }
+  const uint32_t L = c->K + c->KP + RB_A;
 
   // NTT tables
   std::vector<uint32_t> hp(L);
@@ -281,6 +299,39 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
     const uint32_t nw = (uint32_t)mulmod64(wl, ninv, p), nmw = (uint32_t)mulmod64(wl, ninv_m, p);
     hninv[2 * L + j] = make_uint2(nw, shoup_of(nw, (uint32_t)p));
     hninv[3 * L + j] = make_uint2(nmw, shoup_of(nmw, (uint32_t)p));
+  }
+
+  // relinearisation over R: CRT constants and the exactness bound
+  {
+    RbTabs& rb = c->rb;
+    std::memset(&rb, 0, sizeof(rb));
+    rb.roff = (int)(c->K + c->KP);
+    auto shp = [](u64 w, u64 m) { return make_uint2((uint32_t)w, shoup_of((uint32_t)w, (uint32_t)m)); };
+    u128 Rp = 1;
+    for (int a = 0; a < RB_A; ++a) Rp *= R[a];
+    for (int a = 0; a < RB_A; ++a) {
+      const u64 r = R[a];
+      rb.r[a] = (uint32_t)r;
+      rb.t32[a] = shp(((u64)1 << 32) % r, r);
+      rb.one[a] = shoup_of(1, (uint32_t)r);
+      const u64 g = invmod64((u64)((Rp / r) % r), r);  // (R/r_a)^-1 mod r_a
+      const uint32_t jj = (uint32_t)rb.roff + a;
+      rb.isc_n[a] = shp(mulmod64(hninv[jj].x, g, r), r);
+      rb.isc_nw[a] = shp(mulmod64(hninv[2 * L + jj].x, g, r), r);
+      rb.rinv[a] = (float)(1.0 / (double)r);
+    }
+    u64 qmax = 0;
+    for (uint32_t j = 0; j < c->K; ++j) {
+      const u64 qj = q[j];
+      qmax = qj > qmax ? qj : qmax;
+      for (int a = 0; a < RB_A; ++a) rb.crt_q[j][a] = (uint32_t)mont_form((u64)((Rp / R[a]) % qj), qj);
+      rb.negR_q[j] = (uint32_t)mont_form((qj - (u64)(Rp % qj)) % qj, qj);
+    }
+    // |Z| <= D N (w - 1) floor(q_j / 2) must stay below R/4: then
+    // sum_a x~_a / r_a lies within 1/4 of the integer v and the fp32 estimate
+    // (error below 2^-20) rounds to it
+    const u128 zmax = (u128)c->D * N * (((u128)1 << c->log2w) - 1) * (qmax / 2);
+    c->rb_ok = R.size() == (size_t)RB_A && c->D <= (uint32_t)RB_DMAX && zmax < (Rp >> 2);
   }
 
   // exact base conversion and scaling constants
@@ -437,7 +488,99 @@ void launch_tensor(hcnn_ctx* c, const uint32_t* a_, const uint32_t* ae, const ui
 
 void prepare_keys(hcnn_ctx* c);
 
+unsigned cdiv(size_t a, size_t b) { return (unsigned)((a + b - 1) / b); }
+
+// variant bit: relinearisation over the shared basis R (relin_rb.cuh)
+constexpr int RELIN_RBASIS = 16384;
+
+bool rb_active(const hcnn_ctx* c) {
+  return (c->variant & RELIN_RBASIS) && c->rb_ok && (c->logN == 12 || c->logN == 13) && !(c->variant & 64);
+}
+
+// key rows mod r_a in the NTT domain (tiled layout of the R kernels' geometry)
+void prepare_rb_keys(hcnn_ctx* c) {
+  if (c->rb_keys || !c->d_rlk_raw) return;
+  const size_t N = c->N, K = c->K, D = c->D, rows = D * 2 * K;
+  uint32_t* coef = nullptr;
+  pool_malloc(&coef, rows * N * sizeof(uint32_t), c->stream, c->device);
+  if (c->rlk_domain == HCNN_DOMAIN_REF_NTT) {
+    k_ref_to_spectral<<<dim3(cdiv(N, 256), (unsigned)rows), 256, 0, c->stream>>>(c->d_rlk_raw, coef, (int)c->logN);
+    c->launched("k_ref_to_spectral");
+    launch_ntt_rows(c, coef, rows, (int)K, 0, 1);  // back to the coefficient domain mod q_j
+  } else {
+    CK(cudaMemcpyAsync(coef, c->d_rlk_raw, rows * N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->stream));
+  }
+  if (!c->d_rlk_rb) CK(cudaMalloc((void**)&c->d_rlk_rb, RB_A * rows * N * sizeof(uint32_t)));
+  k_rb_key_rows<<<cdiv(rows * N, 256), 256, 0, c->stream>>>(coef, c->d_rlk_rb, (int)D, (int)K, (int)N, c->d_prime,
+                                                           c->rb);
+  c->launched("k_rb_key_rows");
+  for (int a = 0; a < RB_A; ++a)
+    launch_ntt_rows(c, c->d_rlk_rb + a * rows * N, rows, 1, c->rb.roff + a, 2);
+  CK(cudaFreeAsync(coef, c->stream));
+  c->rb_keys = true;
+}
+
+template <int DD>
+void rb_mac_launch(hcnn_ctx* c, const uint32_t* ds, uint32_t* zs, size_t nct) {
+  static std::atomic<uint64_t> cfg{0};
+  per_device_once(cfg, [] {
+    cudaFuncSetAttribute(k_rb_mac<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  });
+  const size_t smem = (size_t)DD * 2 * c->K * RB_MAC_QD * sizeof(uint4);
+  const int cpc = 128;
+  k_rb_mac<DD><<<dim3(c->N / RB_MAC_C, RB_A, cdiv(nct, cpc)), RB_MAC_T, smem, c->stream>>>(
+      ds, c->d_rlk_rb, zs, (int)nct, (int)c->K, (int)c->N, cpc, c->rb);
+}
+
+void launch_rb_mac(hcnn_ctx* c, const uint32_t* ds, uint32_t* zs, size_t nct) {
+  switch (c->D) {
+#define X(DD)                            \
+  case DD:                               \
+    rb_mac_launch<DD>(c, ds, zs, nct);   \
+    break;
+    X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12)
+    X(13) X(14) X(15) X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23)
+#undef X
+    default:
+      fail(HCNN_ERR_UNSUPPORTED, "relinearisation over R: digit count");
+  }
+  c->launched("k_rb_mac");
+}
+
+// relinearisation over R: digit spectra mod r_a, multiply-accumulate with
+// the key, inverse + exact CRT to q_j + (y0, y1)
+void launch_relin_rb(hcnn_ctx* c, const uint32_t* dig, const uint32_t* y3, uint32_t* out, size_t nct) {
+  prepare_rb_keys(c);
+  const size_t N = c->N, K = c->K, D = c->D;
+  uint32_t *ds = nullptr, *zs = nullptr;
+  pool_malloc(&ds, nct * RB_A * D * N * sizeof(uint32_t), c->stream, c->device);
+  pool_malloc(&zs, nct * K * RB_A * 2 * N * sizeof(uint32_t), c->stream, c->device);
+  NttLaunch f{};
+  f.grid = dim3(RB_A, (unsigned)nct);
+  f.dig = dig;
+  f.out = ds;
+  f.D = (int)D;
+  f.reduce_digits = c->log2w >= 30 ? 1 : 0;
+  f.rb = c->rb;
+  ntt_dispatch(c, 7, f, "k_rb_fwd");
+  launch_rb_mac(c, ds, zs, nct);
+  NttLaunch b{};
+  b.grid = dim3((unsigned)K, (unsigned)nct);
+  b.a = zs;
+  b.y3 = y3;
+  b.out = out;
+  b.K = (int)K;
+  b.rb = c->rb;
+  ntt_dispatch(c, 8, b, "k_rb_inv");
+  CK(cudaFreeAsync(ds, c->stream));
+  CK(cudaFreeAsync(zs, c->stream));
+}
+
 void launch_relin(hcnn_ctx* c, const uint32_t* dig, const uint32_t* y3, uint32_t* out, size_t nct) {
+  if (rb_active(c) && c->d_rlk_raw) {
+    launch_relin_rb(c, dig, y3, out, nct);
+    return;
+  }
   prepare_keys(c);
   NttLaunch a{};
   a.rlk_mont = variant_mont(c, c->variant);
@@ -451,8 +594,6 @@ void launch_relin(hcnn_ctx* c, const uint32_t* dig, const uint32_t* y3, uint32_t
   a.reduce_digits = c->rlk_reduce ? 1 : 0;
   ntt_dispatch(c, 2, a, "k_relin");
 }
-
-unsigned cdiv(size_t a, size_t b) { return (unsigned)((a + b - 1) / b); }
 
 // bytes of workspace per ciphertext of a multiply chunk
 size_t mul_ws_per_ct(hcnn_ctx* c, bool general) {
@@ -837,11 +978,12 @@ void layout_key(hcnn_ctx* c, const uint32_t* raw, int domain, size_t rows, uint3
 }
 
 void prepare_keys(hcnn_ctx* c) {
-  if (c->keys_variant == (c->variant & ~(32 | 1024 | 2048 | 4096 | 8192))) return;
+  if (rb_active(c)) prepare_rb_keys(c);
+  if (c->keys_variant == (c->variant & ~(32 | 1024 | 2048 | 4096 | 8192 | RELIN_RBASIS))) return;
   if (c->d_rlk_raw)
     layout_key(c, c->d_rlk_raw, c->rlk_domain, (size_t)c->D * 2 * c->K, &c->d_rlk, variant_mont(c, c->variant));
   if (c->d_pk_raw) layout_key(c, c->d_pk_raw, c->pk_domain, 2 * (size_t)c->K, &c->d_pk, 0);
-  c->keys_variant = c->variant & ~(32 | 1024 | 2048 | 4096 | 8192);
+  c->keys_variant = c->variant & ~(32 | 1024 | 2048 | 4096 | 8192 | RELIN_RBASIS);
 }
 
 }  // namespace
@@ -1047,9 +1189,11 @@ int hcnn_ctx_create(hcnn_ctx** out, uint32_t n, uint32_t k, const uint64_t* prim
     c->t = t;
     c->log2w = log2w;
     // default geometry per ring degree (profiles/r1_micro_sweep.jsonl): the
-    // shuffle-tail radix-16 kernels up to 2^13, mixed-width passes at 2^14,
-    // 2-CTA cluster relinearisation at 2^15
-    c->variant = c->logN == 13 ? 8192 : c->logN == 14 ? (64 | 1024 | 4096) : c->logN == 15 ? (512 | 2048) : 0;
+    // shuffle-tail radix-16 kernels up to 2^13 (persistent square tensor and
+    // relinearisation over R at 2^13: profiles/r2/micro_rbasis.jsonl),
+    // mixed-width passes at 2^14, 2-CTA cluster relinearisation at 2^15
+    c->variant = c->logN == 13 ? (8192 | RELIN_RBASIS) : c->logN == 14 ? (64 | 1024 | 4096)
+                 : c->logN == 15 ? (512 | 2048) : 0;
     build_tables(c.get(), q, t);
     *out = c.release();
   });
@@ -1068,6 +1212,7 @@ int hcnn_ctx_destroy(hcnn_ctx* c) {
     cudaFree(c->d_ninv);
     if (c->d_rlk) cudaFree(c->d_rlk);
     if (c->d_rlk_raw) cudaFree(c->d_rlk_raw);
+    if (c->d_rlk_rb) cudaFree(c->d_rlk_rb);
     if (c->d_pk_raw) cudaFree(c->d_pk_raw);
     cudaFree(c->d_pinv);
     if (c->d_pk) cudaFree(c->d_pk);
@@ -1138,8 +1283,8 @@ int hcnn_ctx_set_option(hcnn_ctx* c, int key, int64_t value) {
       // geometry flags of the fused kernels (ntt_kernels.cuh): +16 one-row
       // relinearisation transforms, +32 square tensors on the radix-32 mixed
       // geometry, +64 mixed-width passes instead of a warp-shuffle tail
-      if (value & ~(int64_t)(16 | 32 | 64 | 512 | 1024 | 2048 | 4096 | 8192))
-        fail(HCNN_ERR_PARAM, "NTT variant flags are 16, 32, 64, 512, 1024, 2048, 4096 and 8192");
+      if (value & ~(int64_t)(16 | 32 | 64 | 512 | 1024 | 2048 | 4096 | 8192 | RELIN_RBASIS))
+        fail(HCNN_ERR_PARAM, "NTT variant flags are 16, 32, 64, 512, 1024, 2048, 4096, 8192 and 16384");
       if ((value & (32 | 64)) && c->logN < 10) fail(HCNN_ERR_UNSUPPORTED, "mixed geometries need N >= 1024");
       if ((value & 512) && c->logN != 15 && c->logN != 14)
         fail(HCNN_ERR_UNSUPPORTED, "cluster kernels are for N = 2^14 and 2^15");
@@ -1182,6 +1327,7 @@ int hcnn_set_relin_key(hcnn_ctx* c, const uint64_t* rlk, int domain) {
     upload_raw_key(c, rlk, (size_t)c->D * 2 * c->K, &c->d_rlk_raw);
     c->rlk_domain = domain;
     c->keys_variant = -1;
+    c->rb_keys = false;
     prepare_keys(c);
     // digits of w = 2^32 may exceed a prime; 2^8 / 2^16 digits never do here
     c->rlk_reduce = false;

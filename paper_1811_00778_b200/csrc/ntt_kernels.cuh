@@ -40,6 +40,8 @@ struct NttLaunch {
   const int64_t* msg;
   const uint32_t* pk;
   const uint2* delta;
+  // relinearisation over R
+  RbTabs rb;
 };
 
 template <class G>
@@ -744,6 +746,130 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
   }
 }
 
+// ------------------------------------------- relinearisation over R (RbTabs)
+// geometries with the R kernels: radix-16 shuffle tail, 256-512 threads
+template <class G>
+__host__ __device__ constexpr bool rb_geom() {
+  return G::E == 16 && !G::MIXED && G::LOGN >= 12 && G::LOGN <= 13 && G::fits(2);
+}
+
+// Step 1 of 3 (bfv.py:368-404 restated over the basis R, common.cuh).  One
+// CTA per (r_a, ct): the D digit rows of c2 through the forward NTT mod r_a,
+// two at a time (the next pair's loads issued before the current pair's
+// transform), spectra fully reduced, stored in the tiled layout.
+// dig: [B][D][N]; dspec: [B][RB_A][D][N].
+template <class G>
+__global__ void __launch_bounds__(G::T, 1)
+    k_rb_fwd(const uint32_t* __restrict__ dig, uint32_t* __restrict__ dspec, int D, int reduce_digits,
+             RbTabs rb, NttTabs nt) {
+  extern __shared__ __align__(16) uint32_t s[];
+  constexpr int E = G::E;
+  const int tid = threadIdx.x;
+  const int a = blockIdx.x;
+  const size_t ct = blockIdx.y;
+  const int jj = rb.roff + a;
+  const uint32_t p = nt.prime[jj];
+  const uint64_t mu = nt.mu[jj];
+  const uint2* tw = nt.tw + (size_t)jj * G::N;
+  const uint32_t* drow = dig + ct * D * G::N;
+  uint32_t* orow = dspec + (ct * RB_A + a) * (size_t)D * G::N;
+  uint32_t x[2 * E];
+  auto load_pair = [&](uint32_t* v, int i) {
+    load_natural<G>(v, drow + (size_t)i * G::N, tid);
+    if (i + 1 < D) load_natural<G>(v + E, drow + (size_t)(i + 1) * G::N, tid);
+  };
+  load_pair(x, 0);
+  int i = 0;
+  for (; i + 1 < D; i += 2) {
+    uint32_t nx[2 * E];
+    if (i + 2 < D) load_pair(nx, i + 2);
+    if (reduce_digits) {
+#pragma unroll
+      for (int e = 0; e < 2 * E; ++e) x[e] = reduce64(x[e], p, mu);
+    }
+    ntt_fwd<G, 2, true>(x, s, tw, p, tid);
+    store_tiled<G>(x, orow + (size_t)i * G::N, tid);
+    store_tiled<G>(x + E, orow + (size_t)(i + 1) * G::N, tid);
+#pragma unroll
+    for (int e = 0; e < 2 * E; ++e) x[e] = nx[e];
+  }
+  if (i < D) {  // odd count: one row left (its loads were issued above)
+    __syncthreads();  // the one-row exchange buffers overlap the pair's
+    if (reduce_digits) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = reduce64(x[e], p, mu);
+    }
+    ntt_fwd<G, 1, true>(x, s, tw, p, tid);
+    store_tiled<G>(x, orow + (size_t)i * G::N, tid);
+  }
+}
+
+// Step 3 of 3.  One CTA per (q_j, ct): for each r_a the pair (Z_0, Z_1) mod
+// r_a through the inverse NTT (two rows in lockstep; the next pair's loads
+// issued first) with (R/r_a)^-1 folded into its scaling, the first two
+// results parked in TMEM, then the exact centred CRT
+//   Z = sum_a x~_a (R/r_a) - v R,  v = rint(sum_a x~_a / r_a)
+// (|Z| / R < 2^-25, so an fp32 estimate decides v) reduced mod q_j with one
+// Montgomery dot product, plus (y0, y1).
+// zspec: [B][K][RB_A][2][N] tiled; y3: [B][3][K][N]; out: [B][2][K][N].
+template <class G>
+__global__ void __launch_bounds__(G::T, 1)
+    k_rb_inv(const uint32_t* __restrict__ zspec, const uint32_t* __restrict__ y3, uint32_t* __restrict__ out,
+             int K, RbTabs rb, NttTabs nt) {
+  extern __shared__ __align__(16) uint32_t s[];
+  __shared__ uint32_t tmem_slot;
+  constexpr int E = G::E;
+  static_assert(E == 16, "TMEM parking in 16-column chunks");
+  const int tid = threadIdx.x;
+  const int j = blockIdx.x;
+  const size_t ct = blockIdx.y;
+  const uint32_t* zr = zspec + (ct * K + j) * (size_t)RB_A * 2 * G::N;
+  constexpr uint32_t COLS = tmem_stash_cols<G, 4 * E>();
+  const uint32_t tbase = tmem_stash_alloc(&tmem_slot, COLS, tid, 4 * E);
+  uint32_t x[2 * E];
+  load_tiled<G>(x, zr, tid);
+  load_tiled<G>(x + E, zr + G::N, tid);
+#pragma unroll
+  for (int a = 0; a < RB_A; ++a) {
+    uint32_t nx[2 * E];
+    if (a + 1 < RB_A) {
+      load_tiled<G>(nx, zr + (size_t)(2 * a + 2) * G::N, tid);
+      load_tiled<G>(nx + E, zr + (size_t)(2 * a + 3) * G::N, tid);
+    }
+    const int jj = rb.roff + a;
+    ntt_inv<G, 2>(x, s, nt.itw + (size_t)jj * G::N, nt.prime[jj], InvScale{rb.isc_n[a], rb.isc_nw[a]}, tid);
+    if (a + 1 < RB_A) {
+      tmem_st16(tbase + (uint32_t)(2 * a) * E, x);
+      tmem_st16(tbase + (uint32_t)(2 * a + 1) * E, x + E);
+#pragma unroll
+      for (int e = 0; e < 2 * E; ++e) x[e] = nx[e];
+    }
+  }
+  const uint32_t q = nt.prime[j];
+  const uint32_t qinv = nt.pinv[j];
+  const uint32_t c0 = rb.crt_q[j][0], c1 = rb.crt_q[j][1], c2 = rb.crt_q[j][2];
+  const uint32_t cR = rb.negR_q[j];
+#pragma unroll
+  for (int part = 0; part < 2; ++part) {
+    uint32_t z0[E], z1[E];
+    tmem_ld16(tbase + (uint32_t)part * E, z0);
+    tmem_ld16(tbase + (uint32_t)(2 + part) * E, z1);
+    const uint32_t* yr = y3 + ((ct * 3 + part) * K + j) * G::N;
+    uint32_t* o = out + ((ct * 2 + part) * K + j) * G::N;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t x2 = x[part * E + e];
+      const float f = __fmaf_rn((float)z0[e], rb.rinv[0],
+                                __fmaf_rn((float)z1[e], rb.rinv[1], (float)x2 * rb.rinv[2]));
+      const uint32_t v = (uint32_t)__float2int_rn(f);
+      const uint64_t acc = (uint64_t)z0[e] * c0 + (uint64_t)z1[e] * c1 + (uint64_t)x2 * c2 + (uint64_t)v * cR;
+      const int idx = natural_index<G>(tid, e);
+      o[idx] = add_mod(redc(acc, q, qinv), yr[idx], q);
+    }
+  }
+  tmem_stash_free(tmem_slot, COLS, tid);
+}
+
 // Public-key encryption from host-drawn randomness (bfv.py:201-216).  One CTA
 // per (ct, prime of q): c0 = INTT(b * NTT(u)) + e1 + Delta m, c1 = INTT(a *
 // NTT(u)) + e2.  u: [P][N] in {0,1}; e1, e2: [P][N] small signed; msg: [P][N]
@@ -854,6 +980,12 @@ void configure_smem() {
   cudaFuncSetAttribute(k_relin<G, relin_acc64<G>(true), 1>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, RelinSmem<G, 1>::BYTES);
   cudaFuncSetAttribute(k_encrypt<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if constexpr (rb_geom<G>()) {
+    cudaFuncSetAttribute(k_rb_fwd<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         G::ntt_smem_words(2) * sizeof(uint32_t));
+    cudaFuncSetAttribute(k_rb_inv<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         G::ntt_smem_words(2) * sizeof(uint32_t));
+  }
   cudaFuncSetAttribute(k_mul_plain<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        G::ntt_smem_words(pair_nr<G>()) * sizeof(uint32_t));
 }
@@ -953,6 +1085,19 @@ cudaError_t launch_with(int op, const NttLaunch& a) {
     case 6:
       k_mul_plain<G><<<a.grid, G::T, G::ntt_smem_words(pair_nr<G>()) * sizeof(uint32_t), a.stream>>>(
           a.a, a.b, a.out, a.K, a.nt);
+      break;
+    case 7:  // relinearisation over R, step 1: digit spectra mod r_a
+    case 8:  // step 3: inverse mod r_a, exact CRT to q_j, + (y0, y1)
+      if constexpr (rb_geom<G>()) {
+        if (op == 7)
+          k_rb_fwd<G><<<a.grid, G::T, G::ntt_smem_words(2) * sizeof(uint32_t), a.stream>>>(
+              a.dig, a.out, a.D, a.reduce_digits, a.rb, a.nt);
+        else
+          k_rb_inv<G><<<a.grid, G::T, G::ntt_smem_words(2) * sizeof(uint32_t), a.stream>>>(
+              a.a, a.y3, a.out, a.K, a.rb, a.nt);
+      } else {
+        return cudaErrorInvalidValue;
+      }
       break;
     default:
       return cudaErrorInvalidValue;

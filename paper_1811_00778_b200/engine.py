@@ -148,7 +148,8 @@ class GpuContext:
         relinearisation, 32 radix-32 square tensor, 64 mixed-width passes, 512
         2-CTA cluster rows at 2^15, 1024 relinearisation sums in TMEM, 2048 /
         4096 square tensor with rows parked in TMEM, 8192 persistent square
-        tensor with TMA prefetch)."""
+        tensor with TMA prefetch, 16384 relinearisation over the shared
+        three-prime basis R)."""
         _lib.check(_lib.lib().hcnn_ctx_set_option(self.handle, 1, int(variant)), "ntt variant")
 
     def variant(self) -> int:
