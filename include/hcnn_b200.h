@@ -75,7 +75,10 @@ enum {
  * CRT back; N = 2^12 and 2^13, at most 23 digits).  Default per N:
  * 8192|16384 at 2^13, 64|1024|4096 at 2^14, 512|2048 at 2^15, 0 otherwise.
  * Results are identical for every setting. */
-enum { HCNN_OPT_NTT_VARIANT = 1 };
+/* HCNN_OPT_TS_CHUNK: ciphertexts per extend/tensor/scale sub-chunk of a
+ * multiply (the tensor's output of one sub-chunk stays in L2 for the scale
+ * kernel); 0 = the whole chunk at once. */
+enum { HCNN_OPT_NTT_VARIANT = 1, HCNN_OPT_TS_CHUNK = 2 };
 int hcnn_ctx_set_option(hcnn_ctx* ctx, int key, int64_t value);
 int64_t hcnn_ctx_query(hcnn_ctx* ctx, int what);
 /* psi (primitive 2N-th root) of prime i, i < K + KP (ntt.py:50-60) */
@@ -189,6 +192,14 @@ int hcnn_ntt(hcnn_ctx* ctx, uint32_t* rows, size_t n_rows, uint32_t limbs, uint3
  * outside [0, 2^32).  This is what engine.upload / eval_network do to a
  * host CipherTensor before it crosses PCIe (engine.py:42-58 objects in). */
 int hcnn_host_narrow(const int64_t* const* src, size_t count, size_t len, uint32_t* dst, int threads);
+
+/* The way back (no device work): dst[i][j] = src[i * len + j] for count HOST
+ * int64 arrays of len residues (the caller's freshly allocated
+ * RingElem.residues) from one HOST u32 buffer (normally the pinned download
+ * of a result tensor), split over `threads` host threads (<= 0: all cores).
+ * What engine.eval_network does to hand a host CipherTensor back
+ * (engine.py:42-58 objects out). */
+int hcnn_host_widen(const uint32_t* src, size_t count, size_t len, int64_t* const* dst, int threads);
 
 /* Return the library pool's free memory on `device` to the driver (the pool
  * keeps freed blocks across synchronisations otherwise).  Synchronises the

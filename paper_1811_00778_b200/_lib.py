@@ -60,6 +60,7 @@ _SIGS = {
     "hcnn_crt_combine": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_size_t, C.c_void_p, C.c_int, C.c_void_p,
                                     C.c_int, C.c_void_p]),
     "hcnn_host_narrow": (C.c_int, [C.c_void_p, C.c_size_t, C.c_size_t, C.c_void_p, C.c_int]),
+    "hcnn_host_widen": (C.c_int, [C.c_void_p, C.c_size_t, C.c_size_t, C.c_void_p, C.c_int]),
     "hcnn_profile": (C.c_int, [C.c_void_p, C.c_int]),
     "hcnn_profile_dump": (C.c_int64, [C.c_void_p, C.c_char_p, C.c_size_t]),
     "hcnn_int_peak": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_double)]),

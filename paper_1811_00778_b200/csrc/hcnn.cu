@@ -5,6 +5,10 @@
 #include <memory>
 #include <mutex>
 #include <thread>
+#include <condition_variable>
+#include <functional>
+
+#include <immintrin.h>
 #include <string>
 #include <vector>
 
@@ -137,6 +141,7 @@ struct hcnn_ctx {
   uint8_t* ws = nullptr;
   size_t ws_bytes = 0;
   size_t ws_limit = size_t(6) << 30;  // whole MNIST layers (800 cts at set 1) in one chunk
+  size_t ts_sub = 0;  // ciphertexts per extend/tensor/scale sub-chunk (0: whole chunk)
   int64_t launches = 0;
   cudaEvent_t switch_ev = nullptr;  // orders the old stream before the new one (hcnn_ctx_set_stream)
 
@@ -556,7 +561,11 @@ void launch_relin_rb(hcnn_ctx* c, const uint32_t* dig, const uint32_t* y3, uint3
   pool_malloc(&ds, nct * RB_A * D * N * sizeof(uint32_t), c->stream, c->device);
   pool_malloc(&zs, nct * K * RB_A * 2 * N * sizeof(uint32_t), c->stream, c->device);
   NttLaunch f{};
-  f.grid = dim3(RB_A, (unsigned)nct);
+  // digits split over up to 4 CTAs per (r_a, ct) when the batch alone would
+  // give fewer than 6 waves of one CTA per SM
+  unsigned split = 1;
+  while (split < 4 && (size_t)RB_A * nct * split < 6 * 148) split *= 2;
+  f.grid = dim3(RB_A, (unsigned)nct, split);
   f.dig = dig;
   f.out = ds;
   f.D = (int)D;
@@ -680,7 +689,14 @@ void multiply(hcnn_ctx* c, const uint32_t* a, const uint32_t* b, size_t n, uint3
     const uint32_t* bc = b + s * 2 * K * N;
     uint32_t* y3 = out3 ? out3 + s * 3 * K * N : (uint32_t*)(ws + ext_bytes * ch);
     uint32_t* dig = out2 ? (uint32_t*)(ws + ext_bytes * ch + 3 * K * N * sizeof(uint32_t) * ch) : nullptr;
-    mul_chunk(c, ac, general ? bc : ac, m, y3, dig, ws);
+    // extend / tensor / scale in sub-chunks whose tensor output can stay in
+    // L2 for k_scale (ts_sub; 0 = the whole chunk at once)
+    const size_t sub = (c->ts_sub && c->ts_sub < m) ? c->ts_sub : m;
+    for (size_t u = 0; u < m; u += sub) {
+      const size_t mu = (m - u < sub) ? m - u : sub;
+      mul_chunk(c, ac + u * 2 * K * N, (general ? bc : ac) + u * 2 * K * N, mu, y3 + u * 3 * K * N,
+                dig ? dig + u * c->D * N : nullptr, ws);
+    }
     if (out2) launch_relin(c, dig, y3, out2 + s * 2 * K * N, m);
   }
 }
@@ -995,8 +1011,96 @@ const char* hcnn_last_error(void) { return g_err.c_str(); }
 namespace {
 // one thread's share of hcnn_host_narrow; returns the OR of all inputs' high
 // words (non-zero: a value outside [0, 2^32))
+// Persistent host worker threads for the drop-in staging (hcnn_host_narrow
+// runs once per row band; spawning its threads every call cost ~0.3 ms).
+// run(n, fn) calls fn(k) for k in [0, n), k = 0 on the caller; one job at a
+// time.  The pool is never destroyed (its idle threads wait on a condition).
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool* p = new HostPool;
+    return *p;
+  }
+  void run(size_t n, const std::function<void(size_t)>& fn) {
+    std::lock_guard<std::mutex> one(run_m_);
+    {
+      std::lock_guard<std::mutex> g(m_);
+      while (nthreads_ + 1 < n) {
+        const size_t id = ++nthreads_;
+        std::thread([this, id] { loop(id); }).detach();
+      }
+      fn_ = &fn;
+      jobs_ = n - 1;
+      pending_ = n - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    fn(0);
+    std::unique_lock<std::mutex> l(m_);
+    done_.wait(l, [&] { return pending_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  void loop(size_t id) {
+    uint64_t seen = 0;
+    std::unique_lock<std::mutex> l(m_);
+    for (;;) {
+      cv_.wait(l, [&] { return gen_ != seen; });
+      seen = gen_;
+      if (id > jobs_) continue;
+      const std::function<void(size_t)>* f = fn_;
+      l.unlock();
+      (*f)(id);
+      l.lock();
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::mutex run_m_, m_;
+  std::condition_variable cv_, done_;
+  const std::function<void(size_t)>* fn_ = nullptr;
+  size_t nthreads_ = 0, jobs_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+};
+
+// AVX2 with streaming stores: the pinned destination is written without
+// being read first (a plain store reads each line for ownership, a third of
+// the host memory traffic of the narrowing, which is memory-bound while the
+// uploads run)
+__attribute__((target("avx2"))) uint64_t narrow_rows_avx2(const int64_t* const* src, size_t a, size_t b,
+                                                          size_t len, uint32_t* dst) {
+  const __m256i perm = _mm256_setr_epi32(0, 2, 4, 6, 1, 3, 5, 7);
+  __m256i hiv = _mm256_setzero_si256();
+  uint64_t hi = 0;
+  for (size_t i = a; i < b; ++i) {
+    const int64_t* s = src[i];
+    uint32_t* d = dst + i * len;
+    size_t j = 0;
+    if ((reinterpret_cast<uintptr_t>(d) & 31) == 0) {
+      for (; j + 8 <= len; j += 8) {
+        const __m256i x = _mm256_permutevar8x32_epi32(_mm256_loadu_si256((const __m256i*)(s + j)), perm);
+        const __m256i y = _mm256_permutevar8x32_epi32(_mm256_loadu_si256((const __m256i*)(s + j + 4)), perm);
+        _mm256_stream_si256((__m256i*)(d + j), _mm256_permute2x128_si256(x, y, 0x20));
+        hiv = _mm256_or_si256(hiv, _mm256_permute2x128_si256(x, y, 0x31));
+      }
+    }
+    for (; j < len; ++j) {
+      const uint64_t v = (uint64_t)s[j];
+      hi |= v >> 32;
+      d[j] = (uint32_t)v;
+    }
+  }
+  _mm_sfence();
+  alignas(32) uint32_t h8[8];
+  _mm256_store_si256((__m256i*)h8, hiv);
+  for (int k = 0; k < 8; ++k) hi |= h8[k];
+  return hi;
+}
+
 __attribute__((optimize("O3"))) uint64_t narrow_rows(const int64_t* const* src, size_t a, size_t b,
                                                       size_t len, uint32_t* dst) {
+  static const bool avx2 = __builtin_cpu_supports("avx2");
+  if (avx2) return narrow_rows_avx2(src, a, b, len, dst);
   uint64_t hi = 0;
   for (size_t i = a; i < b; ++i) {
     const uint64_t* __restrict__ s = reinterpret_cast<const uint64_t*>(src[i]);
@@ -1022,13 +1126,28 @@ int hcnn_host_narrow(const int64_t* const* src, size_t count, size_t len, uint32
     if (nt > 64) nt = 64;
     if (nt > count) nt = count;
     std::vector<uint64_t> bad(nt, 0);
-    std::vector<std::thread> pool;
-    for (size_t k = 1; k < nt; ++k)
-      pool.emplace_back([&, k] { bad[k] = narrow_rows(src, count * k / nt, count * (k + 1) / nt, len, dst); });
-    bad[0] = narrow_rows(src, 0, count / nt, len, dst);
-    for (auto& t : pool) t.join();
+    HostPool::get().run(nt, [&](size_t k) { bad[k] = narrow_rows(src, count * k / nt, count * (k + 1) / nt, len, dst); });
     for (uint64_t b : bad)
       if (b) fail(HCNN_ERR_PARAM, "residue outside [0, 2^32): not a canonical RNS residue");
+  });
+}
+
+int hcnn_host_widen(const uint32_t* src, size_t count, size_t len, int64_t* const* dst, int threads) {
+  return guarded([&] {
+    if (!count || !len) return;
+    if (!src || !dst) fail(HCNN_ERR_PARAM, "null argument");
+    for (size_t i = 0; i < count; ++i)
+      if (!dst[i]) fail(HCNN_ERR_PARAM, "null destination array");
+    size_t nt = threads > 0 ? (size_t)threads : (size_t)std::thread::hardware_concurrency();
+    nt = nt < 1 ? 1 : nt > 64 ? 64 : nt;
+    if (nt > count) nt = count;
+    HostPool::get().run(nt, [&](size_t k) {
+      for (size_t i = count * k / nt; i < count * (k + 1) / nt; ++i) {
+        const uint32_t* __restrict__ s = src + i * len;
+        int64_t* __restrict__ d = dst[i];
+        for (size_t j = 0; j < len; ++j) d[j] = (int64_t)s[j];
+      }
+    });
   });
 }
 
@@ -1289,6 +1408,9 @@ int hcnn_ctx_set_option(hcnn_ctx* c, int key, int64_t value) {
       if ((value & 512) && c->logN != 15 && c->logN != 14)
         fail(HCNN_ERR_UNSUPPORTED, "cluster kernels are for N = 2^14 and 2^15");
       c->variant = (int)value;
+    } else if (key == HCNN_OPT_TS_CHUNK) {
+      if (value < 0) fail(HCNN_ERR_PARAM, "sub-chunk size must be >= 0");
+      c->ts_sub = (size_t)value;
     } else {
       fail(HCNN_ERR_PARAM, "unknown option");
     }

@@ -773,16 +773,22 @@ __global__ void __launch_bounds__(G::T, 1)
   const uint2* tw = nt.tw + (size_t)jj * G::N;
   const uint32_t* drow = dig + ct * D * G::N;
   uint32_t* orow = dspec + (ct * RB_A + a) * (size_t)D * G::N;
+  // digits [i0, i1) of this CTA (blockIdx.z: an even-sized share, so that
+  // small batches still fill the SMs)
+  const int share = ((D + gridDim.z - 1) / gridDim.z + 1) & ~1;
+  const int i0 = blockIdx.z * share;
+  const int i1 = min(D, i0 + share);
+  if (i0 >= i1) return;
   uint32_t x[2 * E];
   auto load_pair = [&](uint32_t* v, int i) {
     load_natural<G>(v, drow + (size_t)i * G::N, tid);
-    if (i + 1 < D) load_natural<G>(v + E, drow + (size_t)(i + 1) * G::N, tid);
+    if (i + 1 < i1) load_natural<G>(v + E, drow + (size_t)(i + 1) * G::N, tid);
   };
-  load_pair(x, 0);
-  int i = 0;
-  for (; i + 1 < D; i += 2) {
+  load_pair(x, i0);
+  int i = i0;
+  for (; i + 1 < i1; i += 2) {
     uint32_t nx[2 * E];
-    if (i + 2 < D) load_pair(nx, i + 2);
+    if (i + 2 < i1) load_pair(nx, i + 2);
     if (reduce_digits) {
 #pragma unroll
       for (int e = 0; e < 2 * E; ++e) x[e] = reduce64(x[e], p, mu);
@@ -793,7 +799,7 @@ __global__ void __launch_bounds__(G::T, 1)
 #pragma unroll
     for (int e = 0; e < 2 * E; ++e) x[e] = nx[e];
   }
-  if (i < D) {  // odd count: one row left (its loads were issued above)
+  if (i < i1) {  // odd count: one row left (its loads were issued above)
     __syncthreads();  // the one-row exchange buffers overlap the pair's
     if (reduce_digits) {
 #pragma unroll

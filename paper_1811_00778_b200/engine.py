@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import hashlib
 import os
+import time
 import threading
 import weakref
 from dataclasses import dataclass
@@ -128,6 +129,9 @@ class GpuContext:
         variant = os.environ.get("HCNN_NTT_VARIANT")
         if variant is not None and self.N >= 1024:
             _lib.check(L.hcnn_ctx_set_option(h, 1, int(variant)), "hcnn_ctx_set_option")
+        ts = os.environ.get("HCNN_TS_CHUNK")
+        if ts is not None:
+            _lib.check(L.hcnn_ctx_set_option(h, 2, int(ts)), "hcnn_ctx_set_option")
         self._rlk_ref = None
         self._weights = {}
         self._finalizer = weakref.finalize(self, L.hcnn_ctx_destroy, h)
@@ -302,7 +306,7 @@ class GpuCipherTensor:
     @property
     def cts(self) -> list:
         if self._cts is None:
-            self._cts = _to_host_cts(self.residues(), self.params, self.host_types)
+            self._cts = _download_cts(self)
         return self._cts
 
     def at(self, y: int, x: int, ch: int):
@@ -323,19 +327,34 @@ def _host_types_of(tensor, params):
     return (type(tensor), None, None, None, params.ctx)
 
 
-def _to_host_cts(res: np.ndarray, params, host_types) -> list:
+def _download_cts(t: "GpuCipherTensor") -> list:
+    """Device tensor -> host Ciphertext objects: one download into a reused
+    pinned u32 buffer, then the residues widened to int64 straight into the
+    objects' fresh arrays by host threads (hcnn_host_widen); single-threaded
+    numpy casts of the result ran at ~4 GB/s on the GPU host."""
+    n = t.data.shape[0]
+    if n == 0:
+        return []
+    g = context_for(t.params, t.data.device)
+    parts, K, N = t.data.shape[1:]
+    pin = _stager(g).out(n * parts * K * N)
+    stream = torch.cuda.current_stream(t.data.device)
+    pin.copy_(t.data.reshape(-1), non_blocking=True)
+    stream.synchronize()
+    arrays = [np.empty((K, N), dtype=np.int64) for _ in range(n * parts)]
+    ptrs = np.array([a.ctypes.data for a in arrays], dtype=np.uintp)
+    _lib.check(_lib.lib().hcnn_host_widen(_lib.C.c_void_p(pin.data_ptr()), n * parts, K * N, ptrs.ctypes.data,
+                                          min(16, os.cpu_count() or 1)), "hcnn_host_widen")
+    host_types = t.host_types
     if host_types and host_types[1] is not None:
         _, ct_cls, el_cls, dom, ctx = host_types
     else:
         from . import bfv as _b
 
-        ct_cls, el_cls, dom, ctx = _b.Ciphertext, _b.RingElem, _b.Domain.COEFF, params.ctx
-    res = res.astype(np.int64)
-    out = []
-    for i in range(res.shape[0]):
-        parts = tuple(el_cls(ctx, np.ascontiguousarray(res[i, p]), dom) for p in range(res.shape[1]))
-        out.append(ct_cls(parts=parts, fingerprint=params.fingerprint))
-    return out
+        ct_cls, el_cls, dom, ctx = _b.Ciphertext, _b.RingElem, _b.Domain.COEFF, t.params.ctx
+    fp = t.params.fingerprint
+    return [ct_cls(parts=tuple(el_cls(ctx, arrays[i * parts + p], dom) for p in range(parts)), fingerprint=fp)
+            for i in range(n)]
 
 
 class _HostStager:
@@ -360,6 +379,13 @@ class _HostStager:
             cls._pool = concurrent.futures.ThreadPoolExecutor(
                 max_workers=max(1, min(16, os.cpu_count() or 1)), thread_name_prefix="hcnn-stage")
         return cls._pool
+
+    def out(self, words: int) -> torch.Tensor:
+        """reused pinned int32 buffer of at least `words` words (downloads)"""
+        ob = getattr(self, "obuf", None)
+        if ob is None or ob.numel() < words:
+            ob = self.obuf = torch.empty(max(words, 1 << 20), dtype=torch.int32, pin_memory=True)
+        return ob[:words]
 
     def get(self, n: int, K: int, N: int) -> torch.Tensor:
         if self.buf is None or self.buf.shape[0] < n or tuple(self.buf.shape[1:]) != (2, K, N):
@@ -605,7 +631,7 @@ def eval_network(tensor, model, rlk, params, counter=None, workers: int = 1, cap
     return _ret(x, was_host)
 
 
-def _eval_network_host(tensor, model, rlk, params, counter, capacity=None, layer_hook=None, bands: int = 6):
+def _eval_network_host(tensor, model, rlk, params, counter, capacity=None, layer_hook=None, bands: int = 12):
     """eval_network of a host CipherTensor (the reference's own objects): its
     int64 residues are narrowed into a reused pinned buffer by row bands, each
     band is uploaded on a copy stream as soon as it is filled, and the leading
@@ -747,6 +773,9 @@ class _Stage:
         return True
 
 
+_BAND_TRACE = None  # list: (ciphertexts uploaded, host time, upload event, compute event) per band
+
+
 def _banded_head(hb, buf, shape, delta, model, rlk, params, counter, up_stream, compute, bands, layer_hook,
                  prepare=None, host_types=None):
     """The network's leading row-local layers (unpadded convolutions, squares,
@@ -797,6 +826,12 @@ def _banded_head(hb, buf, shape, delta, model, rlk, params, counter, up_stream, 
         for st in stages:
             st.run(g, src, rows)
             src, rows = st.out, st.done
+        if _BAND_TRACE is not None:  # tools/dropin_probe.py: per-band upload / compute completion
+            done = torch.cuda.Event(enable_timing=True)
+            done.record(compute)
+            up = torch.cuda.Event(enable_timing=True)
+            up.record(up_stream)
+            _BAND_TRACE.append((hi * row, time.perf_counter(), up, done))
     released = torch.cuda.Event()
     released.record(compute)
     # counters, scales and hooks layer by layer, as the reference's loop has them

@@ -266,4 +266,31 @@ def test_host_narrow_is_exact_and_rejects_out_of_range():
     dst = np.zeros((11, 3, 257), dtype=np.uint32)
     with pytest.raises(ParameterMismatchError):
         _lib.check(_lib.lib().hcnn_host_narrow(ptrs.ctypes.data, 11, 3 * 257, dst.ctypes.data, 4))
+    # 32-byte aligned rows of a multiple of 8 words: the vector (streaming
+    # store) path, including a high word set inside its body
+    big = [rng.integers(0, 1 << 32, (4, 1024)).astype(np.int64) for _ in range(5)]
+    bp = np.array([a.ctypes.data for a in big], dtype=np.uintp)
+    raw = np.zeros(5 * 4096 + 8, dtype=np.uint32)
+    off = ((32 - raw.ctypes.data % 32) % 32) // 4
+    out = raw[off:off + 5 * 4096]
+    _lib.check(_lib.lib().hcnn_host_narrow(bp.ctypes.data, 5, 4096, out.ctypes.data, 2))
+    assert np.array_equal(out.reshape(5, 4, 1024).astype(np.int64), np.stack(big))
+    big[3][1, 17] = 1 << 32
+    with pytest.raises(ParameterMismatchError):
+        _lib.check(_lib.lib().hcnn_host_narrow(bp.ctypes.data, 5, 4096, out.ctypes.data, 2))
     _ = ctypes
+
+
+def test_host_widen_is_exact():
+    """hcnn_host_widen (host-only): one u32 buffer -> count int64 arrays (the
+    drop-in's result objects), every thread count."""
+    from paper_1811_00778_b200 import _lib
+
+    rng = np.random.default_rng(4)
+    src = rng.integers(0, 1 << 32, (7, 2 * 257), dtype=np.uint64).astype(np.uint32)
+    for threads in (1, 3, 0, 64):
+        dst = [np.full((2, 257), -1, dtype=np.int64) for _ in range(7)]
+        ptrs = np.array([a.ctypes.data for a in dst], dtype=np.uintp)
+        _lib.check(_lib.lib().hcnn_host_widen(src.ctypes.data, 7, 2 * 257, ptrs.ctypes.data, threads))
+        assert np.array_equal(np.stack(dst).reshape(7, -1), src.astype(np.int64))
+
