@@ -194,6 +194,10 @@ def ntt_butterflies(name: str, K: int, KP: int, D: int, N: int, cts: float):
         return (K + KP) * 5 * bfly * cts
     if name == "k_relin":
         return K * (D + 2) * bfly * cts
+    if name == "k_rb_fwd":  # D digit transforms mod each of the 3 primes of R
+        return 3 * D * bfly * cts
+    if name == "k_rb_inv":  # 2 parts x 3 primes of R inverse transforms per q_j
+        return 6 * K * bfly * cts
     return None
 
 
@@ -247,6 +251,18 @@ def kernel_work(name: str, K: int, KP: int, D: int, N: int, cts: float):
     elif name == "k_extend":  # per part: K Shoup, fixed point, KP x (K MAC + REDC)
         slots = 2 * N * (K * 4 + K * 2 + KP * (K * 2 + 3))
         byts = 4 * N * 2 * (K + KP)
+        fixed = 0
+    elif name == "k_rb_fwd":  # relinearisation over R: D forward NTTs mod 3 primes
+        slots = 3 * D * bfly * 4
+        byts = 4 * N * (D + 3 * D)
+        fixed = 0
+    elif name == "k_rb_mac":  # 3 x 2K x D lazy 64-bit MACs per coefficient, a fold per output
+        slots = 3 * 2 * K * N * (D * 2 + 7)
+        byts = 4 * N * (3 * D + 6 * K)
+        fixed = 4 * N * 3 * D * 2 * K
+    elif name == "k_rb_inv":  # 6 inverse NTTs per q_j, CRT (4 MACs + REDC) per output
+        slots = K * (6 * bfly * 4 + 2 * N * 12)
+        byts = 4 * N * (6 * K + 2 * K + 2 * K)
         fixed = 0
     else:
         return None
@@ -547,6 +563,19 @@ def run_ours(args):
             kernels[name]["imad_slot_frac"] = round(wk[1] / avg_s / 1e12 / imad_peak, 4)
         if mm:
             kernels[name]["s8d_frac"] = round(3 * mm / avg_s / 1e12 / imad_peak, 4)
+    # the relinearisation over R as one stage (its three kernels) against the
+    # 8(d) relinearisation work of the reference algorithm
+    rb = [n for n in ("k_rb_fwd", "k_rb_mac", "k_rb_inv") if n in prof]
+    if len(rb) == 3:
+        cnt = prof["k_rb_fwd"][0]
+        tot = sum(prof[n][1] for n in rb)
+        mm = s8d_modmuls("k_relin", g0.K, g0.KP, g0.D, g0.N, n_sq / cnt)
+        avg_s = tot / cnt / 1e3
+        kernels["relin_rbasis"] = {"kernels": rb, "launches": cnt, "ms_total": round(tot, 4),
+                                   "share": round(tot / total_ms, 4),
+                                   "s8d_frac": round(3 * mm / avg_s / 1e12 / imad_peak, 4),
+                                   "note": "8(d) relinearisation work (D K + 2K NTTs, 2 D K N MACs) over the "
+                                           "three kernels' time"}
     images = W["images_per_step"]
     value = images / (ms / 1e3)
     in_bytes = int(sum(h.numel() for h in host_in) * 4)

@@ -56,7 +56,11 @@ def main():
     ap.add_argument("--variants", default="default",
                     help="comma list of hcnn_ctx_set_option NTT flags; 'default' = the library's per-N choice")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--ntt64", action="store_true",
+                    help="u64 NTT rows (62-bit primes, hcnn_ntt64) instead of the u32 sweep")
     a = ap.parse_args()
+    if a.ntt64:
+        return ntt64_rows(a)
     t = 5522259017729
     for n in [int(x) for x in a.ns.split(",")]:
         for k in [int(x) for x in a.ks.split(",")]:
@@ -109,6 +113,54 @@ def main():
                 line["hsquare_us_per_ct"] = round(hsq, 3)
                 line["hsquare_bfly_gs"] = round((5 * (k + g.KP) + (g.D + 2) * k) * bfly / (hsq * 1e-6) / 1e9, 1)
                 print(json.dumps(line), flush=True)
+
+
+def ntt64_rows(a):
+    """u64 NTT rows over a 62-bit prime = 1 mod 2N (hcnn_ntt64): forward and
+    inverse time per row, butterflies/s, and the fraction of the measured u64
+    Harvey butterfly rate (hcnn_int_peak kind 16)."""
+    import ctypes
+
+    import torch
+
+    from paper_1811_00778_b200 import _lib
+    from paper_1811_00778_b200.bfv import is_prime
+
+    L = _lib.lib()
+    peak = ctypes.c_double()
+    _lib.check(L.hcnn_int_peak(0, 16, ctypes.byref(peak)))
+    for n in [int(x) for x in a.ns.split(",")]:
+        k = ((1 << 62) - 1) // (2 * n)
+        while not is_prime(k * 2 * n + 1):
+            k -= 1
+        p = k * 2 * n + 1
+        h = ctypes.c_void_p()
+        _lib.check(L.hcnn_codec_create(p, n, 0, ctypes.byref(h)))
+        rng = np.random.default_rng(n)
+        x = torch.from_numpy(rng.integers(0, p, (a.rows, n), dtype=np.uint64).view(np.int64)).cuda()
+        st = torch.cuda.current_stream()
+        line = {"kernel": "k_ntt64", "n": n, "prime_bits": p.bit_length(), "rows": a.rows,
+                "u64_bfly_peak_gs": round(peak.value / 1e9, 1)}
+        for inv in (0, 1):
+            call = lambda: _lib.check(L.hcnn_ntt64(h, ctypes.c_void_p(x.data_ptr()), a.rows, inv,
+                                                   ctypes.c_void_p(st.cuda_stream)))
+            for _ in range(2):
+                call()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(a.reps):
+                call()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / a.reps
+            bf = a.rows * (n // 2) * (n.bit_length() - 1)
+            tag = "inv" if inv else "fwd"
+            line[tag + "_row_us"] = round(ms * 1e3 / a.rows, 4)
+            line[tag + "_gbfly_s"] = round(bf / (ms * 1e-3) / 1e9, 1)
+            line[tag + "_bfly_frac"] = round(bf / (ms * 1e-3) / peak.value, 4)
+            line[tag + "_hbm_gbs"] = round(a.rows * n * 16 / (ms * 1e-3) / 1e9, 1)
+        L.hcnn_codec_destroy(h)
+        print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

@@ -119,6 +119,13 @@ int hcnn_codec_create(uint64_t t, uint32_t n, int device, hcnn_codec** out);
 int hcnn_codec_destroy(hcnn_codec* codec);
 int hcnn_codec_encode(hcnn_codec* codec, const uint64_t* slots, uint64_t* polys, size_t rows, void* stream);
 int hcnn_codec_decode(hcnn_codec* codec, const uint64_t* polys, uint64_t* slots, size_t rows, void* stream);
+/* The u64 negacyclic NTT itself (ntt.py:113-154 for primes up to 62 bits;
+ * replaces transform_rows on wide primes), in place on n_rows device rows of
+ * N u64 over the codec's prime: forward (inverse = 0) natural order in,
+ * bit-reversed positions out (out[i] = a(zeta^(2 brv(i) + 1))); inverse = 1
+ * the way back.  Canonical residues in and out.  One CTA per row up to 2^14,
+ * a 2-CTA cluster at 2^15. */
+int hcnn_ntt64(hcnn_codec* codec, uint64_t* rows, size_t n_rows, int inverse, void* stream);
 
 /* Device memory helpers (stream-ordered). */
 int hcnn_alloc(hcnn_ctx* ctx, size_t bytes, void** out);
@@ -228,7 +235,9 @@ int hcnn_profile(hcnn_ctx* ctx, int enable);
 int64_t hcnn_profile_dump(hcnn_ctx* ctx, char* buf, size_t len);
 
 /* Integer-pipe probe (roofline denominator): kind 0 = 32-bit IMAD,
- * 1 = IMAD.HI (umulhi), 2 = IMAD.WIDE (32x32->64); ops per second. */
+ * 1 = IMAD.HI (umulhi), 2 = IMAD.WIDE (32x32->64), 8 = register-resident
+ * Harvey butterflies on u32 residues (the NTT kernels' attainable rate),
+ * 16 = the same on 62-bit u64 residues (the u64 NTT's); ops per second. */
 int hcnn_int_peak(int device, int kind, double* ops_per_s);
 
 const char* hcnn_last_error(void);

@@ -167,6 +167,38 @@ def ntt_inverse(ctx: Context, res: np.ndarray) -> np.ndarray:
     return a * ctx.untwist % ctx.mods
 
 
+def _wide_tables(p: int, n: int):
+    psi = primitive_2n_root(p, n)
+    fwd, inv = [], []
+    half = n // 2
+    while half >= 1:
+        for sign, tabs in ((1, fwd), (-1, inv)):
+            w = pow(psi * psi % p, sign * (n // (2 * half)), p)
+            tabs.append((half, np.array([[pow(w, j, p) for j in range(half)]], dtype=object)))
+        half //= 2
+    twist = np.array([pow(psi, j, p) for j in range(n)], dtype=object)
+    untwist = np.array([pow(psi, -j, p) * pow(n, -1, p) % p for j in range(n)], dtype=object)
+    return fwd, inv, twist, untwist
+
+
+def ntt_forward_wide(p: int, n: int, res) -> np.ndarray:
+    """ntt_forward for one prime of up to 62 bits in Python ints (ring.py:45-46
+    admits such primes; ring.py:147-154 / ntt.py:113-154 transform them):
+    out[k] = a(psi^(2k+1)), natural order.  res: [rows][n] ints."""
+    fwd, _, twist, _ = _wide_tables(p, n)
+    mods = np.full((1, 1), p, dtype=object)
+    rows = [np.array([[int(v) for v in r]], dtype=object) * twist % p for r in np.atleast_2d(res)]
+    return np.concatenate([_cyclic_dif(a, mods, fwd)[:, bitrev_perm(n)] for a in rows])
+
+
+def ntt_inverse_wide(p: int, n: int, res) -> np.ndarray:
+    """Inverse of ntt_forward_wide (ring.py:156-163)."""
+    _, inv, _, untwist = _wide_tables(p, n)
+    mods = np.full((1, 1), p, dtype=object)
+    rows = [np.array([[int(v) for v in r]], dtype=object) for r in np.atleast_2d(res)]
+    return np.concatenate([_cyclic_dif(a, mods, inv)[:, bitrev_perm(n)] * untwist % p for a in rows])
+
+
 # ---------------------------------------------------------------------------
 # ring arithmetic (ring.py:170-207, 276-335)
 

@@ -33,6 +33,7 @@ _SIGS = {
     "hcnn_codec_destroy": (C.c_int, [C.c_void_p]),
     "hcnn_codec_encode": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "hcnn_codec_decode": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "hcnn_ntt64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p]),
     "hcnn_set_secret_key": (C.c_int, [C.c_void_p, C.c_void_p]),
     "hcnn_decrypt": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]),
     "hcnn_alloc": (C.c_int, [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),

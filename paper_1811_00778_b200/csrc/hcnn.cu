@@ -93,7 +93,7 @@ struct hcnn_codec {
   uint64_t t = 0, zeta = 0;
   ulonglong2* d_tw = nullptr;
   ulonglong2* d_itw = nullptr;
-  ulonglong2 ninv{};
+  ulonglong2 ninv{}, ninv_w{};  // N^-1 and psi^-N/2 N^-1 (the last inverse stage), Shoup
 };
 
 struct hcnn_weights {
@@ -784,6 +784,38 @@ __global__ void k_bfly_peak(uint32_t* out, uint32_t w, uint32_t ws, uint32_t p, 
   if (acc == 0x9e3779b9u) out[0] = acc;
 }
 
+// The u64 counterpart (kind 16): Harvey forward butterflies on 62-bit
+// residues (mul_shoup64_lazy: one 64x64 high product, two 64-bit low
+// products), the attainable rate of the u64 NTT's instruction mix
+__global__ void k_bfly64_peak(uint32_t* out, uint64_t w, uint64_t ws, uint64_t p, int iters) {
+  uint64_t a[8], b[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    a[i] = ((uint64_t)threadIdx.x * 7919 + i + blockIdx.x) % p;
+    b[i] = ((uint64_t)threadIdx.x * 104729 + 3 * i + blockIdx.x) % p;
+  }
+  const uint64_t p2 = 2 * p;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint64_t X = csub64(a[i], p2);
+      const uint64_t T = mul_shoup64_lazy(b[i], w, ws, p);
+      a[i] = X + T;
+      b[i] = X - T + p2;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {
+      const uint64_t t = a[i + 1];
+      a[i + 1] = b[i];
+      b[i] = t;
+    }
+  }
+  uint64_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc ^= a[i] ^ b[i];
+  if (acc == 0x9e3779b97f4a7c15ull) out[0] = (uint32_t)acc;
+}
+
 // Butterfly cost decomposition probes (kinds 10-12), same chain structure as
 // k_bfly_peak.  10: the quotient of b w / p from the fp64 pipe (exact to +-1:
 // b -> double by the 2^52 trick, one DFMA with the magic 1.5 2^52 rounds it to
@@ -1252,6 +1284,11 @@ int hcnn_int_peak(int device, int kind, double* ops_per_s) {
         case 14: k_dot_probe<14><<<blocks, tpb>>>(out, 12345u, iters / 16); break;
         case 15: k_dot_probe<15><<<blocks, tpb>>>(out, 12345u, iters / 16); break;
         case 12: k_bfly_probe<12><<<blocks, tpb>>>(out, 123456789u, 493942125u, 1073643521u, 0.0, iters); break;
+        case 16: {
+          const uint64_t p = 4611686018427322369ull, w = 1234567890123456789ull;
+          k_bfly64_peak<<<blocks, tpb>>>(out, w, (uint64_t)(((u128)w << 64) / p), p, iters / 4);
+          break;
+        }
         default: k_int_peak<5><<<blocks, tpb>>>(out, 0x3e3779b1u, 12345u, iters); break;
       }
     };
@@ -1265,6 +1302,7 @@ int hcnn_int_peak(int device, int kind, double* ops_per_s) {
     CK(cudaEventElapsedTime(&ms, e0, e1));
     *ops_per_s = 5.0 * (kind == 9 ? blocks / 4 : blocks) * tpb * (double)iters * 8 / (ms * 1e-3);
     if (kind >= 13 && kind <= 15) *ops_per_s = 5.0 * blocks * tpb * (double)(iters / 16) * 13 / (ms * 1e-3);
+    if (kind == 16) *ops_per_s = 5.0 * blocks * tpb * (double)(iters / 4) * 8 / (ms * 1e-3);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaFree(out);
@@ -1552,7 +1590,7 @@ static int hcnn_encrypt_impl(hcnn_ctx* c, const int8_t* u, const int8_t* e1, con
 int hcnn_codec_create(uint64_t t, uint32_t n, int device, hcnn_codec** out) {
   return guarded([&] {
     if (!out) fail(HCNN_ERR_PARAM, "null argument");
-    if (n < 2 || (n & (n - 1)) || n > (1u << 15)) fail(HCNN_ERR_UNSUPPORTED, "slot count must be a power of two <= 2^15");
+    if (n < 2 || (n & (n - 1)) || n > (1u << 15)) fail(HCNN_ERR_UNSUPPORTED, "ring degree must be a power of two in [2, 2^15]");
     if (t >= (1ull << 62) || !is_prime64(t)) fail(HCNN_ERR_UNSUPPORTED, "t must be a prime below 2^62");
     if ((t - 1) % (2ull * n)) fail(HCNN_ERR_UNSUPPORTED, "2N does not divide t-1");
     CK(cudaSetDevice(device));
@@ -1578,6 +1616,8 @@ int hcnn_codec_create(uint64_t t, uint32_t n, int device, hcnn_codec** out) {
     }
     const u64 ni = invmod64(n % t, t);
     c->ninv = make_ulonglong2(ni, shoup64(ni));
+    const u64 nw = mulmod64(ipw[n / 2], ni, t);
+    c->ninv_w = make_ulonglong2(nw, shoup64(nw));
     CK(cudaMalloc(&c->d_tw, n * sizeof(ulonglong2)));
     CK(cudaMalloc(&c->d_itw, n * sizeof(ulonglong2)));
     CK(cudaMemcpy(c->d_tw, tw.data(), n * sizeof(ulonglong2), cudaMemcpyHostToDevice));
@@ -1604,11 +1644,23 @@ int hcnn_codec_encode(hcnn_codec* c, const uint64_t* slots, uint64_t* polys, siz
     cudaStream_t st = (cudaStream_t)stream;
     k_permute_brv64<<<dim3(cdiv(c->n, 256), (unsigned)rows), 256, 0, st>>>(slots, polys, (int)c->logn);
     CK(cudaGetLastError());
-    const size_t smem = (size_t)c->n * 8;
-    if (smem > 200 * 1024) fail(HCNN_ERR_UNSUPPORTED, "slot count too large for the u64 NTT");
-    CK(cudaFuncSetAttribute(k_ntt64<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    k_ntt64<true><<<(unsigned)rows, 512, smem, st>>>(polys, (int)c->logn, c->t, c->d_itw, c->ninv);
-    CK(cudaGetLastError());
+    CK(launch_ntt64<true>(polys, rows, (int)c->logn, c->t, c->d_itw, c->ninv, c->ninv_w, st));
+  });
+}
+
+// in-place u64 negacyclic NTT rows over the codec's prime (ntt.py:113-154
+// for primes up to 62 bits): forward natural -> bit-reversed positions,
+// inverse back, fully reduced
+int hcnn_ntt64(hcnn_codec* c, uint64_t* rows, size_t n_rows, int inverse, void* stream) {
+  return guarded([&] {
+    if (!n_rows) return;
+    if (!rows) fail(HCNN_ERR_PARAM, "null argument");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    if (inverse)
+      CK(launch_ntt64<true>(rows, n_rows, (int)c->logn, c->t, c->d_itw, c->ninv, c->ninv_w, st));
+    else
+      CK(launch_ntt64<false>(rows, n_rows, (int)c->logn, c->t, c->d_tw, c->ninv, c->ninv_w, st));
   });
 }
 
@@ -1618,14 +1670,10 @@ int hcnn_codec_decode(hcnn_codec* c, const uint64_t* polys, uint64_t* slots, siz
     if (!rows) return;
     CK(cudaSetDevice(c->device));
     cudaStream_t st = (cudaStream_t)stream;
-    const size_t smem = (size_t)c->n * 8;
-    if (smem > 200 * 1024) fail(HCNN_ERR_UNSUPPORTED, "slot count too large for the u64 NTT");
-    CK(cudaFuncSetAttribute(k_ntt64<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     uint64_t* tmp = nullptr;
     pool_malloc(&tmp, rows * c->n * sizeof(uint64_t), st, c->device);
     CK(cudaMemcpyAsync(tmp, polys, rows * c->n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
-    k_ntt64<false><<<(unsigned)rows, 512, smem, st>>>(tmp, (int)c->logn, c->t, c->d_tw, c->ninv);
-    CK(cudaGetLastError());
+    CK(launch_ntt64<false>(tmp, rows, (int)c->logn, c->t, c->d_tw, c->ninv, c->ninv_w, st));
     k_permute_brv64<<<dim3(cdiv(c->n, 256), (unsigned)rows), 256, 0, st>>>(tmp, slots, (int)c->logn);
     CK(cudaGetLastError());
     CK(cudaFreeAsync(tmp, st));

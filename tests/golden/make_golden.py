@@ -510,6 +510,48 @@ def make_hfir():
         json.dump(meta, fh, indent=1)
 
 
+def make_ntt64():
+    """u64 NTT known answers through the reference's own tables and transform
+    (ntt.NttPlan: psi search, twists, stage-packed twiddles;
+    ntt._transform_rows_numpy on Python ints, exact for 62-bit primes;
+    ring.ntt_forward / ntt_inverse's twist and untwist): natural-order
+    spectra of seeded rows for a 62-bit prime and for the MNIST t."""
+    from hefir import ntt as _ntt
+
+    def prime_below(bits, two_n):
+        k = ((1 << bits) - 1) // two_n
+        while True:
+            cand = k * two_n + 1
+            if cand < (1 << bits) and _ntt.is_probable_prime(cand):
+                return cand
+            k -= 1
+
+    p62 = prime_below(62, 1 << 16)
+    rng = np.random.default_rng(64)
+    out, meta = {}, {"p62": p62, "cases": []}
+    for name, p, n in (("p62_64", p62, 64), ("p62_1024", p62, 1024), ("p62_8192", p62, 8192),
+                       ("t_8192", MNIST_T, 8192)):
+        plan = _ntt.NttPlan(p, n)
+        rev = _ntt.bit_reverse_indices(n)
+        x = np.array([[int(v) for v in rng.integers(0, p, n, dtype=np.uint64)] for _ in range(2)], dtype=object)
+        x[1, :8] = p - 1
+        mods = np.array([p, p], dtype=object)
+        tw = np.array([plan.tw, plan.tw], dtype=object)
+        itw = np.array([plan.itw, plan.itw], dtype=object)
+        fwd = x * np.array(plan.psi_pows, dtype=object) % p          # ring.ntt_forward: twist,
+        _ntt._transform_rows_numpy(fwd, mods, tw, rev)                # then the cyclic transform
+        inv = x.copy()                                                # ring.ntt_inverse of x
+        _ntt._transform_rows_numpy(inv, mods, itw, rev)
+        inv = inv * np.array(plan.ipsi_pows, dtype=object) % p
+        out[name + "_x"] = x.astype(np.uint64)
+        out[name + "_fwd"] = fwd.astype(np.uint64)
+        out[name + "_inv"] = inv.astype(np.uint64)
+        meta["cases"].append({"name": name, "p": p, "n": n})
+    np.savez_compressed(os.path.join(HERE, "ntt64.npz"), **out)
+    with open(os.path.join(HERE, "ntt64.json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["small", "n1024", "cifar64", "set1", "mnist1024", "plain", "hfir"]
     for w in which:

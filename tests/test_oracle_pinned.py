@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 import hcnn_oracle as O
-from conftest import GOLDEN, HAVE_REF, import_reference
+from conftest import GOLDEN, HAVE_REF, import_reference, load_golden
 
 
 def _params(meta):
@@ -268,3 +268,19 @@ def test_hmult_plain_golden():
                 assert np.array_equal(out3, a["s_out3"][k])
             else:
                 assert hashlib.sha256(out3.astype("<u8").tobytes()).hexdigest() == meta["m"]["out3_sha"][k]
+
+
+def test_wide_prime_ntt_golden():
+    """The oracle's u64 NTT (62-bit primes and the 43-bit MNIST t) equals the
+    reference's own tables and transform (tests/golden/ntt64.*, generated by
+    running hefir's NttPlan + transform_rows on Python ints)."""
+    meta, arrs = load_golden("ntt64")
+    for case in meta["cases"]:
+        if case["n"] > 1024:
+            continue  # the object-dtype oracle is slow at 2^13; the GPU tests cover those rows
+        name, p, n = case["name"], case["p"], case["n"]
+        x = arrs[name + "_x"]
+        assert np.array_equal(O.ntt_forward_wide(p, n, x).astype(np.uint64), arrs[name + "_fwd"]), name
+        assert np.array_equal(O.ntt_inverse_wide(p, n, x).astype(np.uint64), arrs[name + "_inv"]), name
+        back = O.ntt_inverse_wide(p, n, O.ntt_forward_wide(p, n, x))
+        assert np.array_equal(back.astype(np.uint64), x), name
