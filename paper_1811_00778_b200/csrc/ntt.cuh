@@ -51,6 +51,10 @@ struct NttGeom {
   static constexpr int NFULL = MIXED ? 1 + (REST + LOGE - 1) / LOGE : LOGN / LOGE;  // passes
   static constexpr int REM = MIXED ? 0 : LOGN % LOGE;  // low bits of the tail
   static constexpr bool SHFL_TAIL = !MIXED && SHFL_TAIL_ && REM > 0;
+  // a one-bit shuffle tail (N = 2^13, 2^9) swaps register halves between the
+  // lane pair once instead of exchanging every butterfly's operands and
+  // results (fwd_swap / inv_swap); the spectral layout keeps the swap
+  static constexpr bool SWAP_TAIL = SHFL_TAIL && REM == 1;
   static constexpr bool REG_TAIL = !MIXED && !SHFL_TAIL_ && REM > 0;
   static_assert(!SHFL_TAIL || T >= 32, "shuffle stages need full warps");
   // shared-memory words for one padded row; an NR-row NTT uses
@@ -374,6 +378,67 @@ DI void inv_shfl(uint32_t* x, const uint2* __restrict__ itw, uint32_t p, int tid
   }
 }
 
+// One-bit shuffle tail by a register-half swap.  Lane L (bit 0 of tid clear)
+// and U = L ^ 1 hold the two operands of every butterfly in the same register
+// e.  swap_halves: L sends x[e + E/2] and receives U's x[e] into it, U sends
+// x[e] and receives L's x[e + E/2] into it; afterwards every butterfly is
+// local: L owns the pairs e < E/2, U the pairs e + E/2, both on registers
+// (e, e + E/2).  The forward ends swapped (spectral_index absorbs it), the
+// inverse starts there and swaps back after its first stage.  One SHFL and
+// three SELs per register pair instead of two SHFLs and ~six SELs per
+// butterfly.
+template <class G, int NR>
+DI void swap_halves(uint32_t* x, int tid) {
+  constexpr int H = G::E / 2;
+  const bool upper = tid & 1;
+#pragma unroll
+  for (int e = 0; e < H; ++e)
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      uint32_t& lo = x[r * G::E + e];
+      uint32_t& hi = x[r * G::E + e + H];
+      const uint32_t got = __shfl_xor_sync(0xffffffffu, upper ? lo : hi, 1);
+      lo = upper ? got : lo;
+      hi = upper ? hi : got;
+    }
+}
+
+template <class G, int NR>
+DI void fwd_swap(uint32_t* x, const uint2* __restrict__ tw, uint32_t p, int tid) {
+  constexpr int H = G::E / 2;
+  constexpr int C = H < TW_CHUNK ? H : TW_CHUNK;
+  const uint32_t p2 = 2 * p;
+  const int off = (tid & 1) ? H : 0;
+  swap_halves<G, NR>(x, tid);
+#pragma unroll
+  for (int c0 = 0; c0 < H; c0 += C) {
+    uint2 w[C];
+    load_shfl_tw<G, 0, C>(w, tw, tid, c0 + off);
+#pragma unroll
+    for (int k = 0; k < C; ++k)
+#pragma unroll
+      for (int r = 0; r < NR; ++r) bfly_fwd(x[r * G::E + c0 + k], x[r * G::E + c0 + k + H], w[k], p, p2);
+  }
+}
+
+template <class G, int NR>
+DI void inv_swap(uint32_t* x, const uint2* __restrict__ itw, uint32_t p, int tid) {
+  constexpr int H = G::E / 2;
+  constexpr int C = H < TW_CHUNK ? H : TW_CHUNK;
+  const uint32_t p2 = 2 * p;
+  const int off = (tid & 1) ? H : 0;
+#pragma unroll
+  for (int c0 = 0; c0 < H; c0 += C) {
+    uint2 w[C];
+    load_shfl_tw<G, 0, C>(w, itw, tid, c0 + off);
+#pragma unroll
+    for (int k = 0; k < C; ++k)
+#pragma unroll
+      for (int r = 0; r < NR; ++r) bfly_inv(x[r * G::E + c0 + k], x[r * G::E + c0 + k + H], w[k], p, p2);
+  }
+  swap_halves<G, NR>(x, tid);
+}
+
 // exchange buffer XI of an NR-row transform
 template <class G, int NR>
 DI uint32_t* xbuf(uint32_t* s, int xi) {
@@ -460,7 +525,13 @@ template <class G>
 DI int spectral_index(int tid, int e) {
   if constexpr (G::MIXED) return gpass_index<G, 0, G::kb(G::NFULL - 1)>(tid, e);
   else if constexpr (G::REG_TAIL) return tail_index<G>(tid, e);
-  else return pass_index<G::REM, G::LOGE>(tid, e);
+  else if constexpr (G::SWAP_TAIL) {
+    // register bit LOGE-1 and lane bit 0 exchanged (fwd_swap)
+    constexpr int H = G::E / 2;
+    const int lane = (tid & ~1) | (e >= H ? 1 : 0);
+    const int ee = (e & (H - 1)) | ((tid & 1) ? H : 0);
+    return pass_index<G::REM, G::LOGE>(lane, ee);
+  } else return pass_index<G::REM, G::LOGE>(tid, e);
 }
 
 // tiled: groups of 4 spectral values, group-major then thread:
@@ -511,7 +582,9 @@ DI void store_tiled(const uint32_t* x, uint32_t* __restrict__ row, int tid) {
 template <class G, int NR = 1, bool FULL = true>
 DI void ntt_fwd(uint32_t* x, uint32_t* s, const uint2* __restrict__ tw, uint32_t p, int tid) {
   fwd_from<G, 0, NR>(x, s, tw, p, tid);
-  if constexpr (G::SHFL_TAIL) {
+  if constexpr (G::SWAP_TAIL) {
+    fwd_swap<G, NR>(x, tw, p, tid);
+  } else if constexpr (G::SHFL_TAIL) {
     fwd_shfl<G, G::REM - 1, NR>(x, tw, p, tid);
   } else if constexpr (G::REG_TAIL) {
     uint32_t* b = xbuf<G, NR>(s, G::NFULL - 1);
@@ -542,7 +615,9 @@ DI void ntt_fwd(uint32_t* x, uint32_t* s, const uint2* __restrict__ tw, uint32_t
 template <class G, int NR = 1>
 DI void ntt_inv(uint32_t* x, uint32_t* s, const uint2* __restrict__ itw, uint32_t p, const InvScale& sc,
                 int tid) {
-  if constexpr (G::SHFL_TAIL) {
+  if constexpr (G::SWAP_TAIL) {
+    inv_swap<G, NR>(x, itw, p, tid);
+  } else if constexpr (G::SHFL_TAIL) {
     inv_shfl<G, 0, NR>(x, itw, p, tid);
   } else if constexpr (G::REG_TAIL) {
     inv_tail<G, G::REM - 1, NR>(x, itw, p, tid);
