@@ -1948,7 +1948,7 @@ int hcnn_conv(hcnn_ctx* c, const uint32_t* in, uint32_t* out, int h, int w, int 
       g.z0 = (int)z0;
       const dim3 grid(cdiv(c->N / 4, tpb), 2 * c->K, zn);
       if (path == 0) {
-        const dim3 gridp(cdiv(c->N / 4, tpb), 2, zn);
+        const dim3 gridp(zn, 2, cdiv(c->N / 4, tpb));
         switch (fb) {
 #define X(FB)                                                                                           \
   case FB: {                                                                                            \

@@ -253,8 +253,12 @@ DI uint32_t f64_mod(double acc, double p, double pinv) {
   return (uint32_t)__double2uint_rn(r);
 }
 
-// grid: x = coefficient quads, y = part, z = out position * nfb + filter block;
-// the block loops over the K limbs, reusing its staged weights (doubles, one
+// grid: x = out position * nfb + filter block, y = part, z = coefficient
+// quads.  Blocks launch x-fastest, so the resident blocks sweep the output
+// positions of ONE coefficient slice: the input rows their windows share
+// (a 1/16 slice of each ciphertext) stay in L2 between neighbouring
+// positions and each input slice crosses HBM about once.
+// The block loops over the K limbs, reusing its staged weights (doubles, one
 // copy for all limbs) and tap table (input ciphertext per tap, -1 when the tap
 // falls in the padding).  smem: FB * taps doubles + taps ints.
 template <int FB>
@@ -266,7 +270,7 @@ __global__ void __launch_bounds__(128)
   const int taps = g.kh * g.kw * g.cg;
   int* tct = reinterpret_cast<int*>(wsd + FB * taps);
   const int nfb = g.f / FB;
-  const int zb = blockIdx.z + g.z0;
+  const int zb = blockIdx.x + g.z0;  // output position x filter block: the fastest grid index
   const int pos = zb / nfb, fbk = zb % nfb;
   const int f0 = fbk * FB;
   const int oy = pos / g.ow, ox = pos % g.ow;
@@ -279,7 +283,7 @@ __global__ void __launch_bounds__(128)
     tct[t] = (iy < 0 || iy >= g.h || ix < 0 || ix >= g.w) ? -1 : (iy * g.w + ix) * g.c + grp * g.cg + ci;
   }
   __syncthreads();
-  const int quad = blockIdx.x * blockDim.x + threadIdx.x;
+  const int quad = blockIdx.z * blockDim.x + threadIdx.x;
   if (quad * 4 >= N) return;
   const int part = blockIdx.y;
   const size_t ct_stride = (size_t)2 * K * N / 4;  // uint4 per ciphertext
