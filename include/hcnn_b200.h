@@ -72,8 +72,8 @@ enum {
  * parked in TMEM, 8192 persistent square tensor (one CTA per SM, TMA
  * prefetch of the next item's rows), 16384 relinearisation over a shared
  * three-prime basis R (digit NTTs mod 3 primes instead of mod every q_j, exact
- * CRT back; N = 2^12 and 2^13, at most 23 digits).  Default per N:
- * 8192|16384 at 2^13, 64|1024|4096 at 2^14, 512|2048 at 2^15, 0 otherwise.
+ * CRT back; N = 2^12 to 2^14, at most 23 digits).  Default per N:
+ * 8192|16384 at 2^13, 64|1024|4096|16384 at 2^14, 512|2048 at 2^15, 0 otherwise.
  * Results are identical for every setting. */
 /* HCNN_OPT_TS_CHUNK: ciphertexts per extend/tensor/scale sub-chunk of a
  * multiply (the tensor's output of one sub-chunk stays in L2 for the scale

@@ -499,7 +499,10 @@ unsigned cdiv(size_t a, size_t b) { return (unsigned)((a + b - 1) / b); }
 constexpr int RELIN_RBASIS = 16384;
 
 bool rb_active(const hcnn_ctx* c) {
-  return (c->variant & RELIN_RBASIS) && c->rb_ok && (c->logN == 12 || c->logN == 13) && !(c->variant & 64);
+  if (!(c->variant & RELIN_RBASIS) || !c->rb_ok) return false;
+  if (c->logN == 12 || c->logN == 13) return !(c->variant & 64);  // radix-16 shuffle-tail kernels
+  if (c->logN == 14) return !(c->variant & 512);                   // one-row kernels, either 2^14 geometry
+  return false;
 }
 
 // key rows mod r_a in the NTT domain (tiled layout of the R kernels' geometry)
@@ -1349,7 +1352,7 @@ int hcnn_ctx_create(hcnn_ctx** out, uint32_t n, uint32_t k, const uint64_t* prim
     // shuffle-tail radix-16 kernels up to 2^13 (persistent square tensor and
     // relinearisation over R at 2^13: profiles/r2/micro_rbasis.jsonl),
     // mixed-width passes at 2^14, 2-CTA cluster relinearisation at 2^15
-    c->variant = c->logN == 13 ? (8192 | RELIN_RBASIS) : c->logN == 14 ? (64 | 1024 | 4096)
+    c->variant = c->logN == 13 ? (8192 | RELIN_RBASIS) : c->logN == 14 ? (64 | 1024 | 4096 | RELIN_RBASIS)
                  : c->logN == 15 ? (512 | 2048) : 0;
     build_tables(c.get(), q, t);
     *out = c.release();

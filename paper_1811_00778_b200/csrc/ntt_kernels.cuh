@@ -830,6 +830,11 @@ template <class G>
 __host__ __device__ constexpr bool rb_geom() {
   return G::E == 16 && !G::MIXED && G::LOGN >= 12 && G::LOGN <= 13 && G::fits(2);
 }
+// 1024-thread geometries (N = 2^14, 64 registers): one-row variants
+template <class G>
+__host__ __device__ constexpr bool rb_geom1() {
+  return G::E == 16 && G::T == 1024 && G::LOGN == 14 && G::fits(1);
+}
 
 // Step 1 of 3 (bfv.py:368-404 restated over the basis R, common.cuh).  One
 // CTA per (r_a, ct): the D digit rows of c2 through the forward NTT mod r_a,
@@ -886,6 +891,101 @@ __global__ void __launch_bounds__(G::T, 1)
     ntt_fwd<G, 1, true>(x, s, tw, p, tid);
     store_tiled<G>(x, orow + (size_t)i * G::N, tid);
   }
+}
+
+// Step 1 at 1024 threads (64 registers): one digit row at a time, the next
+// row's loads issued before the current transform.
+template <class G>
+__global__ void __launch_bounds__(G::T, 1)
+    k_rb_fwd1(const uint32_t* __restrict__ dig, uint32_t* __restrict__ dspec, int D, int reduce_digits,
+              RbTabs rb, NttTabs nt) {
+  extern __shared__ __align__(16) uint32_t s[];
+  constexpr int E = G::E;
+  const int tid = threadIdx.x;
+  const int a = blockIdx.x;
+  const size_t ct = blockIdx.y;
+  const int jj = rb.roff + a;
+  const uint32_t p = nt.prime[jj];
+  const uint64_t mu = nt.mu[jj];
+  const uint2* tw = nt.tw + (size_t)jj * G::N;
+  const uint32_t* drow = dig + ct * D * G::N;
+  uint32_t* orow = dspec + (ct * RB_A + a) * (size_t)D * G::N;
+  const int share = (D + gridDim.z - 1) / gridDim.z;
+  const int i0 = blockIdx.z * share;
+  const int i1 = min(D, i0 + share);
+  if (i0 >= i1) return;
+  uint32_t x[E];
+  load_natural<G>(x, drow + (size_t)i0 * G::N, tid);
+  for (int i = i0; i < i1; ++i) {
+    uint32_t nx[E];
+    if (i + 1 < i1) load_natural<G>(nx, drow + (size_t)(i + 1) * G::N, tid);
+    if (reduce_digits) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = reduce64(x[e], p, mu);
+    }
+    ntt_fwd<G, 1, true>(x, s, tw, p, tid);
+    store_tiled<G>(x, orow + (size_t)i * G::N, tid);
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = nx[e];
+  }
+}
+
+// Step 3 at 1024 threads: per part, the three one-row inverses mod r0, r1, r2
+// (next row's loads issued first; the first two results parked in TMEM),
+// then that part's CRT and store.
+template <class G>
+__global__ void __launch_bounds__(G::T, 1)
+    k_rb_inv1(const uint32_t* __restrict__ zspec, const uint32_t* __restrict__ y3, uint32_t* __restrict__ out,
+              int K, RbTabs rb, NttTabs nt) {
+  extern __shared__ __align__(16) uint32_t s[];
+  __shared__ uint32_t tmem_slot;
+  constexpr int E = G::E;
+  static_assert(E == 16, "TMEM parking in 16-column chunks");
+  const int tid = threadIdx.x;
+  const int j = blockIdx.x;
+  const size_t ct = blockIdx.y;
+  const uint32_t* zr = zspec + (ct * K + j) * (size_t)RB_A * 2 * G::N;
+  constexpr uint32_t COLS = tmem_stash_cols<G, 2 * E>();
+  const uint32_t tbase = tmem_stash_alloc(&tmem_slot, COLS, tid, 2 * E);
+  const uint32_t q = nt.prime[j];
+  const uint32_t qinv = nt.pinv[j];
+  const uint32_t c0 = rb.crt_q[j][0], c1 = rb.crt_q[j][1], c2 = rb.crt_q[j][2];
+  const uint32_t cR = rb.negR_q[j];
+  uint32_t x[E];
+  load_tiled<G>(x, zr, tid);  // row (a = 0, part 0)
+#pragma unroll 1
+  for (int part = 0; part < 2; ++part) {
+#pragma unroll
+    for (int a = 0; a < RB_A; ++a) {
+      uint32_t nx[E];
+      const int nxt = a + 1 < RB_A ? 2 * (a + 1) + part : (part == 0 ? 1 : -1);  // next (a, part) row
+      if (nxt >= 0) load_tiled<G>(nx, zr + (size_t)nxt * G::N, tid);
+      const int jj = rb.roff + a;
+      ntt_inv<G, 1>(x, s, nt.itw + (size_t)jj * G::N, nt.prime[jj], InvScale{rb.isc_n[a], rb.isc_nw[a]}, tid);
+      if (a + 1 < RB_A) {
+        tmem_st16(tbase + (uint32_t)a * E, x);
+      } else {
+        uint32_t z0[E], z1[E];
+        tmem_ld16(tbase, z0);
+        tmem_ld16(tbase + E, z1);
+        const uint32_t* yr = y3 + ((ct * 3 + part) * K + j) * G::N;
+        uint32_t* o = out + ((ct * 2 + part) * K + j) * G::N;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const float f = __fmaf_rn((float)z0[e], rb.rinv[0], __fmaf_rn((float)z1[e], rb.rinv[1], (float)x[e] * rb.rinv[2]));
+          const uint32_t v = (uint32_t)__float2int_rn(f);
+          const uint64_t acc = (uint64_t)z0[e] * c0 + (uint64_t)z1[e] * c1 + (uint64_t)x[e] * c2 + (uint64_t)v * cR;
+          const int idx = natural_index<G>(tid, e);
+          o[idx] = add_mod(redc(acc, q, qinv), yr[idx], q);
+        }
+      }
+      if (nxt >= 0) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) x[e] = nx[e];
+      }
+    }
+  }
+  tmem_stash_free(tmem_slot, COLS, tid);
 }
 
 // Step 3 of 3.  One CTA per (q_j, ct): for each r_a the pair (Z_0, Z_1) mod
@@ -1064,6 +1164,12 @@ void configure_smem() {
   cudaFuncSetAttribute(k_relin<G, relin_acc64<G>(true), 1>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, RelinSmem<G, 1>::BYTES);
   cudaFuncSetAttribute(k_encrypt<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if constexpr (rb_geom1<G>()) {
+    cudaFuncSetAttribute(k_rb_fwd1<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         G::ntt_smem_words(1) * sizeof(uint32_t));
+    cudaFuncSetAttribute(k_rb_inv1<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         G::ntt_smem_words(1) * sizeof(uint32_t));
+  }
   if constexpr (rb_geom<G>()) {
     cudaFuncSetAttribute(k_rb_fwd<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          G::ntt_smem_words(2) * sizeof(uint32_t));
@@ -1195,7 +1301,14 @@ cudaError_t launch_with(int op, const NttLaunch& a) {
       break;
     case 7:  // relinearisation over R, step 1: digit spectra mod r_a
     case 8:  // step 3: inverse mod r_a, exact CRT to q_j, + (y0, y1)
-      if constexpr (rb_geom<G>()) {
+      if constexpr (rb_geom1<G>()) {
+        if (op == 7)
+          k_rb_fwd1<G><<<a.grid, G::T, G::ntt_smem_words(1) * sizeof(uint32_t), a.stream>>>(
+              a.dig, a.out, a.D, a.reduce_digits, a.rb, a.nt);
+        else
+          k_rb_inv1<G><<<a.grid, G::T, G::ntt_smem_words(1) * sizeof(uint32_t), a.stream>>>(
+              a.a, a.y3, a.out, a.K, a.rb, a.nt);
+      } else if constexpr (rb_geom<G>()) {
         if (op == 7)
           k_rb_fwd<G><<<a.grid, G::T, G::ntt_smem_words(2) * sizeof(uint32_t), a.stream>>>(
               a.dig, a.out, a.D, a.reduce_digits, a.rb, a.nt);

@@ -58,7 +58,7 @@ def _three_part(primes, n, rng, count, extreme):
     return x
 
 
-@pytest.mark.parametrize("n,log2w", [(8192, 16), (8192, 32), (8192, 8), (4096, 16)])
+@pytest.mark.parametrize("n,log2w", [(8192, 16), (8192, 32), (8192, 8), (4096, 16), (16384, 16), (16384, 32)])
 def test_rbasis_relinearize_equals_per_prime_kernel(n, log2w):
     """11 primes of 30 bits, t = the MNIST set-1 modulus: relinearize with
     the flag on and off agree bit for bit on random and extreme 3-part
@@ -79,7 +79,7 @@ def test_rbasis_relinearize_equals_per_prime_kernel(n, log2w):
     E._CTXS.clear()
 
 
-@pytest.mark.parametrize("n", [4096, 8192])
+@pytest.mark.parametrize("n", [4096, 8192, 16384])
 def test_rbasis_hsquare_vs_oracle(n):
     """HSquare with the flag on equals the oracle's hmult_raw + relinearize
     (the reference algorithm) on fresh encryptions, 3 primes."""
