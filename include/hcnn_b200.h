@@ -62,7 +62,8 @@ enum {
   HCNN_Q_LOG2W = 4,
   HCNN_Q_WS_BYTES = 5, /* workspace currently held */
   HCNN_Q_KERNELS = 6,  /* kernels launched since creation */
-  HCNN_Q_NTT_VARIANT = 7
+  HCNN_Q_NTT_VARIANT = 7,
+  HCNN_Q_RELIN_RBASIS = 8  /* 1 when relinearisations take the shared-basis R path (flag + parameters) */
 };
 /* Tuning options.  HCNN_OPT_NTT_VARIANT: geometry flags of the fused NTT
  * kernels: 16 one-row relinearisation, 32 radix-32 square tensor, 64
@@ -72,8 +73,9 @@ enum {
  * parked in TMEM, 8192 persistent square tensor (one CTA per SM, TMA
  * prefetch of the next item's rows), 16384 relinearisation over a shared
  * three-prime basis R (digit NTTs mod 3 primes instead of mod every q_j, exact
- * CRT back; N = 2^12 to 2^14, at most 23 digits).  Default per N:
- * 8192|16384 at 2^13, 64|1024|4096|16384 at 2^14, 512|2048 at 2^15, 0 otherwise.
+ * CRT back; N = 2^12 to 2^15 (2-CTA clusters at 2^15), at most 23 digits,
+ * at least 8 primes).  Default per N: 8192|16384 at 2^13,
+ * 64|1024|4096|16384 at 2^14, 512|2048|16384 at 2^15, 0 otherwise.
  * Results are identical for every setting. */
 /* HCNN_OPT_TS_CHUNK: ciphertexts per extend/tensor/scale sub-chunk of a
  * multiply (the tensor's output of one sub-chunk stays in L2 for the scale

@@ -500,8 +500,13 @@ constexpr int RELIN_RBASIS = 16384;
 
 bool rb_active(const hcnn_ctx* c) {
   if (!(c->variant & RELIN_RBASIS) || !c->rb_ok) return false;
+  // 3 D + 6 K transforms and 3x the products against D K + 2 K transforms:
+  // below ~8 primes the per-prime path is as fast or faster (measured at
+  // 2^15: K = 6 17.0 vs 14.7 us, K = 11 32.2 vs 43.2 us per ciphertext)
+  if (c->K < 8) return false;
   if (c->logN == 12 || c->logN == 13) return !(c->variant & 64);  // radix-16 shuffle-tail kernels
-  if (c->logN == 14) return !(c->variant & 512);                   // one-row kernels, either 2^14 geometry
+  if (c->logN == 14) return !(c->variant & 512);                   // one-row kernels (not the 2^14 cluster)
+  if (c->logN == 15) return (c->variant & 512) != 0;               // 2-CTA cluster kernels
   return false;
 }
 
@@ -1353,7 +1358,7 @@ int hcnn_ctx_create(hcnn_ctx** out, uint32_t n, uint32_t k, const uint64_t* prim
     // relinearisation over R at 2^13: profiles/r2/micro_rbasis.jsonl),
     // mixed-width passes at 2^14, 2-CTA cluster relinearisation at 2^15
     c->variant = c->logN == 13 ? (8192 | RELIN_RBASIS) : c->logN == 14 ? (64 | 1024 | 4096 | RELIN_RBASIS)
-                 : c->logN == 15 ? (512 | 2048) : 0;
+                 : c->logN == 15 ? (512 | 2048 | RELIN_RBASIS) : 0;
     build_tables(c.get(), q, t);
     *out = c.release();
   });
@@ -1472,6 +1477,7 @@ int64_t hcnn_ctx_query(hcnn_ctx* c, int what) {
     case HCNN_Q_WS_BYTES: return (int64_t)c->ws_bytes;
     case HCNN_Q_KERNELS: return c->launches;
     case HCNN_Q_NTT_VARIANT: return c->variant;
+    case HCNN_Q_RELIN_RBASIS: return rb_active(c) ? 1 : 0;
     default: return -1;
   }
 }
@@ -1939,11 +1945,20 @@ int hcnn_conv(hcnn_ctx* c, const uint32_t* in, uint32_t* out, int h, int w, int 
         fb = cand;
         break;
       }
-    const size_t zdim = (size_t)g.oh * g.ow * (f / fb);
-    if (zdim > (size_t)INT32_MAX) fail(HCNN_ERR_CAPACITY, "conv: output too large");
-    const size_t smem_d = (size_t)fb * kh * kw * g.cg * sizeof(double) + (size_t)kh * kw * g.cg * sizeof(int);
+    size_t smem_d = (size_t)fb * kh * kw * g.cg * sizeof(double) + (size_t)kh * kw * g.cg * sizeof(int);
     const size_t smem = (size_t)fb * kh * kw * g.cg * sizeof(uint16_t);
     const int path = (wt->wd && wt->flush >= 16 && smem_d <= 96 * 1024) ? 0 : (wt->small && smem <= 48 * 1024) ? 1 : 2;
+    // FP64 path: ten filters per block when the group allows (MNIST conv2:
+    // every loaded input feeds 40 DFMAs instead of 20)
+    if (path == 0 && g.per_group % 10 == 0 && fb < 10) {
+      const size_t s10 = (size_t)10 * kh * kw * g.cg * sizeof(double) + (size_t)kh * kw * g.cg * sizeof(int);
+      if (s10 <= 96 * 1024) {
+        fb = 10;
+        smem_d = s10;
+      }
+    }
+    const size_t zdim = (size_t)g.oh * g.ow * (f / fb);
+    if (zdim > (size_t)INT32_MAX) fail(HCNN_ERR_CAPACITY, "conv: output too large");
     if (path == 2 && !wt->wred) fail(HCNN_ERR_CAPACITY, "conv: filter too large for the small-weight kernel");
     // grid z holds at most 65535 blocks: tile the output blocks over launches
     for (size_t z0 = 0; z0 < zdim; z0 += 65535) {
@@ -1962,7 +1977,7 @@ int hcnn_conv(hcnn_ctx* c, const uint32_t* in, uint32_t* out, int h, int w, int 
     k_conv_f64<FB><<<gridp, tpb, smem_d, c->stream>>>(in, out, wt->wd, g, (int)c->K, (int)c->N, wt->flush, c->d_prime); \
     break;                                                                                              \
   }
-          X(1) X(2) X(4) X(5) X(8)
+          X(1) X(2) X(4) X(5) X(8) X(10)
 #undef X
         }
       } else if (path == 1) {

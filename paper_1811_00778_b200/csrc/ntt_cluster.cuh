@@ -285,4 +285,112 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G::T / 2, (G::T / 2 
   if (warp == 0) tmem_dealloc256(tmem_slot);
 }
 
+// Relinearisation over R (RbTabs, common.cuh) at N = 2^15 on 2-CTA clusters.
+// Step 1: one cluster per (r_a, ct, digit share) — every digit row through
+// the cluster forward NTT mod r_a (the next row's loads issued first),
+// spectra fully reduced, stored in the tiled layout of G.  grid (2 RB_A, B, split).
+// Every CTA of a 2^15 cluster holds 16 warps, so the row loads overlap
+// the other CTAs' transforms.
+template <class G>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G::T / 2, 1)
+    k_rb_fwd_cl(const uint32_t* __restrict__ dig, uint32_t* __restrict__ dspec, int D, int reduce_digits,
+                RbTabs rb, NttTabs nt) {
+  extern __shared__ __align__(16) uint32_t s[];
+  constexpr int E = G::E;
+  const uint32_t rank = cluster_rank();
+  const int vtid = (int)rank * ClusterGeom<G>::TC + threadIdx.x;
+  const int a = blockIdx.x / 2;
+  const size_t ct = blockIdx.y;
+  const int jj = rb.roff + a;
+  const uint32_t p = nt.prime[jj];
+  const uint64_t mu = nt.mu[jj];
+  const uint2* tw = nt.tw + (size_t)jj * G::N;
+  const uint32_t* drow = dig + ct * D * G::N;
+  uint32_t* orow = dspec + (ct * RB_A + a) * (size_t)D * G::N;
+  const int share = (D + gridDim.z - 1) / gridDim.z;
+  const int i0 = blockIdx.z * share;
+  const int i1 = min(D, i0 + share);
+  if (i0 >= i1) return;  // (both CTAs of the cluster take the same branch)
+  cluster_sync_all();  // both CTAs running before any DSMEM store
+  for (int i = i0; i < i1; ++i) {
+    uint32_t x[E];  // (no register prefetch: 32 more live residues would spill)
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = drow[(size_t)i * G::N + natural_index<G>(vtid, e)];
+    if (reduce_digits) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = reduce64(x[e], p, mu);
+    }
+    ntt_fwd_cl<G, 1, true>(x, s, tw, p, vtid, rank);
+#pragma unroll
+    for (int e = 0; e < E; ++e) orow[(size_t)i * G::N + tiled_index<G>(vtid, e)] = x[e];
+  }
+}
+
+// Step 3: one cluster per (q_j, ct); per part the three inverses mod r0, r1,
+// r2 (first two results parked in TMEM), then the exact centred CRT to q_j
+// (k_rb_inv in ntt_kernels.cuh) + (y0, y1).  grid (2 K, B).
+template <class G>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G::T / 2, 1)
+    k_rb_inv_cl(const uint32_t* __restrict__ zspec, const uint32_t* __restrict__ y3, uint32_t* __restrict__ out,
+                int K, RbTabs rb, NttTabs nt) {
+  extern __shared__ __align__(16) uint32_t s[];
+  __shared__ uint32_t tmem_slot;
+  constexpr int E = G::E;
+  static_assert(E == 32 && G::T / 2 == 512, "TMEM plan: 16 warps x 32 lanes x 64 columns");
+  const uint32_t rank = cluster_rank();
+  const int vtid = (int)rank * ClusterGeom<G>::TC + threadIdx.x;
+  const int j = blockIdx.x / 2;
+  const size_t ct = blockIdx.y;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tmem_alloc256(&tmem_slot);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tz = tmem_slot + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(warp >> 2) * 64;
+  const uint32_t* zr = zspec + (ct * K + j) * (size_t)RB_A * 2 * G::N;
+  const uint32_t q = nt.prime[j];
+  const uint32_t qinv = nt.pinv[j];
+  const uint32_t c0 = rb.crt_q[j][0], c1 = rb.crt_q[j][1], c2 = rb.crt_q[j][2];
+  const uint32_t cR = rb.negR_q[j];
+  cluster_sync_all();  // both CTAs running before any DSMEM store
+#pragma unroll 1
+  for (int part = 0; part < 2; ++part) {
+    uint32_t x[E];
+#pragma unroll 1
+    for (int a = 0; a < RB_A; ++a) {
+      const uint32_t* row = zr + (size_t)(2 * a + part) * G::N;
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = row[tiled_index<G>(vtid, e)];
+      const int jj = rb.roff + a;
+      ntt_inv_cl<G>(x, s, nt.itw + (size_t)jj * G::N, nt.prime[jj], InvScale{rb.isc_n[a], rb.isc_nw[a]}, vtid,
+                    rank);
+      if (a + 1 < RB_A) {
+        tmem_st16(tz + a * 32, x);
+        tmem_st16(tz + a * 32 + 16, x + 16);
+      }
+    }
+    const uint32_t* yr = y3 + ((ct * 3 + part) * K + j) * G::N;
+    uint32_t* o = out + ((ct * 2 + part) * K + j) * G::N;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t z0[16], z1[16];
+      tmem_ld16(tz + h * 16, z0);
+      tmem_ld16(tz + 32 + h * 16, z1);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const uint32_t x2 = x[16 * h + e];
+        const float f = __fmaf_rn((float)z0[e], rb.rinv[0], __fmaf_rn((float)z1[e], rb.rinv[1], (float)x2 * rb.rinv[2]));
+        const uint32_t v = (uint32_t)__float2int_rn(f);
+        const uint64_t acc = (uint64_t)z0[e] * c0 + (uint64_t)z1[e] * c1 + (uint64_t)x2 * c2 + (uint64_t)v * cR;
+        const int idx = natural_index<G>(vtid, 16 * h + e);
+        o[idx] = add_mod(redc(acc, q, qinv), yr[idx], q);
+      }
+    }
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  if (warp == 0) tmem_dealloc256(tmem_slot);
+}
+
 }  // namespace hcnn

@@ -1361,7 +1361,23 @@ cudaError_t ntt_launch(int op, const NttLaunch& a) {
       per_device_once(cfg, [] {
         cudaFuncSetAttribute(k_ntt_rows_cl<GC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(k_relin_cl<GC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if constexpr (LOGN == 15) {
+          cudaFuncSetAttribute(k_rb_fwd_cl<GC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+          cudaFuncSetAttribute(k_rb_inv_cl<GC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        }
       });
+      if constexpr (LOGN == 15) {
+        if (op == 7) {  // relinearisation over R, cluster kernels
+          k_rb_fwd_cl<GC><<<dim3(2 * a.grid.x, a.grid.y, a.grid.z), GC::T / 2, smem, a.stream>>>(
+              a.dig, a.out, a.D, a.reduce_digits, a.rb, a.nt);
+          return cudaGetLastError();
+        }
+        if (op == 8) {
+          k_rb_inv_cl<GC><<<dim3(2 * a.grid.x, a.grid.y), GC::T / 2, smem, a.stream>>>(
+              a.a, a.y3, a.out, a.K, a.rb, a.nt);
+          return cudaGetLastError();
+        }
+      }
       if (op == 0 && a.inverse == 2) {  // forward to the tiled key layout of GC
         k_ntt_rows_cl<GC><<<dim3(2 * a.grid.x), GC::T / 2, smem, a.stream>>>(a.rows, a.limbs, a.prime_off,
                                                                              a.inverse, a.nt);

@@ -58,13 +58,14 @@ def _three_part(primes, n, rng, count, extreme):
     return x
 
 
-@pytest.mark.parametrize("n,log2w", [(8192, 16), (8192, 32), (8192, 8), (4096, 16), (16384, 16), (16384, 32)])
+@pytest.mark.parametrize("n,log2w", [(8192, 16), (8192, 32), (8192, 8), (4096, 16), (16384, 16), (16384, 32),
+                                     (32768, 16)])
 def test_rbasis_relinearize_equals_per_prime_kernel(n, log2w):
     """11 primes of 30 bits, t = the MNIST set-1 modulus: relinearize with
     the flag on and off agree bit for bit on random and extreme 3-part
     ciphertexts (w = 2^8 has D = 42 > 23 digits and falls back by design)."""
     E._CTXS.clear()
-    primes = _primes(n, 11)
+    primes = _primes(n, 11 if n < 32768 else 8)
     params = B.BfvParams(B.RnsContext(n, primes), 5522259017729, relin_base=1 << log2w)
     _, _, rlk = B.keygen(params, np.random.default_rng(7 + log2w))
     rng = np.random.default_rng(n + log2w)
@@ -76,15 +77,19 @@ def test_rbasis_relinearize_equals_per_prime_kernel(n, log2w):
     g.set_variant(base | RB)
     got = host(ops.relinearize_device(g, x3, rlk))
     assert np.array_equal(got, want)
+    from paper_1811_00778_b200 import _lib
+
+    # the R path really ran (D <= 23 digits, K >= 8 primes), the per-prime one otherwise
+    assert _lib.lib().hcnn_ctx_query(g.handle, 8) == (1 if g.D <= 23 and len(primes) >= 8 else 0)
     E._CTXS.clear()
 
 
-@pytest.mark.parametrize("n", [4096, 8192, 16384])
+@pytest.mark.parametrize("n", [4096, 8192, 16384, 32768])
 def test_rbasis_hsquare_vs_oracle(n):
     """HSquare with the flag on equals the oracle's hmult_raw + relinearize
-    (the reference algorithm) on fresh encryptions, 3 primes."""
+    (the reference algorithm) on fresh encryptions, 8 primes."""
     E._CTXS.clear()
-    primes = [1073643521, 1073479681, 1073184769]
+    primes = _primes(n, 8)
     t = 65537
     params = B.BfvParams(B.RnsContext(n, primes), t)
     _, pk, rlk = B.keygen(params, np.random.default_rng(n))
@@ -92,6 +97,9 @@ def test_rbasis_hsquare_vs_oracle(n):
     cts = [B.encrypt(pk, B.Plaintext(rng.integers(0, t, n), t), params, rng) for _ in range(2)]
     g = E.context_for(params)
     g.set_variant(g.variant() | RB)
+    from paper_1811_00778_b200 import _lib
+
+    assert _lib.lib().hcnn_ctx_query(g.handle, 8) == 1
     x = dev(np.stack([ct_array(c) for c in cts]))
     got = host(ops.square_device(g, x, rlk))
     op = O.Params(O.Context(n, primes), t)
@@ -109,7 +117,7 @@ def test_rbasis_key_in_coefficient_domain():
 
     E._CTXS.clear()
     n = 8192
-    primes = _primes(n, 4)
+    primes = _primes(n, 8)
     params = B.BfvParams(B.RnsContext(n, primes), 65537)
     _, _, rlk = B.keygen(params, np.random.default_rng(3))
     op = O.Params(O.Context(n, primes), 65537)
@@ -121,6 +129,9 @@ def test_rbasis_key_in_coefficient_domain():
     g.set_variant(g.variant() & ~RB)
     want = host(ops.relinearize_device(g, x3, rlk))
     g.set_variant(g.variant() | RB)
+    from paper_1811_00778_b200 import _lib
+
+    assert _lib.lib().hcnn_ctx_query(g.handle, 8) == 1
     assert np.array_equal(host(ops.relinearize_device(g, x3, key)), want)
     assert np.array_equal(host(ops.relinearize_device(g, x3, rlk)), want)
     E._CTXS.clear()
