@@ -58,14 +58,16 @@ def _three_part(primes, n, rng, count, extreme):
     return x
 
 
-@pytest.mark.parametrize("n,log2w", [(8192, 16), (8192, 32), (8192, 8), (4096, 16), (16384, 16), (16384, 32),
-                                     (32768, 16)])
-def test_rbasis_relinearize_equals_per_prime_kernel(n, log2w):
-    """11 primes of 30 bits, t = the MNIST set-1 modulus: relinearize with
-    the flag on and off agree bit for bit on random and extreme 3-part
-    ciphertexts (w = 2^8 has D = 42 > 23 digits and falls back by design)."""
+@pytest.mark.parametrize("n,log2w,k", [(8192, 16, 11), (8192, 32, 11), (8192, 8, 11), (4096, 16, 11),
+                                       (16384, 16, 11), (16384, 32, 11), (32768, 16, 8),
+                                       (8192, 16, 12), (8192, 16, 8), (8192, 32, 16)])
+def test_rbasis_relinearize_equals_per_prime_kernel(n, log2w, k):
+    """k primes of 30 bits, t = the MNIST set-1 modulus: relinearize with the
+    flag on and off agree bit for bit on random and extreme 3-part ciphertexts.
+    K = 12 gives D = 23, the largest digit count of the R path (its lazy
+    64-bit sums are sized for it); w = 2^8 (D = 42) falls back by design."""
     E._CTXS.clear()
-    primes = _primes(n, 11 if n < 32768 else 8)
+    primes = _primes(n, k)
     params = B.BfvParams(B.RnsContext(n, primes), 5522259017729, relin_base=1 << log2w)
     _, _, rlk = B.keygen(params, np.random.default_rng(7 + log2w))
     rng = np.random.default_rng(n + log2w)
