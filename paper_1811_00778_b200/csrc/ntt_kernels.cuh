@@ -394,6 +394,13 @@ __global__ void __launch_bounds__(G::T, (G::T <= 256 ? 2 : 1))
 template <class G>
 constexpr int tensor_pf_smem_words() { return G::ntt_smem_words(pair_nr<G>()) + 2 * G::N; }
 
+// the persistent square tensor's three inverses as one lockstep transform
+// (its exchange buffers fit inside the pair transform's)
+template <class G>
+__host__ __device__ constexpr bool tensor_nr3() {
+  return G::E == 16 && !G::MIXED && G::ntt_smem_words(3) <= G::ntt_smem_words(pair_nr<G>());
+}
+
 template <class G>
 __global__ void __launch_bounds__(G::T, 1)
     k_tensor_sq_pf(const uint32_t* __restrict__ a, const uint32_t* __restrict__ a_ext,
@@ -452,6 +459,25 @@ __global__ void __launch_bounds__(G::T, 1)
       x[E + e] = umin32(2 * c, 2 * c - p2);
       y[e] = mont_mul(a1, a1, p, pinv);
     }
+    if constexpr (tensor_nr3<G>()) {
+    // the three inverses in lockstep (shared twiddle loads and barriers,
+    // single-buffered exchanges; at 2^13 this also removes the pair version's
+    // 192-byte register spill)
+    uint32_t z[3 * E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      z[e] = x[e];
+      z[E + e] = x[E + e];
+      z[2 * E + e] = y[e];
+    }
+    ntt_inv<G, 3>(z, s, itw, p, ninv, tid);
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      uint32_t* o = d + ((ct * 3 + r) * L + j) * G::N;
+#pragma unroll
+      for (int e = 0; e < E; ++e) o[natural_index<G>(tid, e)] = z[r * E + e];
+    }
+    } else {
     ntt_inv_pair<G>(x, s, itw, p, ninv, tid);
     uint32_t* o0 = d + ((ct * 3 + 0) * L + j) * G::N;
     uint32_t* o1 = d + ((ct * 3 + 1) * L + j) * G::N;
@@ -461,6 +487,7 @@ __global__ void __launch_bounds__(G::T, 1)
       o1[natural_index<G>(tid, e)] = x[E + e];
     }
     inv_store<G>(y, s, itw, p, ninv, tid, d + ((ct * 3 + 2) * L + j) * G::N);
+    }
   }
 }
 
