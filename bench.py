@@ -777,19 +777,24 @@ def run_reference(args):
                                                              "is missing or does not import"}), flush=True)
         return
     _ref_setup(args.seed)
-    vals = []
+    vals, walls = [], []
     with mp.get_context("fork").Pool(cores) as pool:
         for i in range(args.warmup + args.steps):
+            w0 = time.perf_counter()
             parts = _ref_step(cores, pool)
             if i >= args.warmup:
                 vals.append(parts)
+                walls.append(time.perf_counter() - w0)
     parts = tuple(float(np.mean([v[k] for v in vals])) for k in range(3))
     T = _extrapolate(*parts, cores)
     value = 8192 / T
+    # ms_per_step is what one timed step (a bounded sample of the batch) took
+    # on the host clock; the batch latency the sample extrapolates to is
+    # extrapolated_latency_s (value = 8192 images / that latency)
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": "images/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(T * 1e3, 1),
-        "latency_s": round(T, 2), "higher_is_better": True, "scaling": "weak",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(float(np.mean(walls)) * 1e3, 1),
+        "extrapolated_latency_s": round(T, 2), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int (Python big int / int64)", "data": "synthetic",
         "impl": "reference",
         "config": {"workload": "MNIST HCNN, preset 1 (N=8192, 11 primes, t=5522259017729), one 8192-image slot-batch, "

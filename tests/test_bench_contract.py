@@ -50,4 +50,8 @@ def test_bench_reference_arm_line():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["unit"] == "images/s" and d["value"] > 0
     assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["kind"] in ("port", "reference")
+    # the timed region a step reports is the sample's own host time, well
+    # inside the run; the full-batch latency it extrapolates to is separate
+    assert d["ms_per_step"] * d["steps"] < 600e3
+    assert d["extrapolated_latency_s"] * 1e3 > d["ms_per_step"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
