@@ -137,3 +137,24 @@ def test_rbasis_key_in_coefficient_domain():
     assert np.array_equal(host(ops.relinearize_device(g, x3, key)), want)
     assert np.array_equal(host(ops.relinearize_device(g, x3, rlk)), want)
     E._CTXS.clear()
+
+
+@pytest.mark.parametrize("n,base", [(16384, 1024 | 4096), (16384, 0), (8192, 0), (4096, 0)])
+def test_rbasis_on_other_geometries(n, base):
+    """The R path under the non-default geometries of its ring degrees (2^14
+    shuffle-tail instead of mixed passes, plain variants) equals the
+    per-prime kernel bit for bit."""
+    E._CTXS.clear()
+    primes = _primes(n, 10)
+    params = B.BfvParams(B.RnsContext(n, primes), 65537)
+    _, _, rlk = B.keygen(params, np.random.default_rng(9))
+    x3 = dev(_three_part(primes, n, np.random.default_rng(10), 3, True))
+    g = E.context_for(params)
+    g.set_variant(base)
+    want = host(ops.relinearize_device(g, x3, rlk))
+    g.set_variant(base | RB)
+    from paper_1811_00778_b200 import _lib
+
+    assert _lib.lib().hcnn_ctx_query(g.handle, 8) == 1
+    assert np.array_equal(host(ops.relinearize_device(g, x3, rlk)), want)
+    E._CTXS.clear()
