@@ -63,7 +63,8 @@ enum {
   HCNN_Q_WS_BYTES = 5, /* workspace currently held */
   HCNN_Q_KERNELS = 6,  /* kernels launched since creation */
   HCNN_Q_NTT_VARIANT = 7,
-  HCNN_Q_RELIN_RBASIS = 8  /* 1 when relinearisations take the shared-basis R path (flag + parameters) */
+  HCNN_Q_RELIN_RBASIS = 8  /* 1 when relinearisations of at least HCNN_OPT_RB_MIN_BATCH ciphertexts take
+                              the shared-basis R path (flag + parameters) */
 };
 /* Tuning options.  HCNN_OPT_NTT_VARIANT: geometry flags of the fused NTT
  * kernels: 16 one-row relinearisation, 32 radix-32 square tensor, 64
@@ -80,7 +81,10 @@ enum {
 /* HCNN_OPT_TS_CHUNK: ciphertexts per extend/tensor/scale sub-chunk of a
  * multiply (the tensor's output of one sub-chunk stays in L2 for the scale
  * kernel); 0 = the whole chunk at once. */
-enum { HCNN_OPT_NTT_VARIANT = 1, HCNN_OPT_TS_CHUNK = 2 };
+/* HCNN_OPT_RB_MIN_BATCH: smallest number of ciphertexts relinearised over R
+ * (flag 16384) in one call; smaller batches take the per-prime kernel, which
+ * is faster there (default 12). */
+enum { HCNN_OPT_NTT_VARIANT = 1, HCNN_OPT_TS_CHUNK = 2, HCNN_OPT_RB_MIN_BATCH = 3 };
 int hcnn_ctx_set_option(hcnn_ctx* ctx, int key, int64_t value);
 int64_t hcnn_ctx_query(hcnn_ctx* ctx, int what);
 /* psi (primitive 2N-th root) of prime i, i < K + KP (ntt.py:50-60) */

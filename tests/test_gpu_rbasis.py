@@ -25,6 +25,15 @@ from paper_1811_00778_b200 import ops  # noqa: E402
 RB = 16384
 
 
+def rb_context(params):
+    """engine context with every batch size on the R path when the flag is set"""
+    from paper_1811_00778_b200 import _lib
+
+    g = E.context_for(params)
+    _lib.check(_lib.lib().hcnn_ctx_set_option(g.handle, 3, 1), "rb min batch")
+    return g
+
+
 def dev(arr):
     return torch.from_numpy(np.ascontiguousarray(np.asarray(arr).astype(np.uint32)).view(np.int32)).cuda()
 
@@ -72,7 +81,7 @@ def test_rbasis_relinearize_equals_per_prime_kernel(n, log2w, k):
     _, _, rlk = B.keygen(params, np.random.default_rng(7 + log2w))
     rng = np.random.default_rng(n + log2w)
     x3 = dev(_three_part(primes, n, rng, 6, True))
-    g = E.context_for(params)
+    g = rb_context(params)
     base = g.variant() & ~RB
     g.set_variant(base)
     want = host(ops.relinearize_device(g, x3, rlk))
@@ -97,7 +106,7 @@ def test_rbasis_hsquare_vs_oracle(n):
     _, pk, rlk = B.keygen(params, np.random.default_rng(n))
     rng = np.random.default_rng(n + 1)
     cts = [B.encrypt(pk, B.Plaintext(rng.integers(0, t, n), t), params, rng) for _ in range(2)]
-    g = E.context_for(params)
+    g = rb_context(params)
     g.set_variant(g.variant() | RB)
     from paper_1811_00778_b200 import _lib
 
@@ -127,7 +136,7 @@ def test_rbasis_key_in_coefficient_domain():
                       for k0, k1 in rlk.components])
     key = hfir.DeviceRelinKey(coeff.astype(np.uint64), params.w, params.fingerprint)
     x3 = dev(_three_part(primes, n, np.random.default_rng(5), 4, True))
-    g = E.context_for(params)
+    g = rb_context(params)
     g.set_variant(g.variant() & ~RB)
     want = host(ops.relinearize_device(g, x3, rlk))
     g.set_variant(g.variant() | RB)
@@ -149,7 +158,7 @@ def test_rbasis_on_other_geometries(n, base):
     params = B.BfvParams(B.RnsContext(n, primes), 65537)
     _, _, rlk = B.keygen(params, np.random.default_rng(9))
     x3 = dev(_three_part(primes, n, np.random.default_rng(10), 3, True))
-    g = E.context_for(params)
+    g = rb_context(params)
     g.set_variant(base)
     want = host(ops.relinearize_device(g, x3, rlk))
     g.set_variant(base | RB)
@@ -157,4 +166,26 @@ def test_rbasis_on_other_geometries(n, base):
 
     assert _lib.lib().hcnn_ctx_query(g.handle, 8) == 1
     assert np.array_equal(host(ops.relinearize_device(g, x3, rlk)), want)
+    E._CTXS.clear()
+
+
+def test_small_batches_take_the_per_prime_kernel():
+    """Below HCNN_OPT_RB_MIN_BATCH (default 12) relinearisation runs the
+    per-prime kernel (faster for a handful of ciphertexts), from it on the R
+    path; results are identical."""
+    E._CTXS.clear()
+    n = 8192
+    primes = _primes(n, 11)
+    params = B.BfvParams(B.RnsContext(n, primes), 65537)
+    _, _, rlk = B.keygen(params, np.random.default_rng(12))
+    g = E.context_for(params)
+    x3 = dev(_three_part(primes, n, np.random.default_rng(13), 16, True))
+    outs = {}
+    for count in (4, 16):
+        g.profile(True)
+        outs[count] = host(ops.relinearize_device(g, x3[:count], rlk))
+        names = set(g.profile_read())
+        g.profile(False)
+        assert ("k_rb_fwd" in names) == (count >= 12) and ("k_relin" in names) == (count < 12), names
+    assert np.array_equal(outs[4], outs[16][:4])
     E._CTXS.clear()
