@@ -366,8 +366,10 @@ def run_ours(args):
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         ev0.record(stream)
+        h0 = time.perf_counter()
         for _ in range(args.steps):
             outs = step()
+        host_issue_ms = (time.perf_counter() - h0) * 1e3 / args.steps  # host time to enqueue a step
         ev1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -626,6 +628,7 @@ def run_ours(args):
         "e2e_dropin": dropin,
         "logits_shape_per_batch": result_shape,
         "gpu_launches": int(launches),
+        "host_issue_ms_per_step": round(host_issue_ms, 3),
         "kernels": kernels,
         "roofline": roof,
         "clocks": clk.summary(),
