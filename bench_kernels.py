@@ -112,6 +112,17 @@ def main():
                     hsq += us
                 line["hsquare_us_per_ct"] = round(hsq, 3)
                 line["hsquare_bfly_gs"] = round((5 * (k + g.KP) + (g.D + 2) * k) * bfly / (hsq * 1e-6) / 1e9, 1)
+                # general ct x ct multiply + relinearise (bfv.hmult: two extensions,
+                # 4 forward + 3 inverse transforms per prime), CUDA events around the calls
+                y = torch.roll(x, 1, 0).contiguous()
+                ops.hmult_device(g, x, y, rlk)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(a.reps):
+                    ops.hmult_device(g, x, y, rlk)
+                e1.record()
+                torch.cuda.synchronize()
+                line["hmult_us_per_ct"] = round(e0.elapsed_time(e1) / a.reps / a.cts * 1e3, 3)
                 print(json.dumps(line), flush=True)
 
 
