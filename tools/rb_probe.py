@@ -1,3 +1,9 @@
+"""Which ring degrees take the relinearisation over R by default: for N =
+2^13, 2^14, 2^15 with 6 primes, print N, the default NTT variant, the digit
+count and hcnn_ctx_query(HCNN_Q_RELIN_RBASIS).
+
+    python tools/rb_probe.py
+"""
 import numpy as np, sys
 sys.path.insert(0,'.')
 from paper_1811_00778_b200 import bfv as B, engine as E, _lib
