@@ -89,7 +89,9 @@ int hcnn_ctx_set_option(hcnn_ctx* ctx, int key, int64_t value);
 int64_t hcnn_ctx_query(hcnn_ctx* ctx, int what);
 /* psi (primitive 2N-th root) of prime i, i < K + KP (ntt.py:50-60) */
 uint64_t hcnn_ctx_prime(hcnn_ctx* ctx, int i, uint64_t* psi);
-/* upper bound on the workspace the context may hold (default 6 GiB) */
+/* upper bound on the multiply / relinearisation scratch the context may hold
+ * per call: the workspace plus the relinearisation-over-R spectra (default
+ * 12 GiB; batches are chunked to fit) */
 int hcnn_ctx_set_workspace_limit(hcnn_ctx* ctx, size_t bytes);
 
 /* Relinearisation key, host u64 [digits][2][K][N] (RelinKey.components,

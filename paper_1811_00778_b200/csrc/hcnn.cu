@@ -140,7 +140,9 @@ struct hcnn_ctx {
   bool rlk_reduce = false;
   uint8_t* ws = nullptr;
   size_t ws_bytes = 0;
-  size_t ws_limit = size_t(6) << 30;  // whole MNIST layers (800 cts at set 1) in one chunk
+  // memory for the multiply / relinearisation scratch (the workspace plus the
+  // R-basis spectra): whole MNIST layers (800 cts at set 1) in one chunk
+  size_t ws_limit = size_t(12) << 30;
   size_t ts_sub = 0;  // ciphertexts per extend/tensor/scale sub-chunk (0: whole chunk)
   // smallest batch relinearised over R (below it the per-prime kernel is
   // faster: set 1, 8 cts 20.2 vs 23.6 us, 16 cts 18.5 vs 16.8 us per ct)
@@ -615,6 +617,12 @@ void launch_relin(hcnn_ctx* c, const uint32_t* dig, const uint32_t* y3, uint32_t
   ntt_dispatch(c, 2, a, "k_relin");
 }
 
+// scratch of the relinearisation over R per ciphertext (digit spectra and
+// the multiply-accumulate output; allocated from the library pool per call)
+size_t rb_bytes_per_ct(const hcnn_ctx* c) {
+  return rb_active(c) ? ((size_t)RB_A * c->D + (size_t)c->K * RB_A * 2) * c->N * sizeof(uint32_t) : 0;
+}
+
 // bytes of workspace per ciphertext of a multiply chunk
 size_t mul_ws_per_ct(hcnn_ctx* c, bool general) {
   const size_t N = c->N, K = c->K, KP = c->KP;
@@ -625,8 +633,8 @@ size_t mul_ws_per_ct(hcnn_ctx* c, bool general) {
   return b * sizeof(uint32_t);
 }
 
-size_t chunk_cts(hcnn_ctx* c, size_t n, bool general) {
-  size_t per = mul_ws_per_ct(c, general);
+size_t chunk_cts(hcnn_ctx* c, size_t n, bool general, bool relin) {
+  const size_t per = mul_ws_per_ct(c, general) + (relin ? rb_bytes_per_ct(c) : 0);
   size_t ch = c->ws_limit / per;
   if (ch < 1) ch = 1;
   if (ch > 16384) ch = 16384;
@@ -690,7 +698,7 @@ void multiply(hcnn_ctx* c, const uint32_t* a, const uint32_t* b, size_t n, uint3
   if (n == 0) return;
   const size_t N = c->N, K = c->K;
   const bool general = a != b;
-  const size_t ch = chunk_cts(c, n, general);
+  const size_t ch = chunk_cts(c, n, general, out2 != nullptr);
   const size_t per = mul_ws_per_ct(c, general);
   uint8_t* ws = c->workspace(per * ch);
   const size_t ext_bytes = ((general ? 2 : 1) * 2 * c->KP + 3 * (K + c->KP)) * N * sizeof(uint32_t);
@@ -2131,7 +2139,7 @@ int hcnn_relinearize(hcnn_ctx* c, const uint32_t* in3, uint32_t* out, size_t n) 
     CK(cudaSetDevice(c->device));
     if (n == 0) return;
     const size_t per = (size_t)c->D * c->N * sizeof(uint32_t);
-    size_t ch = c->ws_limit / per;
+    size_t ch = c->ws_limit / (per + rb_bytes_per_ct(c));
     if (ch < 1) ch = 1;
     if (ch > 65535) ch = 65535;
     if (ch > n) ch = n;

@@ -132,6 +132,9 @@ class GpuContext:
         ts = os.environ.get("HCNN_TS_CHUNK")
         if ts is not None:
             _lib.check(L.hcnn_ctx_set_option(h, 2, int(ts)), "hcnn_ctx_set_option")
+        ws = os.environ.get("HCNN_WS_LIMIT_GB")
+        if ws is not None:
+            _lib.check(L.hcnn_ctx_set_workspace_limit(h, int(float(ws) * (1 << 30))), "workspace limit")
         self._rlk_ref = None
         self._weights = {}
         self._finalizer = weakref.finalize(self, L.hcnn_ctx_destroy, h)
