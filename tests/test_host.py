@@ -294,3 +294,53 @@ def test_host_widen_is_exact():
         _lib.check(_lib.lib().hcnn_host_widen(src.ctypes.data, 7, 2 * 257, ptrs.ctypes.data, threads))
         assert np.array_equal(np.stack(dst).reshape(7, -1), src.astype(np.int64))
 
+
+
+def test_rbasis_crt_identity_in_python_ints():
+    """The arithmetic of the relinearisation over R (csrc/relin_rb.cuh,
+    k_rb_inv), restated with Python ints at N = 64 with the worst-case
+    digits (w - 1) and keys: the negacyclic sums Z = sum_i d_i k~_i (keys
+    centred mod q_j) are recovered from their residues mod r0, r1, r2 by
+    x~_a = Z (R/r_a)^-1 mod r_a, v = rint(sum_a x~_a / r_a) in float32, and
+    Z = sum_a x~_a (R/r_a) - v R, so Z mod q_j equals the reference's
+    sum_i d_i k_{i,j} mod q_j (bfv.py:368-404)."""
+    r = [894959617, 893255681, 889454593]  # the library's R primes (= 1 mod 2^17, below 2^32/sqrt(23))
+    R = r[0] * r[1] * r[2]
+    n, D, w = 64, 21, 1 << 16
+    q = 1073643521
+    rng = np.random.default_rng(11)
+
+    def negacyclic(a, b):
+        out = [0] * n
+        for i in range(n):
+            for j in range(n):
+                k = i + j
+                if k < n:
+                    out[k] += a[i] * b[j]
+                else:
+                    out[k - n] -= a[i] * b[j]
+        return out
+
+    for trial in range(3):
+        if trial == 0:  # extreme: every digit w - 1, keys at +-(q - 1) / 2
+            digits = [[w - 1] * n for _ in range(D)]
+            keys = [[(q - 1) // 2 if (i + j) % 2 else -((q - 1) // 2) for j in range(n)] for i in range(D)]
+        else:
+            digits = [[int(v) for v in rng.integers(0, w, n)] for _ in range(D)]
+            keys = [[int(v) - (q - 1) // 2 for v in rng.integers(0, q, n)] for _ in range(D)]
+        Z = [0] * n
+        for i in range(D):
+            for k, v in enumerate(negacyclic(digits[i], keys[i])):
+                Z[k] += v
+        assert max(abs(z) for z in Z) * 4 < R  # the host check |Z| <= R / 4
+        rinv = [np.float32(1.0 / ra) for ra in r]
+        for k in range(n):
+            xt = [Z[k] * pow(R // ra, -1, ra) % ra for ra in r]
+            f = np.float32(0)
+            for a in range(3):
+                f = np.float32(f + np.float32(xt[a]) * rinv[a])
+            v = int(np.rint(f))
+            back = sum(xt[a] * (R // r[a]) for a in range(3)) - v * R
+            assert back == Z[k]
+            assert back % q == sum(digits[i][kk] * keys[i][(k - kk) % n] * (1 if kk <= k else -1)
+                                   for i in range(D) for kk in range(n)) % q
