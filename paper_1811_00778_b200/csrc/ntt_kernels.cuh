@@ -860,7 +860,7 @@ __host__ __device__ constexpr bool rb_geom() {
 // 1024-thread geometries (N = 2^14, 64 registers): one-row variants
 template <class G>
 __host__ __device__ constexpr bool rb_geom1() {
-  return G::E == 16 && G::T == 1024 && G::LOGN == 14 && G::fits(1);
+  return G::E == 16 && G::T == 1024 && G::LOGN == 14 && (G::ntt_smem_words(1) + G::N) * 4 <= 220 * 1024;
 }
 
 // Step 1 of 3 (bfv.py:368-404 restated over the basis R, common.cuh).  One
@@ -920,13 +920,18 @@ __global__ void __launch_bounds__(G::T, 1)
   }
 }
 
-// Step 1 at 1024 threads (64 registers): one digit row at a time, the next
-// row's loads issued before the current transform.
+// Step 1 at 1024 threads (64 registers): one digit row at a time; the next
+// row streams into a shared-memory stage by one TMA bulk copy (a register
+// prefetch would not fit the 64-register budget).
+template <class G>
+constexpr int rb1_smem_words() { return G::ntt_smem_words(1) + G::N; }
+
 template <class G>
 __global__ void __launch_bounds__(G::T, 1)
     k_rb_fwd1(const uint32_t* __restrict__ dig, uint32_t* __restrict__ dspec, int D, int reduce_digits,
               RbTabs rb, NttTabs nt) {
   extern __shared__ __align__(16) uint32_t s[];
+  __shared__ __align__(8) uint64_t bar;
   constexpr int E = G::E;
   const int tid = threadIdx.x;
   const int a = blockIdx.x;
@@ -941,31 +946,46 @@ __global__ void __launch_bounds__(G::T, 1)
   const int i0 = blockIdx.z * share;
   const int i1 = min(D, i0 + share);
   if (i0 >= i1) return;
-  uint32_t x[E];
-  load_natural<G>(x, drow + (size_t)i0 * G::N, tid);
+  uint32_t* stage = s + G::ntt_smem_words(1);
+  auto fetch = [&](int i) {
+    fence_proxy_async();
+    mbar_expect_tx(&bar, G::N * 4);
+    bulk_g2s(stage, drow + (size_t)i * G::N, G::N * 4, &bar);
+  };
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    fetch(i0);
+  }
+  __syncthreads();
+  uint32_t phase = 0;
   for (int i = i0; i < i1; ++i) {
-    uint32_t nx[E];
-    if (i + 1 < i1) load_natural<G>(nx, drow + (size_t)(i + 1) * G::N, tid);
+    uint32_t x[E];
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = stage[natural_index<G>(tid, e)];
+    __syncthreads();  // every thread has read the stage
+    if (tid == 0 && i + 1 < i1) fetch(i + 1);
     if (reduce_digits) {
 #pragma unroll
       for (int e = 0; e < E; ++e) x[e] = reduce64(x[e], p, mu);
     }
     ntt_fwd<G, 1, true>(x, s, tw, p, tid);
     store_tiled<G>(x, orow + (size_t)i * G::N, tid);
-#pragma unroll
-    for (int e = 0; e < E; ++e) x[e] = nx[e];
   }
 }
 
 // Step 3 at 1024 threads: per part, the three one-row inverses mod r0, r1, r2
-// (next row's loads issued first; the first two results parked in TMEM),
-// then that part's CRT and store.
+// (each next row staged by TMA; the first two results parked in TMEM), then
+// that part's CRT and store.
 template <class G>
 __global__ void __launch_bounds__(G::T, 1)
     k_rb_inv1(const uint32_t* __restrict__ zspec, const uint32_t* __restrict__ y3, uint32_t* __restrict__ out,
               int K, RbTabs rb, NttTabs nt) {
   extern __shared__ __align__(16) uint32_t s[];
   __shared__ uint32_t tmem_slot;
+  __shared__ __align__(8) uint64_t bar;
   constexpr int E = G::E;
   static_assert(E == 16, "TMEM parking in 16-column chunks");
   const int tid = threadIdx.x;
@@ -973,20 +993,41 @@ __global__ void __launch_bounds__(G::T, 1)
   const size_t ct = blockIdx.y;
   const uint32_t* zr = zspec + (ct * K + j) * (size_t)RB_A * 2 * G::N;
   constexpr uint32_t COLS = tmem_stash_cols<G, 2 * E>();
-  const uint32_t tbase = tmem_stash_alloc(&tmem_slot, COLS, tid, 2 * E);
+  uint32_t* stage = s + G::ntt_smem_words(1);
+  auto fetch = [&](int row) {  // row (a, part) = 2 a + part
+    fence_proxy_async();
+    mbar_expect_tx(&bar, G::N * 4);
+    bulk_g2s(stage, zr + (size_t)row * G::N, G::N * 4, &bar);
+  };
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    fetch(0);  // (a = 0, part 0)
+  }
+  const uint32_t tbase = tmem_stash_alloc(&tmem_slot, COLS, tid, 2 * E);  // (synchronises the CTA)
   const uint32_t q = nt.prime[j];
   const uint32_t qinv = nt.pinv[j];
   const uint32_t c0 = rb.crt_q[j][0], c1 = rb.crt_q[j][1], c2 = rb.crt_q[j][2];
   const uint32_t cR = rb.negR_q[j];
-  uint32_t x[E];
-  load_tiled<G>(x, zr, tid);  // row (a = 0, part 0)
+  uint32_t phase = 0;
 #pragma unroll 1
   for (int part = 0; part < 2; ++part) {
 #pragma unroll
     for (int a = 0; a < RB_A; ++a) {
-      uint32_t nx[E];
+      uint32_t x[E];
+      mbar_wait(&bar, phase);
+      phase ^= 1;
+      {
+        const uint4* v = reinterpret_cast<const uint4*>(stage) + tid;
+#pragma unroll
+        for (int k = 0; k < E / 4; ++k) {
+          const uint4 w4 = v[k * G::T];
+          x[4 * k] = w4.x, x[4 * k + 1] = w4.y, x[4 * k + 2] = w4.z, x[4 * k + 3] = w4.w;
+        }
+      }
+      __syncthreads();  // every thread has read the stage
       const int nxt = a + 1 < RB_A ? 2 * (a + 1) + part : (part == 0 ? 1 : -1);  // next (a, part) row
-      if (nxt >= 0) load_tiled<G>(nx, zr + (size_t)nxt * G::N, tid);
+      if (tid == 0 && nxt >= 0) fetch(nxt);
       const int jj = rb.roff + a;
       ntt_inv<G, 1>(x, s, nt.itw + (size_t)jj * G::N, nt.prime[jj], InvScale{rb.isc_n[a], rb.isc_nw[a]}, tid);
       if (a + 1 < RB_A) {
@@ -1005,10 +1046,6 @@ __global__ void __launch_bounds__(G::T, 1)
           const int idx = natural_index<G>(tid, e);
           o[idx] = add_mod(redc(acc, q, qinv), yr[idx], q);
         }
-      }
-      if (nxt >= 0) {
-#pragma unroll
-        for (int e = 0; e < E; ++e) x[e] = nx[e];
       }
     }
   }
@@ -1193,9 +1230,9 @@ void configure_smem() {
   cudaFuncSetAttribute(k_encrypt<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if constexpr (rb_geom1<G>()) {
     cudaFuncSetAttribute(k_rb_fwd1<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         G::ntt_smem_words(1) * sizeof(uint32_t));
+                         rb1_smem_words<G>() * sizeof(uint32_t));
     cudaFuncSetAttribute(k_rb_inv1<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         G::ntt_smem_words(1) * sizeof(uint32_t));
+                         rb1_smem_words<G>() * sizeof(uint32_t));
   }
   if constexpr (rb_geom<G>()) {
     cudaFuncSetAttribute(k_rb_fwd<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1330,10 +1367,10 @@ cudaError_t launch_with(int op, const NttLaunch& a) {
     case 8:  // step 3: inverse mod r_a, exact CRT to q_j, + (y0, y1)
       if constexpr (rb_geom1<G>()) {
         if (op == 7)
-          k_rb_fwd1<G><<<a.grid, G::T, G::ntt_smem_words(1) * sizeof(uint32_t), a.stream>>>(
+          k_rb_fwd1<G><<<a.grid, G::T, rb1_smem_words<G>() * sizeof(uint32_t), a.stream>>>(
               a.dig, a.out, a.D, a.reduce_digits, a.rb, a.nt);
         else
-          k_rb_inv1<G><<<a.grid, G::T, G::ntt_smem_words(1) * sizeof(uint32_t), a.stream>>>(
+          k_rb_inv1<G><<<a.grid, G::T, rb1_smem_words<G>() * sizeof(uint32_t), a.stream>>>(
               a.a, a.y3, a.out, a.K, a.rb, a.nt);
       } else if constexpr (rb_geom<G>()) {
         if (op == 7)
