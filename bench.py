@@ -207,6 +207,7 @@ def s8d_modmuls(name: str, K: int, KP: int, D: int, N: int, cts: float, logq: in
     split over the kernels that do the work; 3 IMAD per modmul (Shoup)."""
     B = (N // 2) * (N.bit_length() - 1)
     L = K + KP
+    name = name[:-3] if name.endswith("_tc") else name  # same work, tensor-core dots
     if name == "k_tensor":  # 2 fwd + 3 inv NTTs over Q u P, 3 pointwise products
         m = (2 * L + 3 * L) * B + 3 * L * N
     elif name == "k_relin":  # D fwd + 2 inv NTTs over Q, 2 D pointwise MACs
@@ -234,6 +235,13 @@ def kernel_work(name: str, K: int, KP: int, D: int, N: int, cts: float):
     logn = N.bit_length() - 1
     bfly = (N // 2) * logn
     L = K + KP
+    if name == "k_scale_tc":  # the dot products on the tensor cores; per part: K Shoup + fixed
+        # point, KP x (REDC + 2 Shoup + fixed point), K x REDC on the integer pipe
+        part = K * 4 + K * 2 + KP * (3 + 2 * 4 + 2) + K * 3
+        digits = K * 4 + K * 2 + (K + 1) * (K * 2 + 2)
+        return 4 * N * (3 * L + 3 * K + D) * cts, N * (3 * part + digits) * cts
+    if name == "k_extend_tc":  # per part: K Shoup, fixed point, KP x REDC (dots on the tensor cores)
+        return 4 * N * 2 * (K + KP) * cts, 2 * N * (K * 4 + K * 2 + KP * 3) * cts
     if name == "k_tensor":  # 2 fwd + 3 inv NTT per prime, 3 products, N^-1 scaling
         slots = L * (5 * bfly * 4 + 3 * N * 8 + 3 * N * 4)
         byts = L * N * 4 * (2 + 3)

@@ -63,8 +63,10 @@ enum {
   HCNN_Q_WS_BYTES = 5, /* workspace currently held */
   HCNN_Q_KERNELS = 6,  /* kernels launched since creation */
   HCNN_Q_NTT_VARIANT = 7,
-  HCNN_Q_RELIN_RBASIS = 8  /* 1 when relinearisations of at least HCNN_OPT_RB_MIN_BATCH ciphertexts take
+  HCNN_Q_RELIN_RBASIS = 8, /* 1 when relinearisations of at least HCNN_OPT_RB_MIN_BATCH ciphertexts take
                               the shared-basis R path (flag + parameters) */
+  HCNN_Q_TC_BCONV = 9      /* 1 when the multiply's base conversions run on the tensor cores (flag 32768
+                              + parameters) */
 };
 /* Tuning options.  HCNN_OPT_NTT_VARIANT: geometry flags of the fused NTT
  * kernels: 16 one-row relinearisation, 32 radix-32 square tensor, 64
@@ -75,8 +77,10 @@ enum {
  * prefetch of the next item's rows), 16384 relinearisation over a shared
  * three-prime basis R (digit NTTs mod 3 primes instead of mod every q_j, exact
  * CRT back; N = 2^12 to 2^15 (2-CTA clusters at 2^15), at most 23 digits,
- * at least 8 primes).  Default per N: 8192|16384 at 2^13,
- * 64|1024|4096|16384 at 2^14, 512|2048|16384 at 2^15, 0 otherwise.
+ * at least 8 primes), 32768 the multiply's exact base conversions (k_extend,
+ * k_scale) as u8 x u8 -> s32 tcgen05 MMAs (at most 15 primes in Q and P,
+ * N >= 128).  Default per N: 32768 plus 8192|16384 at 2^13,
+ * 64|1024|4096|16384 at 2^14, 512|2048|16384 at 2^15.
  * Results are identical for every setting. */
 /* HCNN_OPT_TS_CHUNK: ciphertexts per extend/tensor/scale sub-chunk of a
  * multiply (the tensor's output of one sub-chunk stays in L2 for the scale

@@ -7,9 +7,12 @@
 //             + base-w digits of the canonical c2           (bfv.py:350-365)
 //   k_digits  base-w digits of part 2 of a 3-part ct         (bfv.py:350-365)
 #pragma once
+#include <cstdlib>
 #include "common.cuh"
 
 namespace hcnn {
+
+struct TcTabs;
 
 struct ConvLaunch {
   cudaStream_t stream;
@@ -18,6 +21,8 @@ struct ConvLaunch {
   uint32_t* out;
   uint32_t* dig;
   int N;
+  const TcTabs* tc;  // ops 4 / 5: the tensor-core conversion matrices (tc_bconv.cuh)
+  size_t tiles;      // ops 4 / 5: 128-coefficient tiles
 };
 
 // write the D base-2^db digits of the canonical value held in S
@@ -225,10 +230,67 @@ __global__ void __launch_bounds__(128)
   m[ct * N + n] = r;
 }
 
-// op: 0 extend, 1 scale, 2 digits, 3 decrypt rounding
+}  // namespace hcnn
+
+#include "tc_bconv.cuh"
+
+namespace hcnn {
+
+// resident CTAs per SM of the tensor-core conversions (TMEM: 64 columns each,
+// at most 8; registers: 7 at __launch_bounds__(128, 7))
+constexpr int TC_CTAS_PER_SM = 7;
+
+// op: 0 extend, 1 scale, 2 digits, 3 decrypt rounding,
+//     4 extend / 5 scale on the tensor cores (K, KP <= 15, N % 128 == 0)
 template <int K, int KP>
 cudaError_t conv_launch(int op, const ConvLaunch& a, const ConvTabs& tb) {
   switch (op) {
+    case 4:
+    case 5: {
+      if constexpr (K <= 15 && KP <= 15) {
+        static_assert(sizeof(TcSmem) <= 48 * 1024, "no opt-in needed");
+        // resident CTAs per SM, per device and kernel (the occupancy query
+        // costs host time: once per device)
+        static int slots[2][2][64];
+        const char* ce = getenv("HCNN_TC_COLS");  // tuning probe
+        const bool wide = ce && atoi(ce) == 128;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        int& per = slots[op - 4][wide][dev & 63];
+        if (per == 0) {
+          // __launch_bounds__(128, 7) caps the registers at 72: 7 CTAs fit by
+          // registers, shared memory (17 KB each) and TMEM (64 columns each;
+          // 4 CTAs with 128)
+          int sms = 0;
+          cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+          int occ = wide ? 4 : TC_CTAS_PER_SM;
+          if (const char* e = getenv("HCNN_TC_CTAS")) {  // tuning probe
+            const int c = atoi(e);
+            if (c > 0 && c < occ) occ = c;
+          }
+          per = sms * occ;
+        }
+        const size_t cap = (size_t)per;
+        const unsigned grid = (unsigned)(a.tiles < cap ? a.tiles : cap);
+        if (grid == 0) return cudaSuccess;
+        if (op == 4) {
+          if (wide)
+            k_extend_tc<K, KP, 128><<<grid, TC_M, sizeof(TcSmem), a.stream>>>(a.in, a.out, a.N, a.tiles, tb, *a.tc);
+          else
+            k_extend_tc<K, KP, 64><<<grid, TC_M, sizeof(TcSmem), a.stream>>>(a.in, a.out, a.N, a.tiles, tb, *a.tc);
+        } else {
+          if (wide)
+            k_scale_tc<K, KP, 128><<<grid, TC_M, sizeof(TcSmem), a.stream>>>(a.in, a.out, a.dig, a.N, a.tiles, tb,
+                                                                              *a.tc);
+          else
+            k_scale_tc<K, KP, 64><<<grid, TC_M, sizeof(TcSmem), a.stream>>>(a.in, a.out, a.dig, a.N, a.tiles, tb,
+                                                                             *a.tc);
+        }
+        break;
+      } else {
+        return cudaErrorInvalidValue;
+      }
+    }
     case 0:
       k_extend<K, KP><<<a.grid, a.block, 0, a.stream>>>(a.in, a.out, a.N, tb);
       break;

@@ -136,6 +136,11 @@ struct hcnn_ctx {
   RbTabs rb{};
   uint32_t* d_rlk_rb = nullptr;  // [RB_A][D][2K][N] NTT domain mod r_a, tiled
   bool rb_keys = false;
+  // base conversions on the tensor cores (TC_BCONV, tc_bconv.cuh): usable
+  // when K, KP <= 15 and 128 | N
+  bool tc_ok = false;
+  uint32_t* d_tcb = nullptr;  // the two 4 KB byte matrices
+  TcTabs tc{};
   uint2* d_delta = nullptr;
   bool rlk_reduce = false;
   uint8_t* ws = nullptr;
@@ -422,6 +427,33 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
   }
   for (int w2 = 0; w2 < WMAX; ++w2) tb.h_w[w2] = h.word(w2);
 
+  // tensor-core conversion matrices (tc_bconv.cuh): B[4o+e][4i+b] =
+  // byte e of (2^8b c_io 2^32 mod m_o); input i = nin is the overflow count v
+  c->tc_ok = c->K <= 15 && c->KP <= 15 && N % TC_M == 0;
+  if (c->tc_ok) {
+    std::vector<uint8_t> hb(2 * TC_N * TC_KB, 0);
+    auto fill = [&](uint8_t* B, uint32_t nin, uint32_t nout, auto cin, auto cv, auto mod) {
+      for (uint32_t o = 0; o < nout; ++o) {
+        const u64 m = mod(o);
+        for (uint32_t i = 0; i <= nin; ++i) {
+          const u64 cc = i < nin ? cin(i, o) : cv(o);
+          for (int b = 0; b < (i < nin ? 4 : 1); ++b) {
+            const u64 cp = mont_form(mulmod64(cc, ((u64)1 << (8 * b)) % m, m), m);
+            for (int e = 0; e < 4; ++e) B[tc_off(4 * (int)o + e, 4 * (int)i + b)] = (uint8_t)(cp >> (8 * e));
+          }
+        }
+      }
+    };
+    fill(hb.data(), c->K, c->KP, [&](uint32_t i, uint32_t j) { return mod_small(div_small(Q, q[i]), P[j]); },
+         [&](uint32_t j) { return (P[j] - mod_small(Q, P[j])) % P[j]; }, [&](uint32_t j) { return P[j]; });
+    fill(hb.data() + TC_N * TC_KB, c->KP, c->K,
+         [&](uint32_t j, uint32_t i) { return mod_small(div_small(Pp, P[j]), q[i]); },
+         [&](uint32_t i) { return (q[i] - mod_small(Pp, q[i])) % q[i]; }, [&](uint32_t i) { return q[i]; });
+    CK(cudaMalloc(&c->d_tcb, hb.size()));
+    CK(cudaMemcpy(c->d_tcb, hb.data(), hb.size(), cudaMemcpyHostToDevice));
+    c->tc = TcTabs{c->d_tcb, c->d_tcb + TC_N * TC_KB / 4};
+  }
+
   // upload
   CK(cudaMalloc(&c->d_prime, L * sizeof(uint32_t)));
   CK(cudaMalloc(&c->d_mu, L * sizeof(uint64_t)));
@@ -502,6 +534,9 @@ unsigned cdiv(size_t a, size_t b) { return (unsigned)((a + b - 1) / b); }
 
 // variant bit: relinearisation over the shared basis R (relin_rb.cuh)
 constexpr int RELIN_RBASIS = 16384;
+constexpr int TC_BCONV = 32768;  // k_extend / k_scale on the tensor cores (tc_bconv.cuh)
+
+bool tc_active(const hcnn_ctx* c) { return (c->variant & TC_BCONV) && c->tc_ok; }
 
 bool rb_active(const hcnn_ctx* c) {
   if (!(c->variant & RELIN_RBASIS) || !c->rb_ok) return false;
@@ -671,20 +706,24 @@ void mul_chunk(hcnn_ctx* c, const uint32_t* a, const uint32_t* b, size_t nct, ui
   ConvLaunch ca{};
   ca.block = dim3(tpb);
   ca.grid = dim3(cdiv(N, tpb), (unsigned)(nct * 2));
+  const bool tc = tc_active(c);
+  ca.tc = &c->tc;
+  ca.tiles = nct * 2 * (N / TC_M);
   ca.in = a;
   ca.out = ae;
-  conv_dispatch(c, 0, ca, "k_extend");
+  conv_dispatch(c, tc ? 4 : 0, ca, tc ? "k_extend_tc" : "k_extend");
   if (!square) {
     ca.in = b;
     ca.out = be;
-    conv_dispatch(c, 0, ca, "k_extend");
+    conv_dispatch(c, tc ? 4 : 0, ca, tc ? "k_extend_tc" : "k_extend");
   }
   launch_tensor(c, a, ae, b, be, d, nct, square ? 1 : 0);
   ca.grid = dim3(cdiv(N, tpb), (unsigned)(nct * 3));
+  ca.tiles = nct * 3 * (N / TC_M);
   ca.in = d;
   ca.out = y3;
   ca.dig = dig;
-  conv_dispatch(c, 1, ca, "k_scale");
+  conv_dispatch(c, tc ? 5 : 1, ca, tc ? "k_scale_tc" : "k_scale");
   (void)K;
 }
 
@@ -1046,11 +1085,11 @@ void layout_key(hcnn_ctx* c, const uint32_t* raw, int domain, size_t rows, uint3
 
 void prepare_keys(hcnn_ctx* c) {
   if (rb_active(c)) prepare_rb_keys(c);
-  if (c->keys_variant == (c->variant & ~(32 | 1024 | 2048 | 4096 | 8192 | RELIN_RBASIS))) return;
+  if (c->keys_variant == (c->variant & ~(32 | 1024 | 2048 | 4096 | 8192 | RELIN_RBASIS | TC_BCONV))) return;
   if (c->d_rlk_raw)
     layout_key(c, c->d_rlk_raw, c->rlk_domain, (size_t)c->D * 2 * c->K, &c->d_rlk, variant_mont(c, c->variant));
   if (c->d_pk_raw) layout_key(c, c->d_pk_raw, c->pk_domain, 2 * (size_t)c->K, &c->d_pk, 0);
-  c->keys_variant = c->variant & ~(32 | 1024 | 2048 | 4096 | 8192 | RELIN_RBASIS);
+  c->keys_variant = c->variant & ~(32 | 1024 | 2048 | 4096 | 8192 | RELIN_RBASIS | TC_BCONV);
 }
 
 }  // namespace
@@ -1368,8 +1407,13 @@ int hcnn_ctx_create(hcnn_ctx** out, uint32_t n, uint32_t k, const uint64_t* prim
     // shuffle-tail radix-16 kernels up to 2^13 (persistent square tensor and
     // relinearisation over R at 2^13: profiles/r2/micro_rbasis.jsonl),
     // mixed-width passes at 2^14, 2-CTA cluster relinearisation at 2^15
-    c->variant = c->logN == 13 ? (8192 | RELIN_RBASIS) : c->logN == 14 ? (64 | 1024 | 4096 | RELIN_RBASIS)
-                 : c->logN == 15 ? (512 | 2048 | RELIN_RBASIS) : 0;
+    // base conversions on the tensor cores wherever the parameters allow
+    // (MNIST set 1 17.58 -> 16.66 ms, set 3 38.3 -> 36.4 ms, CIFAR set 5
+    // -4 %: tools/tc_sweep.sh, tools/tc_ab.sh)
+    c->variant = TC_BCONV | (c->logN == 13   ? (8192 | RELIN_RBASIS)
+                             : c->logN == 14 ? (64 | 1024 | 4096 | RELIN_RBASIS)
+                             : c->logN == 15 ? (512 | 2048 | RELIN_RBASIS)
+                                             : 0);
     build_tables(c.get(), q, t);
     *out = c.release();
   });
@@ -1389,6 +1433,7 @@ int hcnn_ctx_destroy(hcnn_ctx* c) {
     if (c->d_rlk) cudaFree(c->d_rlk);
     if (c->d_rlk_raw) cudaFree(c->d_rlk_raw);
     if (c->d_rlk_rb) cudaFree(c->d_rlk_rb);
+    if (c->d_tcb) cudaFree(c->d_tcb);
     if (c->d_pk_raw) cudaFree(c->d_pk_raw);
     cudaFree(c->d_pinv);
     if (c->d_pk) cudaFree(c->d_pk);
@@ -1459,8 +1504,8 @@ int hcnn_ctx_set_option(hcnn_ctx* c, int key, int64_t value) {
       // geometry flags of the fused kernels (ntt_kernels.cuh): +16 one-row
       // relinearisation transforms, +32 square tensors on the radix-32 mixed
       // geometry, +64 mixed-width passes instead of a warp-shuffle tail
-      if (value & ~(int64_t)(16 | 32 | 64 | 512 | 1024 | 2048 | 4096 | 8192 | RELIN_RBASIS))
-        fail(HCNN_ERR_PARAM, "NTT variant flags are 16, 32, 64, 512, 1024, 2048, 4096, 8192 and 16384");
+      if (value & ~(int64_t)(16 | 32 | 64 | 512 | 1024 | 2048 | 4096 | 8192 | RELIN_RBASIS | TC_BCONV))
+        fail(HCNN_ERR_PARAM, "NTT variant flags are 16, 32, 64, 512, 1024, 2048, 4096, 8192, 16384 and 32768");
       if ((value & (32 | 64)) && c->logN < 10) fail(HCNN_ERR_UNSUPPORTED, "mixed geometries need N >= 1024");
       if ((value & 512) && c->logN != 15 && c->logN != 14)
         fail(HCNN_ERR_UNSUPPORTED, "cluster kernels are for N = 2^14 and 2^15");
@@ -1492,6 +1537,7 @@ int64_t hcnn_ctx_query(hcnn_ctx* c, int what) {
     case HCNN_Q_KERNELS: return c->launches;
     case HCNN_Q_NTT_VARIANT: return c->variant;
     case HCNN_Q_RELIN_RBASIS: return rb_active(c) ? 1 : 0;
+    case HCNN_Q_TC_BCONV: return tc_active(c) ? 1 : 0;
     default: return -1;
   }
 }

@@ -1,0 +1,133 @@
+"""Base conversions on the tensor cores (flag TC_BCONV = 32768,
+csrc/tc_bconv.cuh): the multiply's Q -> P extension (k_extend) and its exact
+t/q scale-and-round (k_scale, both conversions) as u8 x u8 -> s32 tcgen05
+MMAs.  Whatever the flag, every output limb must equal the reference's
+hmult_raw / hsquare (bfv.py:331-347, 407-443): checked against the integer
+kernels on random and extreme inputs and against the pinned oracle."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import hcnn_oracle as O  # noqa: E402
+from helpers import ct_array  # noqa: E402
+
+from paper_1811_00778_b200 import _lib  # noqa: E402
+from paper_1811_00778_b200 import bfv as B  # noqa: E402
+from paper_1811_00778_b200 import engine as E  # noqa: E402
+from paper_1811_00778_b200 import ops  # noqa: E402
+
+TC = 32768
+Q_TC = 9
+
+
+def dev(arr):
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(arr).astype(np.uint32)).view(np.int32)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy().view(np.uint32).astype(np.int64)
+
+
+def _primes(n, k):
+    out, c = [], (1 << 30) // (2 * n)
+    while len(out) < k:
+        p = c * 2 * n + 1
+        if p < (1 << 30) and all(p % d for d in range(3, int(p ** 0.5) + 1, 2)):
+            out.append(p)
+        c -= 1
+    return out
+
+
+def _two_part(primes, n, rng, count):
+    """[count][2][K][N] canonical residues; the first rows hold q - 1, 0,
+    (q-1)/2 and (q+1)/2 in every limb (lifts at the edges of [0, q) and at the
+    centre, where the CRT overflow estimate is decided exactly)"""
+    k = len(primes)
+    p = np.array(primes, dtype=np.int64)[:, None]
+    x = rng.integers(0, 1 << 62, (count, 2, k, n)) % p
+    x[0, 0] = p - 1
+    x[0, 1] = 0
+    x[1, 0] = (p - 1) // 2
+    x[1, 1] = (p + 1) // 2 % p
+    return x
+
+
+@pytest.mark.parametrize("n,k,t", [(8192, 11, 5522259017729), (8192, 6, 65537), (1024, 4, 257),
+                                   (16384, 11, 5522259017729), (32768, 12, 65537), (4096, 13, 65537),
+                                   (8192, 10, 2424833)])
+def test_tc_hmult_raw_equals_integer_kernels(n, k, t):
+    """hmult_raw (square and general) with the flag on and off agree bit for
+    bit; the flag is reported active."""
+    E._CTXS.clear()
+    primes = _primes(n, k)
+    params = B.BfvParams(B.RnsContext(n, primes), t)
+    g = E.context_for(params)
+    rng = np.random.default_rng(n + k)
+    a = dev(_two_part(primes, n, rng, 5))
+    b = dev(_two_part(primes, n, rng, 5)[::-1])
+    base = g.variant() & ~TC
+    g.set_variant(base)
+    assert _lib.lib().hcnn_ctx_query(g.handle, Q_TC) == 0
+    want_sq = host(ops.hmult_raw_device(g, a, a))
+    want = host(ops.hmult_raw_device(g, a, b))
+    g.set_variant(base | TC)
+    assert _lib.lib().hcnn_ctx_query(g.handle, Q_TC) == 1
+    g.profile(True)
+    got_sq = host(ops.hmult_raw_device(g, a, a))
+    names = set(g.profile_read())
+    g.profile(False)
+    assert {"k_extend_tc", "k_scale_tc"} <= names and "k_scale" not in names, names
+    got = host(ops.hmult_raw_device(g, a, b))
+    assert np.array_equal(got_sq, want_sq)
+    assert np.array_equal(got, want)
+    E._CTXS.clear()
+
+
+@pytest.mark.parametrize("n,k", [(8192, 11), (16384, 8)])
+def test_tc_hsquare_vs_oracle(n, k):
+    """HSquare (digits of the scaled c2 feed the relinearisation) with the flag
+    on equals the oracle's hmult_raw + relinearize on fresh encryptions."""
+    E._CTXS.clear()
+    primes = _primes(n, k)
+    t = 65537
+    params = B.BfvParams(B.RnsContext(n, primes), t)
+    _, pk, rlk = B.keygen(params, np.random.default_rng(n))
+    rng = np.random.default_rng(n + 1)
+    cts = [B.encrypt(pk, B.Plaintext(rng.integers(0, t, n), t), params, rng) for _ in range(3)]
+    g = E.context_for(params)
+    g.set_variant(g.variant() | TC)
+    assert _lib.lib().hcnn_ctx_query(g.handle, Q_TC) == 1
+    x = dev(np.stack([ct_array(c) for c in cts]))
+    got = host(ops.square_device(g, x, rlk))
+    op = O.Params(O.Context(n, primes), t)
+    orlk = [(k0.residues, k1.residues) for k0, k1 in rlk.components]
+    for i, c in enumerate(cts):
+        ref3 = O.hmult_raw(op, (c.parts[0].residues, c.parts[1].residues))
+        assert np.array_equal(got[i], np.stack(O.relinearize(op, ref3, orlk)))
+    E._CTXS.clear()
+
+
+def test_tc_unavailable_for_16_primes():
+    """K = 16 (4 K + 1 bytes exceed the 64-byte MMA row): the flag is accepted
+    and the integer kernels run."""
+    E._CTXS.clear()
+    n = 1024
+    primes = _primes(n, 16)
+    params = B.BfvParams(B.RnsContext(n, primes), 65537)
+    g = E.context_for(params)
+    g.set_variant(g.variant() | TC)
+    assert _lib.lib().hcnn_ctx_query(g.handle, Q_TC) == 0
+    a = dev(_two_part(primes, n, np.random.default_rng(1), 2))
+    g.profile(True)
+    ops.hmult_raw_device(g, a, a)
+    names = set(g.profile_read())
+    g.profile(False)
+    assert "k_scale" in names and "k_scale_tc" not in names
+    E._CTXS.clear()
