@@ -540,7 +540,7 @@ def run_ours(args):
                         "imad_slots_per_launch": ops},
                 "avg_launch_ms": round(avg_s * 1e3, 4),
                 "share_of_step": round(tot / total_ms, 4),
-                "note": "integer-pipe kernel: tensor cores unused by design; DESIGN.md section 4",
+                "note": "integer-pipe kernel (NTT butterflies); the base conversions around it run on the tensor cores (k_extend_tc, k_scale_tc: DESIGN.md section 4.2)",
             }
             mm = s8d_modmuls(dom, g0.K, g0.KP, g0.D, g0.N, n_sq / cnt)
             if mm:
