@@ -431,7 +431,7 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
   // byte e of (2^8b c_io 2^32 mod m_o); input i = nin is the overflow count v
   c->tc_ok = c->K <= 15 && c->KP <= 15 && N % TC_M == 0;
   if (c->tc_ok) {
-    std::vector<uint8_t> hb(2 * TC_N * TC_KB, 0);
+    std::vector<uint8_t> hb(3 * TC_N * TC_KB, 0);
     auto fill = [&](uint8_t* B, uint32_t nin, uint32_t nout, auto cin, auto cv, auto mod) {
       for (uint32_t o = 0; o < nout; ++o) {
         const u64 m = mod(o);
@@ -449,9 +449,27 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
     fill(hb.data() + TC_N * TC_KB, c->KP, c->K,
          [&](uint32_t j, uint32_t i) { return mod_small(div_small(Pp, P[j]), q[i]); },
          [&](uint32_t i) { return (q[i] - mod_small(Pp, q[i])) % q[i]; }, [&](uint32_t i) { return q[i]; });
+    // the digits' canonical lift: row s = byte s of sum_i xt_i (q/q_i) + V (2^(32 W) - q),
+    // W = words_for(K) (the words the kernel carries; the lift is < 2q there)
+    {
+      uint8_t* B = hb.data() + 2 * TC_N * TC_KB;
+      const int W = words_for((int)c->K);
+      auto byte_of = [](const Big& x, int k) { return (uint8_t)(x.word(k / 4) >> (8 * (k % 4))); };
+      for (uint32_t i = 0; i < c->K; ++i) {
+        const Big qh = div_small(Q, q[i]);
+        for (int b = 0; b < 4; ++b)
+          for (int sb = b; sb < 4 * W; ++sb) B[tc_off(sb, 4 * (int)i + b)] = byte_of(qh, sb - b);
+      }
+      uint64_t cy = 1;
+      for (int w2 = 0; w2 < W; ++w2) {  // two's complement words of q
+        const uint64_t x = (uint64_t)(~Q.word(w2) & 0xffffffffu) + cy;
+        cy = x >> 32;
+        for (int u = 0; u < 4; ++u) B[tc_off(4 * w2 + u, 4 * (int)c->K)] = (uint8_t)(x >> (8 * u));
+      }
+    }
     CK(cudaMalloc(&c->d_tcb, hb.size()));
     CK(cudaMemcpy(c->d_tcb, hb.data(), hb.size(), cudaMemcpyHostToDevice));
-    c->tc = TcTabs{c->d_tcb, c->d_tcb + TC_N * TC_KB / 4};
+    c->tc = TcTabs{c->d_tcb, c->d_tcb + TC_N * TC_KB / 4, c->d_tcb + 2 * TC_N * TC_KB / 4};
   }
 
   // upload

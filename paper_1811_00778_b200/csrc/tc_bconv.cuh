@@ -39,6 +39,9 @@ constexpr int TC_LBO = 128, TC_SBO = 512;
 struct TcTabs {
   const uint32_t* bqp;  // Q -> P: rows 4j+e (j < KP), K bytes 4i+b (i < K), 4K = v
   const uint32_t* bpq;  // P -> Q: rows 4i+e (i < K), K bytes 4j+b (j < KP), 4KP = v
+  const uint32_t* bdg;  // canonical lift for the digits: row s (byte s of the
+                        // lift), K byte 4i+b: byte s-b of q/q_i; 4K: byte s of
+                        // 2^(32 W) - q
 };
 
 // byte offset of (row, k) in a core-matrix tile
@@ -154,6 +157,7 @@ struct TcSmem {
   uint8_t a[TC_TILE_BYTES];
   uint8_t bqp[TC_N * TC_KB];
   uint8_t bpq[TC_N * TC_KB];
+  uint8_t bdg[TC_N * TC_KB];
   uint64_t bar;
   uint32_t tmem;
 };
@@ -237,6 +241,7 @@ __global__ void __launch_bounds__(TC_M, 7)
   const int tid = threadIdx.x, warp = tid >> 5;
   tc_load_b(sm.bqp, tc.bqp);
   tc_load_b(sm.bpq, tc.bpq);
+  if (dig != nullptr) tc_load_b(sm.bdg, tc.bdg);
   if (tid == 0) {
     mbar_init(&sm.bar, 1);
     fence_mbar_init();
@@ -311,21 +316,61 @@ __global__ void __launch_bounds__(TC_M, 7)
     uint32_t* dst = y3 + row * K * N + n;
 #pragma unroll
     for (int i = 0; i < K; ++i) dst[(size_t)i * N] = yq[i];
-    if (part == 2 && dig != nullptr) {
-      uint32_t xt[K];
-#pragma unroll
-      for (int i = 0; i < K; ++i) xt[i] = mul_shoup(yq[i], tb.qhi[i], tb.qhis[i], tb.q[i]);
-      uint64_t Fq = 0;
-#pragma unroll
-      for (int i = 0; i < K; ++i) Fq += frac59(xt[i], tb.qg[i], tb.qk[i]);
+    if (part == 2 && dig != nullptr) {  // uniform over the tile
+      // canonical binary of y_2 mod q: sum_i xt_i (q/q_i) - V q as bytes on
+      // the tensor cores (exact mod 2^(32 W), the value lies in [0, 2q)),
+      // words by one carry pass, then at most one more q off
       uint32_t S[words_for(K)];
-      mw_lift<K>(xt, tb, S);
-      mw_sub_mq<K>(S, (uint32_t)(Fq >> FRAC_BITS), tb);
+      {
+        uint32_t xt[K];
+        uint64_t Fq = 0;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          xt[i] = mul_shoup(yq[i], tb.qhi[i], tb.qhis[i], tb.q[i]);
+          Fq += frac59(xt[i], tb.qg[i], tb.qk[i]);
+        }
+        tc_put_row<K>(sm.a, tid, xt, (uint32_t)(Fq >> FRAC_BITS));
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      __syncthreads();  // every lane has drained the P -> Q sums
+      if (tid == 0) {
+        tc_fence_after();
+        tc_mma64(tbase, sm.a, sm.bdg);
+        tc_commit(&sm.bar);
+      }
+      mbar_wait(&sm.bar, phase);
+      phase ^= 1;
+      tc_fence_after();
+      {
+        uint64_t carry = 0;
+#pragma unroll
+        for (int g = 0; g < (words_for(K) + 3) / 4; ++g) {
+          uint32_t v[16];
+          tc_ld16(tlane + 16 * g, v);
+          tc_wait_ld();
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int w = 4 * g + u;
+            if (w < words_for(K)) {
+              const uint64_t x = carry + v[4 * u] + ((uint64_t)v[4 * u + 1] << 8) +
+                                 ((uint64_t)v[4 * u + 2] << 16) + ((uint64_t)v[4 * u + 3] << 24);
+              S[w] = (uint32_t)x;
+              carry = x >> 32;
+            }
+          }
+        }
+      }
       {
         uint32_t Tq[words_for(K)];
+        uint32_t borrow = 0;
 #pragma unroll
-        for (int w = 0; w < words_for(K); ++w) Tq[w] = S[w];
-        if (!mw_sub_mq<K>(Tq, 1, tb)) {
+        for (int w = 0; w < words_for(K); ++w) {
+          const uint64_t d = (uint64_t)S[w] - tb.q_w[w] - borrow;
+          Tq[w] = (uint32_t)d;
+          borrow = (uint32_t)(d >> 63);
+        }
+        if (!borrow) {
 #pragma unroll
           for (int w = 0; w < words_for(K); ++w) S[w] = Tq[w];
         }
