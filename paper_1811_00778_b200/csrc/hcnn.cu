@@ -431,7 +431,7 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
   // byte e of (2^8b c_io 2^32 mod m_o); input i = nin is the overflow count v
   c->tc_ok = c->K <= 15 && c->KP <= 15 && N % TC_M == 0;
   if (c->tc_ok) {
-    std::vector<uint8_t> hb(3 * TC_N * TC_KB, 0);
+    std::vector<uint8_t> hb(4 * TC_N * TC_KB, 0);
     auto fill = [&](uint8_t* B, uint32_t nin, uint32_t nout, auto cin, auto cv, auto mod) {
       for (uint32_t o = 0; o < nout; ++o) {
         const u64 m = mod(o);
@@ -446,6 +446,13 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
     };
     fill(hb.data(), c->K, c->KP, [&](uint32_t i, uint32_t j) { return mod_small(div_small(Q, q[i]), P[j]); },
          [&](uint32_t j) { return (P[j] - mod_small(Q, P[j])) % P[j]; }, [&](uint32_t j) { return P[j]; });
+    // the scale's Q -> P conversion with -E_j folded in: (p_j - r_j) E_j directly
+    fill(hb.data() + 3 * TC_N * TC_KB, c->K, c->KP,
+         [&](uint32_t i, uint32_t j) {
+           return mulmod64(mod_small(div_small(Q, q[i]), P[j]), (P[j] - tb.Ej[j]) % P[j], P[j]);
+         },
+         [&](uint32_t j) { return mulmod64((P[j] - mod_small(Q, P[j])) % P[j], (P[j] - tb.Ej[j]) % P[j], P[j]); },
+         [&](uint32_t j) { return P[j]; });
     fill(hb.data() + TC_N * TC_KB, c->KP, c->K,
          [&](uint32_t j, uint32_t i) { return mod_small(div_small(Pp, P[j]), q[i]); },
          [&](uint32_t i) { return (q[i] - mod_small(Pp, q[i])) % q[i]; }, [&](uint32_t i) { return q[i]; });
@@ -469,7 +476,8 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
     }
     CK(cudaMalloc(&c->d_tcb, hb.size()));
     CK(cudaMemcpy(c->d_tcb, hb.data(), hb.size(), cudaMemcpyHostToDevice));
-    c->tc = TcTabs{c->d_tcb, c->d_tcb + TC_N * TC_KB / 4, c->d_tcb + 2 * TC_N * TC_KB / 4};
+    c->tc = TcTabs{c->d_tcb, c->d_tcb + TC_N * TC_KB / 4, c->d_tcb + 3 * TC_N * TC_KB / 4,
+                   c->d_tcb + 2 * TC_N * TC_KB / 4};
   }
 
   // upload
@@ -1425,10 +1433,11 @@ int hcnn_ctx_create(hcnn_ctx** out, uint32_t n, uint32_t k, const uint64_t* prim
     // shuffle-tail radix-16 kernels up to 2^13 (persistent square tensor and
     // relinearisation over R at 2^13: profiles/r2/micro_rbasis.jsonl),
     // mixed-width passes at 2^14, 2-CTA cluster relinearisation at 2^15
-    // base conversions on the tensor cores wherever the parameters allow
-    // (MNIST set 1 17.58 -> 16.66 ms, set 3 38.3 -> 36.4 ms, CIFAR set 5
-    // -4 %: tools/tc_sweep.sh, tools/tc_ab.sh)
-    c->variant = TC_BCONV | (c->logN == 13   ? (8192 | RELIN_RBASIS)
+    // base conversions on the tensor cores from K = 8 primes (MNIST set 1
+    // 17.58 -> 16.46 ms, set 3 38.3 -> 36.4 ms, CIFAR set 5 -4 %; HSquare at
+    // K = 11-12 -5..-9 %, at K = 6 +2..3 %: tools/tc_sweep.sh, tools/tc_ab.sh,
+    // profiles/r2/micro_sweep_v4.jsonl)
+    c->variant = (k >= 8 ? TC_BCONV : 0) | (c->logN == 13   ? (8192 | RELIN_RBASIS)
                              : c->logN == 14 ? (64 | 1024 | 4096 | RELIN_RBASIS)
                              : c->logN == 15 ? (512 | 2048 | RELIN_RBASIS)
                                              : 0);

@@ -39,6 +39,7 @@ constexpr int TC_LBO = 128, TC_SBO = 512;
 struct TcTabs {
   const uint32_t* bqp;  // Q -> P: rows 4j+e (j < KP), K bytes 4i+b (i < K), 4K = v
   const uint32_t* bpq;  // P -> Q: rows 4i+e (i < K), K bytes 4j+b (j < KP), 4KP = v
+  const uint32_t* bsc;  // scale, Q -> P with -E_j folded in: byte e of 2^8b (-E_j c_ij) 2^32 mod p_j
   const uint32_t* bdg;  // canonical lift for the digits: row s (byte s of the
                         // lift), K byte 4i+b: byte s-b of q/q_i; 4K: byte s of
                         // 2^(32 W) - q
@@ -239,7 +240,7 @@ __global__ void __launch_bounds__(TC_M, 7)
   extern __shared__ __align__(1024) uint8_t smraw[];
   TcSmem& sm = *reinterpret_cast<TcSmem*>(smraw);
   const int tid = threadIdx.x, warp = tid >> 5;
-  tc_load_b(sm.bqp, tc.bqp);
+  tc_load_b(sm.bqp, tc.bsc);  // the scale's Q -> P matrix (-E_j folded in)
   tc_load_b(sm.bpq, tc.bpq);
   if (dig != nullptr) tc_load_b(sm.bdg, tc.bdg);
   if (tid == 0) {
@@ -290,8 +291,8 @@ __global__ void __launch_bounds__(TC_M, 7)
     uint64_t F = 0;
     tc_drain<KP>(tlane, [&](int j, const uint32_t* acc) {
       const uint32_t pj = tb.p[j];
-      const uint32_t rj = tc_redc(acc, pj, tb.ppinv[j]);
-      uint32_t a = add_mod(mul_shoup(dp[j], tb.C[j], tb.Cs[j], pj), mul_shoup(pj - rj, tb.Ej[j], tb.Ejs[j], pj), pj);
+      const uint32_t er = tc_redc(acc, pj, tb.ppinv[j]);  // (p_j - r_j) E_j mod p_j
+      uint32_t a = add_mod(mul_shoup(dp[j], tb.C[j], tb.Cs[j], pj), er, pj);
       a = add_mod(a, tb.F[j], pj);
       yt[j] = a;
       F += frac59(a, tb.pg[j], tb.pk[j]);
