@@ -344,3 +344,98 @@ def test_rbasis_crt_identity_in_python_ints():
             assert back == Z[k]
             assert back % q == sum(digits[i][kk] * keys[i][(k - kk) % n] * (1 if kk <= k else -1)
                                    for i in range(D) for kk in range(n)) % q
+
+
+def _tc_bytes(x):
+    """little-endian bytes of u32 words (the A rows of tc_bconv.cuh)"""
+    return [(int(x) >> (8 * b)) & 0xFF for b in range(4)]
+
+
+def test_tensor_core_base_conversion_identity_in_python_ints():
+    """The byte-split identity behind k_extend_tc / k_scale_tc
+    (csrc/tc_bconv.cuh), restated with the kernel's integer
+    widths: A[4i+b] = byte b of x~_i, B[4o+e][4i+b] = byte e of
+    (2^8b c_io 2^32 mod m_o); four s32 column sums per output (each
+    < 2^22), S = sum_e acc_e 2^8e < 2^46.1, one REDC -> the exact residue
+    (sum_i x~_i c_io + v c_vo) mod m_o, for worst-case (all-ones) and random
+    operands at K = 15 (the largest the 64-byte row takes)."""
+    import random
+
+    rnd = random.Random(5)
+    primes = [1073479681, 1072496641, 1071513601, 1070727169, 1069219841, 1068564481, 1068433409,
+              1068236801, 1065811969, 1065484289, 1064697857, 1063452673, 1063321601, 1063059457,
+              1062862849]
+    K = 15
+    for trial in range(40):
+        m = primes[trial % len(primes)]
+        minv = (-pow(m, -1, 1 << 32)) % (1 << 32)
+        c = [rnd.randrange(m) for _ in range(K)]
+        cv = rnd.randrange(m)
+        if trial < 4:
+            xt = [(1 << 30) - 1] * K  # every byte 0xFF / 0x3F: the largest column sums
+            v = 255
+        else:
+            xt = [rnd.randrange(primes[i]) for i in range(K)]
+            v = rnd.randrange(K + 1)
+        bcols = [[0] * 64 for _ in range(4)]
+        for i in range(K + 1):
+            ci = c[i] if i < K else cv
+            for b in range(4 if i < K else 1):
+                cp = ((ci << (8 * b)) << 32) % m
+                for e in range(4):
+                    bcols[e][4 * i + b] = (cp >> (8 * e)) & 0xFF
+        arow = sum((_tc_bytes(x) for x in xt), []) + [v, 0, 0, 0]
+        arow += [0] * (64 - len(arow))
+        acc = [sum(a * bb for a, bb in zip(arow, bcols[e])) for e in range(4)]
+        assert all(0 <= s < (1 << 22) for s in acc)
+        S = acc[0] + (acc[1] << 8) + (acc[2] << 16) + (acc[3] << 24)
+        assert S < (1 << 47)
+        u = (S * minv) % (1 << 32)
+        r = (S + u * m) >> 32
+        r = r if r < m else r - m
+        assert r == (sum(x * ci for x, ci in zip(xt, c)) + v * cv) % m
+
+
+def test_tensor_core_digit_lift_identity_in_python_ints():
+    """The digits' canonical lift on the tensor cores: column s sums
+    byte(s-b) of q/q_i times byte b of x~_i, plus byte s of 2^(32W) - q times
+    V; one carry pass gives sum_i x~_i (q/q_i) - V q exactly (mod 2^(32W),
+    where the value lies in [0, 2q)), as mw_lift / mw_sub_mq do."""
+    import random
+
+    rnd = random.Random(9)
+    qs = [1073643521, 1073479681, 1073184769, 1073053697, 1072857089, 1072496641, 1071513601,
+          1070727169, 1069219841, 1068564481, 1068433409]
+    K = len(qs)
+    q = 1
+    for p in qs:
+        q *= p
+    W = (30 * K + 5 + 31) // 32 + 1
+    neg = (1 << (32 * W)) - q
+    for _ in range(30):
+        x = rnd.randrange(q)
+        xt = [x * pow(q // p, -1, p) % p for p in qs]
+        lift = sum(t * (q // p) for t, p in zip(xt, qs))
+        V = lift // q - rnd.randrange(2)  # the fixed-point estimate: v or v - 1
+        V = max(V, 0)
+        cols = [0] * (4 * W)
+        for i, t in enumerate(xt):
+            qb = (q // qs[i]).to_bytes(4 * W, "little")
+            tb = _tc_bytes(t)
+            for b in range(4):
+                for s in range(b, 4 * W):
+                    cols[s] += tb[b] * qb[s - b]
+        nb = neg.to_bytes(4 * W, "little")
+        for s in range(4 * W):
+            cols[s] += V * nb[s]
+        assert max(cols) < (1 << 22)
+        words, carry = [], 0
+        for w in range(W):
+            t = carry + cols[4 * w] + (cols[4 * w + 1] << 8) + (cols[4 * w + 2] << 16) + (cols[4 * w + 3] << 24)
+            words.append(t & 0xFFFFFFFF)
+            carry = t >> 32
+        S = sum(wd << (32 * i) for i, wd in enumerate(words))
+        assert S == lift - V * q and 0 <= S < 2 * q
+        if S >= q:
+            S -= q
+        assert S == x
