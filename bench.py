@@ -264,6 +264,10 @@ def kernel_work(name: str, K: int, KP: int, D: int, N: int, cts: float):
         slots = 3 * D * bfly * 4
         byts = 4 * N * (D + 3 * D)
         fixed = 0
+    elif name == "k_rb_mac_tc":  # the products on the tensor cores; a REDC per output on the integer pipe
+        slots = 3 * 2 * K * N * 4
+        byts = 4 * N * (3 * D + 6 * K)
+        fixed = 3 * N * 96 * 96
     elif name == "k_rb_mac":  # 3 x 2K x D lazy 64-bit MACs per coefficient, a fold per output
         slots = 3 * 2 * K * N * (D * 2 + 7)
         byts = 4 * N * (3 * D + 6 * K)
@@ -575,7 +579,7 @@ def run_ours(args):
             kernels[name]["s8d_frac"] = round(3 * mm / avg_s / 1e12 / imad_peak, 4)
     # the relinearisation over R as one stage (its three kernels) against the
     # 8(d) relinearisation work of the reference algorithm
-    rb = [n for n in ("k_rb_fwd", "k_rb_mac", "k_rb_inv") if n in prof]
+    rb = [n for n in ("k_rb_fwd", "k_rb_mac", "k_rb_mac_tc", "k_rb_inv") if n in prof]
     if len(rb) == 3:
         cnt = prof["k_rb_fwd"][0]
         tot = sum(prof[n][1] for n in rb)

@@ -103,7 +103,7 @@ def main():
                 line["ntt_gbfly_s"] = round(a.rows * bfly / (per * 1e-3) / 1e9, 1)
                 line["ntt_hbm_gbs"] = round(a.rows * n * 8 / (per * 1e-3) / 1e9, 1)
                 hsq = 0.0
-                for name in ("k_extend", "k_extend_tc", "k_tensor", "k_scale", "k_scale_tc", "k_relin", "k_rb_fwd", "k_rb_mac", "k_rb_inv"):
+                for name in ("k_extend", "k_extend_tc", "k_tensor", "k_scale", "k_scale_tc", "k_relin", "k_rb_fwd", "k_rb_mac", "k_rb_mac_tc", "k_rb_inv"):
                     if name not in prof:  # the per-prime or the R-basis relinearisation
                         continue
                     c_, t_ = prof[name]

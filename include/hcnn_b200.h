@@ -79,7 +79,9 @@ enum {
  * CRT back; N = 2^12 to 2^15 (2-CTA clusters at 2^15), at most 23 digits,
  * at least 8 primes), 32768 the multiply's exact base conversions (k_extend,
  * k_scale) as u8 x u8 -> s32 tcgen05 MMAs (at most 15 primes in Q and P,
- * N >= 128).  Default: 32768 from K = 8 primes, plus per N 8192|16384 at 2^13,
+ * N >= 128), 65536 the relinearisation multiply-accumulate over R on the
+ * tensor cores (k_rb_mac_tc; exact, opt-in: slower than the integer kernel at
+ * every measured size).  Default: 32768 from K = 8 primes, plus per N 8192|16384 at 2^13,
  * 64|1024|4096|16384 at 2^14, 512|2048|16384 at 2^15.
  * Results are identical for every setting. */
 /* HCNN_OPT_TS_CHUNK: ciphertexts per extend/tensor/scale sub-chunk of a

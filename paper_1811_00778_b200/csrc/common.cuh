@@ -84,6 +84,7 @@ struct RbTabs {
   uint32_t r[RB_A];
   uint2 t32[RB_A];     // 2^32 mod r_a (Shoup): folds the high word of a 64-bit sum
   uint32_t one[RB_A];  // floor(2^32 / r_a): the Shoup word of 1 (low word)
+  uint32_t rpinv[RB_A];  // -r_a^-1 mod 2^32 (REDC of the tensor-core MAC)
   uint2 isc_n[RB_A], isc_nw[RB_A];  // inverse scaling N^-1 g_a, psi^-N/2 N^-1 g_a with
                                     // g_a = (R/r_a)^-1 mod r_a: the inverse leaves x~_a
   float rinv[RB_A];    // 1 / r_a: v = rint(sum_a x~_a / r_a) (|Z| / R < 2^-25)

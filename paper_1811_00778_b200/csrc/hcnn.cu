@@ -136,6 +136,8 @@ struct hcnn_ctx {
   RbTabs rb{};
   uint32_t* d_rlk_rb = nullptr;  // [RB_A][D][2K][N] NTT domain mod r_a, tiled
   bool rb_keys = false;
+  uint8_t* d_rlk_tc = nullptr;  // [RB_A][N][RBT_BT] byte-split key matrices (RB_MAC_TC)
+  bool rb_tc_keys = false;
   // base conversions on the tensor cores (TC_BCONV, tc_bconv.cuh): usable
   // when K, KP <= 15 and 128 | N
   bool tc_ok = false;
@@ -329,6 +331,7 @@ void build_tables(hcnn_ctx* c, const std::vector<u64>& q, uint64_t t) {
       rb.r[a] = (uint32_t)r;
       rb.t32[a] = shp(((u64)1 << 32) % r, r);
       rb.one[a] = shoup_of(1, (uint32_t)r);
+      rb.rpinv[a] = neg_inv32((uint32_t)r);
       const u64 g = invmod64((u64)((Rp / r) % r), r);  // (R/r_a)^-1 mod r_a
       const uint32_t jj = (uint32_t)rb.roff + a;
       rb.isc_n[a] = shp(mulmod64(hninv[jj].x, g, r), r);
@@ -597,10 +600,41 @@ void prepare_rb_keys(hcnn_ctx* c) {
     launch_ntt_rows(c, c->d_rlk_rb + a * rows * N, rows, 1, c->rb.roff + a, 2);
   CK(cudaFreeAsync(coef, c->stream));
   c->rb_keys = true;
+  c->rb_tc_keys = false;
+}
+
+// variant bit: the relinearisation multiply-accumulate on the tensor cores
+constexpr int RB_MAC_TC = 65536;
+
+bool rb_mac_tc(const hcnn_ctx* c) {
+  return (c->variant & RB_MAC_TC) && c->D <= 23 && 2 * c->K <= RBT_N / 4 && c->N % (4 * RBT_NB) == 0;
+}
+
+void prepare_rb_tc_keys(hcnn_ctx* c) {
+  if (c->rb_tc_keys) return;
+  const size_t N = c->N, K = c->K, D = c->D;
+  const size_t bytes = (size_t)RB_A * N * RBT_BT;
+  if (!c->d_rlk_tc) CK(cudaMalloc((void**)&c->d_rlk_tc, bytes));
+  CK(cudaMemsetAsync(c->d_rlk_tc, 0, bytes, c->stream));
+  const size_t total = (size_t)RB_A * D * 2 * K * N;
+  k_rb_key_tc<<<cdiv(total, 256), 256, 0, c->stream>>>(c->d_rlk_rb, c->d_rlk_tc, (int)D, (int)(2 * K), (int)N,
+                                                      c->rb);
+  c->launched("k_rb_key_tc");
+  c->rb_tc_keys = true;
 }
 
 template <int DD>
 void rb_mac_launch(hcnn_ctx* c, const uint32_t* ds, uint32_t* zs, size_t nct) {
+  if (rb_mac_tc(c)) {
+    static std::atomic<uint64_t> cfg_tc{0};
+    per_device_once(cfg_tc, [] {
+      cudaFuncSetAttribute(k_rb_mac_tc<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RbtSmem));
+    });
+    prepare_rb_tc_keys(c);
+    k_rb_mac_tc<DD><<<dim3(c->N / RBT_NB, RB_A), TC_M, sizeof(RbtSmem), c->stream>>>(
+        ds, c->d_rlk_tc, zs, (int)nct, (int)c->K, (int)c->N, c->rb);
+    return;
+  }
   static std::atomic<uint64_t> cfg{0};
   per_device_once(cfg, [] {
     cudaFuncSetAttribute(k_rb_mac<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
@@ -623,7 +657,7 @@ void launch_rb_mac(hcnn_ctx* c, const uint32_t* ds, uint32_t* zs, size_t nct) {
     default:
       fail(HCNN_ERR_UNSUPPORTED, "relinearisation over R: digit count");
   }
-  c->launched("k_rb_mac");
+  c->launched(rb_mac_tc(c) ? "k_rb_mac_tc" : "k_rb_mac");
 }
 
 // relinearisation over R: digit spectra mod r_a, multiply-accumulate with
@@ -1111,11 +1145,11 @@ void layout_key(hcnn_ctx* c, const uint32_t* raw, int domain, size_t rows, uint3
 
 void prepare_keys(hcnn_ctx* c) {
   if (rb_active(c)) prepare_rb_keys(c);
-  if (c->keys_variant == (c->variant & ~(32 | 1024 | 2048 | 4096 | 8192 | RELIN_RBASIS | TC_BCONV))) return;
+  if (c->keys_variant == (c->variant & ~(32 | 1024 | 2048 | 4096 | 8192 | RELIN_RBASIS | TC_BCONV | RB_MAC_TC))) return;
   if (c->d_rlk_raw)
     layout_key(c, c->d_rlk_raw, c->rlk_domain, (size_t)c->D * 2 * c->K, &c->d_rlk, variant_mont(c, c->variant));
   if (c->d_pk_raw) layout_key(c, c->d_pk_raw, c->pk_domain, 2 * (size_t)c->K, &c->d_pk, 0);
-  c->keys_variant = c->variant & ~(32 | 1024 | 2048 | 4096 | 8192 | RELIN_RBASIS | TC_BCONV);
+  c->keys_variant = c->variant & ~(32 | 1024 | 2048 | 4096 | 8192 | RELIN_RBASIS | TC_BCONV | RB_MAC_TC);
 }
 
 }  // namespace
@@ -1460,6 +1494,7 @@ int hcnn_ctx_destroy(hcnn_ctx* c) {
     if (c->d_rlk) cudaFree(c->d_rlk);
     if (c->d_rlk_raw) cudaFree(c->d_rlk_raw);
     if (c->d_rlk_rb) cudaFree(c->d_rlk_rb);
+    if (c->d_rlk_tc) cudaFree(c->d_rlk_tc);
     if (c->d_tcb) cudaFree(c->d_tcb);
     if (c->d_pk_raw) cudaFree(c->d_pk_raw);
     cudaFree(c->d_pinv);
@@ -1531,8 +1566,8 @@ int hcnn_ctx_set_option(hcnn_ctx* c, int key, int64_t value) {
       // geometry flags of the fused kernels (ntt_kernels.cuh): +16 one-row
       // relinearisation transforms, +32 square tensors on the radix-32 mixed
       // geometry, +64 mixed-width passes instead of a warp-shuffle tail
-      if (value & ~(int64_t)(16 | 32 | 64 | 512 | 1024 | 2048 | 4096 | 8192 | RELIN_RBASIS | TC_BCONV))
-        fail(HCNN_ERR_PARAM, "NTT variant flags are 16, 32, 64, 512, 1024, 2048, 4096, 8192, 16384 and 32768");
+      if (value & ~(int64_t)(16 | 32 | 64 | 512 | 1024 | 2048 | 4096 | 8192 | RELIN_RBASIS | TC_BCONV | RB_MAC_TC))
+        fail(HCNN_ERR_PARAM, "NTT variant flags are 16, 32, 64, 512, 1024, 2048, 4096, 8192, 16384, 32768 and 65536");
       if ((value & (32 | 64)) && c->logN < 10) fail(HCNN_ERR_UNSUPPORTED, "mixed geometries need N >= 1024");
       if ((value & 512) && c->logN != 15 && c->logN != 14)
         fail(HCNN_ERR_UNSUPPORTED, "cluster kernels are for N = 2^14 and 2^15");

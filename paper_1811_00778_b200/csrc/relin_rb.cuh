@@ -11,6 +11,7 @@
 // q_j is the same residue the reference computes, bit for bit.
 #pragma once
 #include "common.cuh"
+#include "tc_bconv.cuh"
 
 namespace hcnn {
 
@@ -124,6 +125,184 @@ __global__ void k_rb_key_rows(const uint32_t* __restrict__ coef, uint32_t* __res
     const uint32_t val = (neg && m) ? r - m : m;
     out[(((size_t)a * D + i) * 2 * K + 2 * j + part) * N + n] = val;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Step 2 on the tensor cores (flag RB_MAC_TC).  For one r_a and one
+// coefficient n, Z[ct][jp] = sum_i D[ct][i] K[i][jp] is a (ciphertexts x D) x
+// (D x 2K) product with a key matrix that changes with n; byte-split like
+// tc_bconv.cuh: A[ct][4i+b] = byte b of D[ct][i], B_n[4jp+e][4i+b] = byte e
+// of (2^8b K[i][jp] 2^32 mod r_a) (built once per key by k_rb_key_tc), four
+// s32 columns per output (< 92 * 255^2 < 2^23), one REDC.  A CTA takes four
+// consecutive positions n (16-byte loads and stores of the tiled rows) and
+// walks the ciphertexts in tiles of 128; two positions per MMA batch (TMEM
+// 256 columns, two CTAs per SM).  Exact, but off by default: at set 1 it
+// moves the algorithmic bytes (ncu: 1.72 GB read, 1.52 GB written per launch)
+// at 0.8 TB/s, latency-bound with 8 warps per SM (3.6 vs 1.39 ms per launch
+// for k_rb_mac); a deeper pipeline (asynchronous copies into a staging tile,
+// more warps for the REDC epilogue) is what it needs.
+constexpr int RBT_KB = 96;                   // K bytes: 4 D <= 92
+constexpr int RBT_SBO = RBT_KB / 16 * 128;   // 768: next 8 rows
+constexpr int RBT_N = 96;                    // columns: 4 x 2K <= 88
+constexpr int RBT_TILE = TC_M * RBT_KB;      // 12 KB (A, 128 ciphertexts)
+constexpr int RBT_BT = RBT_N * RBT_KB;       // 9 KB (B, one position)
+constexpr int RBT_NB = 4;                    // positions per CTA
+
+__host__ __device__ constexpr int rbt_off(int row, int k) {
+  return (row >> 3) * RBT_SBO + (k >> 4) * 128 + (row & 7) * 16 + (k & 15);
+}
+
+DI uint64_t rbt_desc(const void* smem) {
+  const uint32_t a = smem_u32(smem);
+  return (uint64_t)((a >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(RBT_SBO >> 4) << 32) |
+         (1ull << 46);
+}
+
+// D[tmem] = A x B^T over 96 K-bytes (three k32 steps)
+DI void rbt_mma(uint32_t tmem, const uint8_t* a, const uint8_t* b) {
+  const uint64_t da = rbt_desc(a), db = rbt_desc(b);
+  constexpr uint32_t id = (2u << 4) | ((uint32_t)(RBT_N >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+#pragma unroll
+  for (int k = 0; k < RBT_KB / 32; ++k) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
+        "l"(da + 16 * k), "l"(db + 16 * k), "r"(id), "r"(k)
+        : "memory");
+  }
+}
+
+// kx: [RB_A][D][2K][N] key spectra mod r_a -> kt: [RB_A][N][RBT_BT] bytes
+// (zero-filled beforehand)
+__global__ void k_rb_key_tc(const uint32_t* __restrict__ kx, uint8_t* __restrict__ kt, int D, int K2, int N,
+                            RbTabs rb) {
+  const size_t total = (size_t)RB_A * D * K2 * N;
+  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int n = (int)(idx % N);
+  const size_t row = idx / N;  // (a, i, jp)
+  const int jp = (int)(row % K2);
+  const int i = (int)((row / K2) % D);
+  const int a = (int)(row / ((size_t)K2 * D));
+  const uint64_t r = rb.r[a];
+  const uint64_t k = kx[idx] % r;
+  uint8_t* dst = kt + ((size_t)a * N + n) * RBT_BT;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const uint64_t g = ((uint64_t)1 << (8 * b + 32)) % r;  // 2^(8b+32) mod r
+    const uint32_t c = (uint32_t)(k * g % r);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) dst[rbt_off(4 * jp + e, 4 * i + b)] = (uint8_t)(c >> (8 * e));
+  }
+}
+
+struct RbtSmem {
+  uint8_t a[RBT_NB][RBT_TILE];
+  uint8_t b[RBT_NB][RBT_BT];
+  uint64_t bar;
+  uint32_t tmem;
+};
+
+// dspec: [B][RB_A][D][N]; kt: [RB_A][N][RBT_BT]; zspec: [B][K][RB_A][2][N]
+template <int DD>
+__global__ void __launch_bounds__(TC_M, 2)
+    k_rb_mac_tc(const uint32_t* __restrict__ dspec, const uint8_t* __restrict__ kt, uint32_t* __restrict__ zspec,
+                int nct, int K, int N, RbTabs rb) {
+  static_assert(4 * DD <= RBT_KB, "digits exceed the 96-byte row");
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  RbtSmem& sm = *reinterpret_cast<RbtSmem*>(smraw);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int a = blockIdx.y;
+  const int n0 = blockIdx.x * RBT_NB;
+  const int K2 = 2 * K;
+  const uint32_t r = rb.r[a], rinv = rb.rpinv[a];
+  {  // the key matrices of the four positions (contiguous)
+    const uint4* src = reinterpret_cast<const uint4*>(kt + ((size_t)a * N + n0) * RBT_BT);
+    uint4* dst = reinterpret_cast<uint4*>(&sm.b[0][0]);
+    for (int i = tid; i < RBT_NB * RBT_BT / 16; i += TC_M) dst[i] = __ldg(src + i);
+  }
+  if (tid == 0) {
+    mbar_init(&sm.bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&sm.tmem))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = sm.tmem;
+  const uint32_t tlane = tbase + ((uint32_t)(warp * 32) << 16);
+  uint32_t phase = 0;
+  for (int c0 = 0; c0 < nct; c0 += TC_M) {
+    const int ct = c0 + tid;
+    const bool live = ct < nct;
+    {  // this thread's row of the four A tiles: 16-byte loads of its digit rows
+      uint4 d[DD];
+      const uint4* dp = reinterpret_cast<const uint4*>(dspec + ((size_t)ct * RB_A + a) * DD * N + n0);
+#pragma unroll
+      for (int i = 0; i < DD; ++i) d[i] = live ? __ldg(dp + (size_t)i * (N / 4)) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int c = 0; c < RBT_KB / 16; ++c) {
+        uint32_t w[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = 4 * c + u;
+          const uint4 v = i < DD ? d[i] : make_uint4(0, 0, 0, 0);
+          w[0][u] = v.x;
+          w[1][u] = v.y;
+          w[2][u] = v.z;
+          w[3][u] = v.w;
+        }
+#pragma unroll
+        for (int k = 0; k < RBT_NB; ++k)
+          *reinterpret_cast<uint4*>(&sm.a[k][rbt_off(tid, 16 * c)]) = make_uint4(w[k][0], w[k][1], w[k][2], w[k][3]);
+      }
+    }
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      fence_proxy_async();
+      tc_fence_before();
+      __syncthreads();
+      if (tid == 0) {
+        tc_fence_after();
+        rbt_mma(tbase, sm.a[2 * half], sm.b[2 * half]);
+        rbt_mma(tbase + 128, sm.a[2 * half + 1], sm.b[2 * half + 1]);
+        tc_commit(&sm.bar);
+      }
+      mbar_wait(&sm.bar, phase);
+      phase ^= 1;
+      tc_fence_after();
+      uint32_t out[2][RBT_N / 4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int g = 0; g < RBT_N / 16; ++g) {
+          uint32_t v[16];
+          tc_ld16(tlane + 128 * h + 16 * g, v);
+          tc_wait_ld();
+#pragma unroll
+          for (int u = 0; u < 4; ++u) out[h][4 * g + u] = tc_redc(&v[4 * u], r, rinv);
+        }
+      }
+      tc_fence_before();
+      if (live) {  // positions n0 + 2 half, + 1 of every (j, part) row
+        uint32_t* zp = zspec + (size_t)ct * K * RB_A * 2 * N + (size_t)a * 2 * N + n0 + 2 * half;
+#pragma unroll
+        for (int jp = 0; jp < RBT_N / 4; ++jp) {
+          if (jp < K2)
+            *reinterpret_cast<uint2*>(zp + ((size_t)(jp >> 1) * RB_A * 2 + (jp & 1)) * N) =
+                make_uint2(out[0][jp], out[1][jp]);
+        }
+      }
+    }
+    __syncthreads();  // A tiles and the accumulators are free for the next tile
+  }
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tbase) : "memory");
 }
 
 }  // namespace hcnn

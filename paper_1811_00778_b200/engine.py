@@ -156,7 +156,8 @@ class GpuContext:
         2-CTA cluster rows at 2^15, 1024 relinearisation sums in TMEM, 2048 /
         4096 square tensor with rows parked in TMEM, 8192 persistent square
         tensor with TMA prefetch, 16384 relinearisation over the shared
-        three-prime basis R, 32768 base conversions on the tensor cores)."""
+        three-prime basis R, 32768 base conversions on the tensor cores,
+        65536 the relinearisation multiply-accumulate on the tensor cores)."""
         _lib.check(_lib.lib().hcnn_ctx_set_option(self.handle, 1, int(variant)), "ntt variant")
 
     def variant(self) -> int:

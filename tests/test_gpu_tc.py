@@ -131,3 +131,64 @@ def test_tc_unavailable_for_16_primes():
     g.profile(False)
     assert "k_scale" in names and "k_scale_tc" not in names
     E._CTXS.clear()
+
+
+RB = 16384
+RB_MAC_TC = 65536
+
+
+def _three_part(primes, n, rng, count):
+    k = len(primes)
+    p = np.array(primes, dtype=np.int64)[:, None]
+    x = rng.integers(0, 1 << 62, (count, 3, k, n)) % p
+    x[0, 2] = p - 1  # every digit w - 1: the largest key-switching sums
+    x[1, 2] = (p - 1) // 2
+    return x
+
+
+@pytest.mark.parametrize("n,k,count", [(8192, 11, 20), (8192, 12, 131), (16384, 11, 13), (4096, 8, 140)])
+def test_tc_relinearisation_mac_equals_integer_mac(n, k, count):
+    """The relinearisation multiply-accumulate over R on the tensor cores
+    (flag 65536, k_rb_mac_tc) equals the integer k_rb_mac bit for bit, for
+    batches that are not multiples of the 128-ciphertext tile."""
+    E._CTXS.clear()
+    primes = _primes(n, k)
+    params = B.BfvParams(B.RnsContext(n, primes), 5522259017729 if n <= 8192 else 65537)
+    _, _, rlk = B.keygen(params, np.random.default_rng(k + n))
+    x3 = dev(_three_part(primes, n, np.random.default_rng(n + k + count), count))
+    g = E.context_for(params)
+    _lib.check(_lib.lib().hcnn_ctx_set_option(g.handle, 3, 1), "rb min batch")
+    base = (g.variant() | RB) & ~RB_MAC_TC
+    g.set_variant(base)
+    assert _lib.lib().hcnn_ctx_query(g.handle, 8) == 1
+    want = host(ops.relinearize_device(g, x3, rlk))
+    g.set_variant(base | RB_MAC_TC)
+    g.profile(True)
+    got = host(ops.relinearize_device(g, x3, rlk))
+    names = set(g.profile_read())
+    g.profile(False)
+    assert "k_rb_mac_tc" in names and "k_rb_mac" not in names, names
+    assert np.array_equal(got, want)
+    E._CTXS.clear()
+
+
+def test_tc_mac_hsquare_vs_oracle():
+    """HSquare with every tensor-core path on equals the oracle."""
+    E._CTXS.clear()
+    n, k, t = 8192, 11, 65537
+    primes = _primes(n, k)
+    params = B.BfvParams(B.RnsContext(n, primes), t)
+    _, pk, rlk = B.keygen(params, np.random.default_rng(3))
+    rng = np.random.default_rng(4)
+    cts = [B.encrypt(pk, B.Plaintext(rng.integers(0, t, n), t), params, rng) for _ in range(12)]
+    g = E.context_for(params)
+    g.set_variant(g.variant() | RB | TC | RB_MAC_TC)
+    x = dev(np.stack([ct_array(c) for c in cts]))
+    got = host(ops.square_device(g, x, rlk))
+    op = O.Params(O.Context(n, primes), t)
+    orlk = [(k0.residues, k1.residues) for k0, k1 in rlk.components]
+    for i in (0, 11):
+        c = cts[i]
+        ref3 = O.hmult_raw(op, (c.parts[0].residues, c.parts[1].residues))
+        assert np.array_equal(got[i], np.stack(O.relinearize(op, ref3, orlk)))
+    E._CTXS.clear()
