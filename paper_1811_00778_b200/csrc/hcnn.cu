@@ -631,7 +631,7 @@ void rb_mac_launch(hcnn_ctx* c, const uint32_t* ds, uint32_t* zs, size_t nct) {
       cudaFuncSetAttribute(k_rb_mac_tc<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RbtSmem));
     });
     prepare_rb_tc_keys(c);
-    k_rb_mac_tc<DD><<<dim3(c->N / RBT_NB, RB_A), TC_M, sizeof(RbtSmem), c->stream>>>(
+    k_rb_mac_tc<DD><<<dim3(c->N / RBT_NB, RB_A), RBT_T, sizeof(RbtSmem), c->stream>>>(
         ds, c->d_rlk_tc, zs, (int)nct, (int)c->K, (int)c->N, c->rb);
     return;
   }

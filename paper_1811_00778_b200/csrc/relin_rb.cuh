@@ -135,12 +135,9 @@ __global__ void k_rb_key_rows(const uint32_t* __restrict__ coef, uint32_t* __res
 // of (2^8b K[i][jp] 2^32 mod r_a) (built once per key by k_rb_key_tc), four
 // s32 columns per output (< 92 * 255^2 < 2^23), one REDC.  A CTA takes four
 // consecutive positions n (16-byte loads and stores of the tiled rows) and
-// walks the ciphertexts in tiles of 128; two positions per MMA batch (TMEM
-// 256 columns, two CTAs per SM).  Exact, but off by default: at set 1 it
-// moves the algorithmic bytes (ncu: 1.72 GB read, 1.52 GB written per launch)
-// at 0.8 TB/s, latency-bound with 8 warps per SM (3.6 vs 1.39 ms per launch
-// for k_rb_mac); a deeper pipeline (asynchronous copies into a staging tile,
-// more warps for the REDC epilogue) is what it needs.
+// walks the ciphertexts in tiles of 128 (see k_rb_mac_tc below).  Exact and
+// opt-in: 3.97 ms per MNIST step against 2.79 ms for k_rb_mac (DESIGN.md
+// section 9, item 0).
 constexpr int RBT_KB = 96;                   // K bytes: 4 D <= 92
 constexpr int RBT_SBO = RBT_KB / 16 * 128;   // 768: next 8 rows
 constexpr int RBT_N = 96;                    // columns: 4 x 2K <= 88
@@ -196,113 +193,137 @@ __global__ void k_rb_key_tc(const uint32_t* __restrict__ kx, uint8_t* __restrict
   }
 }
 
+constexpr int RBT_T = 256;                   // threads: two warps per TMEM lane quadrant
+constexpr int RBT_SROW = 25 * 16;            // staging bytes per ciphertext: 24 digit rows x 4 positions,
+                                             // padded so 8 consecutive rows hit distinct banks
+
 struct RbtSmem {
-  uint8_t a[RBT_NB][RBT_TILE];
-  uint8_t b[RBT_NB][RBT_BT];
+  uint8_t a[RBT_NB][RBT_TILE];               // A tiles; after the MMAs the output staging
+  uint8_t b[RBT_NB][RBT_BT];                 // key matrices of the four positions
+  uint8_t stg[2][TC_M * RBT_SROW];           // digit rows as loaded, double-buffered
   uint64_t bar;
   uint32_t tmem;
 };
 
+DI void cp_async16(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes)
+               : "memory");
+}
+DI void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+DI void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
 // dspec: [B][RB_A][D][N]; kt: [RB_A][N][RBT_BT]; zspec: [B][K][RB_A][2][N]
+// One CTA per (four positions, r_a), walking the ciphertexts in tiles of
+// 128: the next tile's digit rows stream into a staging buffer by
+// asynchronous copies while the current one is transposed into the A tiles,
+// multiplied (four MMAs, 512 TMEM columns) and reduced.
 template <int DD>
-__global__ void __launch_bounds__(TC_M, 2)
+__global__ void __launch_bounds__(RBT_T, 1)
     k_rb_mac_tc(const uint32_t* __restrict__ dspec, const uint8_t* __restrict__ kt, uint32_t* __restrict__ zspec,
                 int nct, int K, int N, RbTabs rb) {
   static_assert(4 * DD <= RBT_KB, "digits exceed the 96-byte row");
   extern __shared__ __align__(1024) uint8_t smraw[];
   RbtSmem& sm = *reinterpret_cast<RbtSmem*>(smraw);
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int a = blockIdx.y;
   const int n0 = blockIdx.x * RBT_NB;
   const int K2 = 2 * K;
   const uint32_t r = rb.r[a], rinv = rb.rpinv[a];
-  {  // the key matrices of the four positions (contiguous)
-    const uint4* src = reinterpret_cast<const uint4*>(kt + ((size_t)a * N + n0) * RBT_BT);
-    uint4* dst = reinterpret_cast<uint4*>(&sm.b[0][0]);
-    for (int i = tid; i < RBT_NB * RBT_BT / 16; i += TC_M) dst[i] = __ldg(src + i);
+  auto fetch = [&](int c0, int buf) {  // digit rows of ciphertexts c0 .. c0 + 127
+    for (int task = tid; task < TC_M * DD; task += RBT_T) {
+      const int row = task / DD, i = task % DD;
+      const int ct = c0 + row;
+      const uint32_t* src = ct < nct ? dspec + (((size_t)ct * RB_A + a) * DD + i) * N + n0 : dspec;
+      cp_async16(&sm.stg[buf][row * RBT_SROW + i * 16], src, ct < nct ? 16u : 0u);
+    }
+    cp_async_commit();
+  };
+  {  // the key matrices of the four positions (contiguous), asynchronously
+     // with the first tile's rows (same commit group)
+    const uint8_t* src = kt + ((size_t)a * N + n0) * RBT_BT;
+    for (int i = tid; i < RBT_NB * RBT_BT / 16; i += RBT_T) cp_async16(&sm.b[0][16 * i], src + 16 * i, 16u);
   }
   if (tid == 0) {
     mbar_init(&sm.bar, 1);
     fence_mbar_init();
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&sm.tmem))
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&sm.tmem))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  fence_proxy_async();
+  fetch(0, 0);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = sm.tmem;
-  const uint32_t tlane = tbase + ((uint32_t)(warp * 32) << 16);
+  const int quad = warp & 3, pp = warp >> 2;  // TMEM lane quadrant; positions 2 pp, 2 pp + 1
+  const uint32_t tlane = tbase + ((uint32_t)(quad * 32) << 16);
   uint32_t phase = 0;
-  for (int c0 = 0; c0 < nct; c0 += TC_M) {
-    const int ct = c0 + tid;
-    const bool live = ct < nct;
-    {  // this thread's row of the four A tiles: 16-byte loads of its digit rows
-      uint4 d[DD];
-      const uint4* dp = reinterpret_cast<const uint4*>(dspec + ((size_t)ct * RB_A + a) * DD * N + n0);
+  int buf = 0;
+  for (int c0 = 0; c0 < nct; c0 += TC_M, buf ^= 1) {
+    if (c0 + TC_M < nct) fetch(c0 + TC_M, buf ^ 1);
+    else cp_async_commit();  // an empty group keeps the wait count uniform
+    cp_async_wait1();
+    __syncthreads();  // this tile's rows have landed (every thread's copies)
+    // transpose: staging [row][digit][4 positions] -> A tile k [row][4 digits]
+    for (int task = tid; task < TC_M * (RBT_KB / 16); task += RBT_T) {
+      const int row = task % TC_M, c = task / TC_M;  // rows fastest: conflict-free
+      uint4 v[4];
 #pragma unroll
-      for (int i = 0; i < DD; ++i) d[i] = live ? __ldg(dp + (size_t)i * (N / 4)) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-      for (int c = 0; c < RBT_KB / 16; ++c) {
-        uint32_t w[4][4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i = 4 * c + u;
-          const uint4 v = i < DD ? d[i] : make_uint4(0, 0, 0, 0);
-          w[0][u] = v.x;
-          w[1][u] = v.y;
-          w[2][u] = v.z;
-          w[3][u] = v.w;
-        }
-#pragma unroll
-        for (int k = 0; k < RBT_NB; ++k)
-          *reinterpret_cast<uint4*>(&sm.a[k][rbt_off(tid, 16 * c)]) = make_uint4(w[k][0], w[k][1], w[k][2], w[k][3]);
-      }
+      for (int u = 0; u < 4; ++u)
+        v[u] = *reinterpret_cast<const uint4*>(&sm.stg[buf][row * RBT_SROW + (4 * c + u) * 16]);
+      *reinterpret_cast<uint4*>(&sm.a[0][rbt_off(row, 16 * c)]) = make_uint4(v[0].x, v[1].x, v[2].x, v[3].x);
+      *reinterpret_cast<uint4*>(&sm.a[1][rbt_off(row, 16 * c)]) = make_uint4(v[0].y, v[1].y, v[2].y, v[3].y);
+      *reinterpret_cast<uint4*>(&sm.a[2][rbt_off(row, 16 * c)]) = make_uint4(v[0].z, v[1].z, v[2].z, v[3].z);
+      *reinterpret_cast<uint4*>(&sm.a[3][rbt_off(row, 16 * c)]) = make_uint4(v[0].w, v[1].w, v[2].w, v[3].w);
     }
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      fence_proxy_async();
-      tc_fence_before();
-      __syncthreads();
-      if (tid == 0) {
-        tc_fence_after();
-        rbt_mma(tbase, sm.a[2 * half], sm.b[2 * half]);
-        rbt_mma(tbase + 128, sm.a[2 * half + 1], sm.b[2 * half + 1]);
-        tc_commit(&sm.bar);
-      }
-      mbar_wait(&sm.bar, phase);
-      phase ^= 1;
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
       tc_fence_after();
-      uint32_t out[2][RBT_N / 4];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int k = 0; k < RBT_NB; ++k) rbt_mma(tbase + 128 * k, sm.a[k], sm.b[k]);
+      tc_commit(&sm.bar);
+    }
+    mbar_wait(&sm.bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    uint32_t out[2][RBT_N / 4];
 #pragma unroll
-        for (int g = 0; g < RBT_N / 16; ++g) {
-          uint32_t v[16];
-          tc_ld16(tlane + 128 * h + 16 * g, v);
-          tc_wait_ld();
+    for (int h = 0; h < 2; ++h) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) out[h][4 * g + u] = tc_redc(&v[4 * u], r, rinv);
-        }
-      }
-      tc_fence_before();
-      if (live) {  // positions n0 + 2 half, + 1 of every (j, part) row
-        uint32_t* zp = zspec + (size_t)ct * K * RB_A * 2 * N + (size_t)a * 2 * N + n0 + 2 * half;
+      for (int g = 0; g < RBT_N / 16; ++g) {
+        uint32_t v[16];
+        tc_ld16(tlane + 128 * (2 * pp + h) + 16 * g, v);
+        tc_wait_ld();
 #pragma unroll
-        for (int jp = 0; jp < RBT_N / 4; ++jp) {
-          if (jp < K2)
-            *reinterpret_cast<uint2*>(zp + ((size_t)(jp >> 1) * RB_A * 2 + (jp & 1)) * N) =
-                make_uint2(out[0][jp], out[1][jp]);
-        }
+        for (int u = 0; u < 4; ++u) out[h][4 * g + u] = tc_redc(&v[4 * u], r, rinv);
       }
     }
-    __syncthreads();  // A tiles and the accumulators are free for the next tile
+    tc_fence_before();
+    // the MMAs have read A: stage the sums there as [jp][row][4 positions]
+    {
+      const int row = quad * 32 + lane;
+      uint8_t* ost = &sm.a[0][0];
+#pragma unroll
+      for (int jp = 0; jp < RBT_N / 4; ++jp)
+        *reinterpret_cast<uint2*>(ost + (jp * TC_M + row) * 16 + pp * 8) = make_uint2(out[0][jp], out[1][jp]);
+    }
+    __syncthreads();
+    for (int task = tid; task < TC_M * K2; task += RBT_T) {
+      const int row = task % TC_M, jp = task / TC_M;
+      const int ct = c0 + row;
+      if (ct < nct)
+        *reinterpret_cast<uint4*>(zspec + (size_t)ct * K * RB_A * 2 * N +
+                                  ((size_t)(jp >> 1) * RB_A * 2 + (size_t)a * 2 + (jp & 1)) * N + n0) =
+            *reinterpret_cast<const uint4*>(&sm.a[0][(jp * TC_M + row) * 16]);
+    }
+    __syncthreads();  // the staging reads are done before the next transpose
   }
   tc_fence_after();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tbase) : "memory");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase) : "memory");
 }
 
 }  // namespace hcnn
