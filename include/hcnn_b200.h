@@ -65,8 +65,8 @@ enum {
   HCNN_Q_NTT_VARIANT = 7,
   HCNN_Q_RELIN_RBASIS = 8, /* 1 when relinearisations of at least HCNN_OPT_RB_MIN_BATCH ciphertexts take
                               the shared-basis R path (flag + parameters) */
-  HCNN_Q_TC_BCONV = 9      /* 1 when the multiply's base conversions run on the tensor cores (flag 32768
-                              + parameters) */
+  HCNN_Q_TC_BCONV = 9      /* 1 when the multiply's base conversions of chunks of at least 12
+                              ciphertexts run on the tensor cores (flag 32768 + parameters) */
 };
 /* Tuning options.  HCNN_OPT_NTT_VARIANT: geometry flags of the fused NTT
  * kernels: 16 one-row relinearisation, 32 radix-32 square tensor, 64

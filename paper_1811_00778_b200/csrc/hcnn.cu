@@ -566,6 +566,7 @@ constexpr int RELIN_RBASIS = 16384;
 constexpr int TC_BCONV = 32768;  // k_extend / k_scale on the tensor cores (tc_bconv.cuh)
 
 bool tc_active(const hcnn_ctx* c) { return (c->variant & TC_BCONV) && c->tc_ok; }
+constexpr size_t TC_MIN_BATCH = 12;  // ciphertexts per multiply chunk for the tensor-core conversions
 
 bool rb_active(const hcnn_ctx* c) {
   if (!(c->variant & RELIN_RBASIS) || !c->rb_ok) return false;
@@ -766,7 +767,9 @@ void mul_chunk(hcnn_ctx* c, const uint32_t* a, const uint32_t* b, size_t nct, ui
   ConvLaunch ca{};
   ca.block = dim3(tpb);
   ca.grid = dim3(cdiv(N, tpb), (unsigned)(nct * 2));
-  const bool tc = tc_active(c);
+  // a handful of ciphertexts: the integer kernels' shorter latency wins
+  // (set 1, one HSquare 0.119 vs 0.123 ms; 8 cts 20.5 vs 20.8 us each)
+  const bool tc = tc_active(c) && nct >= TC_MIN_BATCH;
   ca.tc = &c->tc;
   ca.tiles = nct * 2 * (N / TC_M);
   ca.in = a;

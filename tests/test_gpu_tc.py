@@ -70,8 +70,8 @@ def test_tc_hmult_raw_equals_integer_kernels(n, k, t):
     params = B.BfvParams(B.RnsContext(n, primes), t)
     g = E.context_for(params)
     rng = np.random.default_rng(n + k)
-    a = dev(_two_part(primes, n, rng, 5))
-    b = dev(_two_part(primes, n, rng, 5)[::-1])
+    a = dev(_two_part(primes, n, rng, 13))  # >= 12: the tensor-core path's minimum batch
+    b = dev(_two_part(primes, n, rng, 13)[::-1])
     base = g.variant() & ~TC
     g.set_variant(base)
     assert _lib.lib().hcnn_ctx_query(g.handle, Q_TC) == 0
@@ -100,17 +100,41 @@ def test_tc_hsquare_vs_oracle(n, k):
     params = B.BfvParams(B.RnsContext(n, primes), t)
     _, pk, rlk = B.keygen(params, np.random.default_rng(n))
     rng = np.random.default_rng(n + 1)
-    cts = [B.encrypt(pk, B.Plaintext(rng.integers(0, t, n), t), params, rng) for _ in range(3)]
+    cts = [B.encrypt(pk, B.Plaintext(rng.integers(0, t, n), t), params, rng) for _ in range(12)]
     g = E.context_for(params)
     g.set_variant(g.variant() | TC)
     assert _lib.lib().hcnn_ctx_query(g.handle, Q_TC) == 1
     x = dev(np.stack([ct_array(c) for c in cts]))
+    g.profile(True)
     got = host(ops.square_device(g, x, rlk))
+    names = set(g.profile_read())
+    g.profile(False)
+    assert "k_scale_tc" in names, names
     op = O.Params(O.Context(n, primes), t)
     orlk = [(k0.residues, k1.residues) for k0, k1 in rlk.components]
-    for i, c in enumerate(cts):
+    for i in (0, 5, 11):
+        c = cts[i]
         ref3 = O.hmult_raw(op, (c.parts[0].residues, c.parts[1].residues))
         assert np.array_equal(got[i], np.stack(O.relinearize(op, ref3, orlk)))
+    E._CTXS.clear()
+
+
+def test_tc_small_batches_take_the_integer_kernels():
+    """Below 12 ciphertexts per chunk the integer conversions run (shorter
+    latency); results are identical either way."""
+    E._CTXS.clear()
+    n, k = 8192, 11
+    primes = _primes(n, k)
+    g = E.context_for(B.BfvParams(B.RnsContext(n, primes), 5522259017729))
+    a = dev(_two_part(primes, n, np.random.default_rng(2), 12))
+    outs = {}
+    for count in (4, 12):
+        g.profile(True)
+        outs[count] = host(ops.hmult_raw_device(g, a[:count], a[:count]))
+        names = set(g.profile_read())
+        g.profile(False)
+        assert ("k_scale_tc" in names) == (count >= 12) and ("k_scale" in names) == (count < 12), names
+    assert np.array_equal(outs[4], outs[12][:4])
     E._CTXS.clear()
 
 
@@ -124,7 +148,7 @@ def test_tc_unavailable_for_16_primes():
     g = E.context_for(params)
     g.set_variant(g.variant() | TC)
     assert _lib.lib().hcnn_ctx_query(g.handle, Q_TC) == 0
-    a = dev(_two_part(primes, n, np.random.default_rng(1), 2))
+    a = dev(_two_part(primes, n, np.random.default_rng(1), 12))
     g.profile(True)
     ops.hmult_raw_device(g, a, a)
     names = set(g.profile_read())
