@@ -252,8 +252,10 @@ cudaError_t conv_launch(int op, const ConvLaunch& a, const ConvTabs& tb) {
         // resident CTAs per SM, per device and kernel (the occupancy query
         // costs host time: once per device)
         static int slots[2][2][64];
-        const char* ce = getenv("HCNN_TC_COLS");  // tuning probe
-        const bool wide = ce && atoi(ce) == 128;
+        static const bool wide = [] {  // tuning probe (tools/tc_sweep.sh): 128 TMEM columns, 4 CTAs per SM
+          const char* ce = getenv("HCNN_TC_COLS");
+          return ce && atoi(ce) == 128;
+        }();
         int dev = 0;
         cudaGetDevice(&dev);
         int& per = slots[op - 4][wide][dev & 63];
