@@ -420,7 +420,7 @@ class _HostStager:
         # about 20 ms while the uploads run; tools/host_bw_probe.py)
         dst = stage.data_ptr() + lo * 2 * K * N * 4
         _lib.check(_lib.lib().hcnn_host_narrow(ptrs.ctypes.data, 2 * (hi - lo), K * N, _lib.C.c_void_p(dst),
-                                               min(16, os.cpu_count() or 1)), "hcnn_host_narrow")
+                                               _narrow_threads()), "hcnn_host_narrow")
 
     def _fill_numpy(self, stage, cts, lo, hi):
         arr = stage.numpy().view(np.uint32)
@@ -436,6 +436,13 @@ class _HostStager:
         cuts = np.linspace(lo, hi, min(hi - lo, 4 * nw) + 1).astype(np.int64)
         for f in [pool.submit(job, int(a), int(b)) for a, b in zip(cuts[:-1], cuts[1:])]:
             f.result()
+
+
+def _narrow_threads() -> int:
+    """host threads of the int64 -> u32 narrowing (HCNN_NARROW_THREADS, else
+    min(16, cores)); the narrowing is host-memory-bound"""
+    v = os.environ.get("HCNN_NARROW_THREADS")
+    return max(1, int(v)) if v else min(16, os.cpu_count() or 1)
 
 
 def _stager(g) -> _HostStager:
